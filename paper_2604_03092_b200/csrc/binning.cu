@@ -1,0 +1,351 @@
+// binning.cu — projection, depth order and tile binning.
+//
+//   k_project     per-surfel float64 projection (bit-exact with rasterizer.py:201-281),
+//                 64-B splat record, bbox, and an ORDER-PRESERVING compaction of the
+//                 on-screen surfels (chained scan, decoupled look-back) so the sort
+//                 input is in input-index order.
+//   k_radix_hist  digit histograms of all passes in one read.
+//   k_onesweep    one stable LSD radix pass (8-bit digits) with decoupled look-back.
+//   k_tie_fix     the depth key is the upper 32 bits of the float64 z; runs of equal
+//                 keys whose z differ in the low bits are re-sorted by (z64, index),
+//                 giving exactly the reference order lexsort((index, z))
+//                 (rasterizer.py:318-320).
+//   k_scan_emit   chained scan of per-surfel tile counts in depth order, fused with
+//                 pair emission: (tile id, surfel index) pairs come out in depth order,
+//                 so a stable sort on tile id alone yields per-tile depth-ordered lists.
+//   k_tile_ranges [start, end) of each tile in the sorted pair list.
+#include <cuda_fp16.h>
+
+#include "s2d_kernels.h"
+
+namespace s2d {
+
+namespace {
+
+constexpr uint32_t kFull = 0xffffffffu;
+
+// block-wide exclusive scan of one uint32 per thread (256 threads); returns exclusive
+// value, writes block total to *total.
+__device__ __forceinline__ uint32_t block_exclusive_scan_256(uint32_t v, uint32_t *smem8,
+                                                             uint32_t *total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) smem8[warp] = x;
+    __syncthreads();
+    uint32_t wsum = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+        const uint32_t t = smem8[w];
+        if (w < warp) wsum += t;
+        tot += t;
+    }
+    *total = tot;
+    return wsum + x - v;
+}
+
+// ------------------------------------------------------------------ projection
+
+__global__ void __launch_bounds__(kProjThreads) k_project(const ProjectArgs a) {
+    __shared__ int s_tile;
+    __shared__ uint32_t s_w[8];
+    __shared__ uint32_t s_base;
+    if (threadIdx.x == 0) s_tile = atomicAdd(a.ticket, 1);
+    __syncthreads();
+    const int tile = s_tile;
+    const int64_t i = (int64_t)tile * kProjThreads + threadIdx.x;
+    const ViewParams &P = a.P;
+    bool on = false, degen = false;
+    ExactProj e;
+    if (i < P.n) {
+        const ParamView pv(a.params, P.n);
+        project_exact(P, pv, i, e);
+        on = e.on_screen;
+        degen = e.in_front && !e.valid;
+        a.flags[i] = (uint8_t)((e.in_front ? 1 : 0) | (e.valid ? 2 : 0) | (on ? 4 : 0));
+        if (on) {
+            // M = J Bc (2x2), Minv = M^-1; Sigma = M M^T equals the reference cov2.
+            const double M00 = e.J[0][0] * e.Bc[0][0] + e.J[0][2] * e.Bc[2][0];
+            const double M01 = e.J[0][0] * e.Bc[0][1] + e.J[0][2] * e.Bc[2][1];
+            const double M10 = e.J[1][1] * e.Bc[1][0] + e.J[1][2] * e.Bc[2][0];
+            const double M11 = e.J[1][1] * e.Bc[1][1] + e.J[1][2] * e.Bc[2][1];
+            const double det = M00 * M11 - M01 * M10;
+            const double id = 1.0 / det;
+            SplatRecord r;
+            const float cxh = (float)e.cx, cyh = (float)e.cy;
+            const __half2 lo = __floats2half2_rn((float)(e.cx - (double)cxh), (float)(e.cy - (double)cyh));
+            r.q0 = make_float4(cxh, cyh, __uint_as_float(*reinterpret_cast<const uint32_t *>(&lo)),
+                               pv.opac[i]);
+            r.q1 = make_float4((float)(M11 * id), (float)(-M01 * id), (float)(-M10 * id), (float)(M00 * id));
+            r.q2 = make_float4(pv.colors[3 * i], pv.colors[3 * i + 1], pv.colors[3 * i + 2], (float)e.p[2]);
+            // camera-frame normal R_cw R(q)[:,2], oriented toward the camera (N1)
+            double nn[3];
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                nn[k] = P.r_cw[3 * k] * e.R[2] + P.r_cw[3 * k + 1] * e.R[5] + P.r_cw[3 * k + 2] * e.R[8];
+            const double sg = (nn[0] * e.p[0] + nn[1] * e.p[1] + nn[2] * e.p[2]) > 0.0 ? -1.0 : 1.0;
+            // guard band of the float32 Mahalanobis distance
+            const double kappa = sqrt(e.lmax / e.lmin);
+            const double gb = 4e-5 * kappa + 6e-6 / sqrt(e.lmin) + 4e-6;
+            r.q3 = make_float4((float)(sg * nn[0]), (float)(sg * nn[1]), (float)(sg * nn[2]), (float)gb);
+            a.rec[i] = r;
+            a.rect[i] = make_short4((short)e.x0, (short)e.x1, (short)e.y0, (short)e.y1);
+            a.z64[i] = e.p[2];
+        }
+    }
+    // degenerate count (rasterizer.py:244)
+    const uint32_t dm = __ballot_sync(kFull, degen);
+    if ((threadIdx.x & 31) == 0 && dm) atomicAdd(&a.stats->degenerate, __popc(dm));
+    // order-preserving compaction
+    uint32_t tot;
+    const uint32_t ex = block_exclusive_scan_256(on ? 1u : 0u, s_w, &tot);
+    if (threadIdx.x == 0) {
+        s_base = lookback_exclusive(a.status, 1, tile, tot);
+        const int ntiles = (int)((P.n + kProjThreads - 1) / kProjThreads);
+        if (tile == ntiles - 1) a.stats->visible = (int)(s_base + tot);
+    }
+    __syncthreads();
+    if (on) {
+        const uint32_t pos = s_base + ex;
+        a.keys[pos] = (uint32_t)((uint64_t)__double_as_longlong(e.p[2]) >> 32);
+        a.vals[pos] = (uint32_t)i;
+    }
+}
+
+// --------------------------------------------------------------- radix sorting
+
+__global__ void __launch_bounds__(256) k_radix_hist(const uint32_t *__restrict__ keys,
+                                                    const int *__restrict__ d_n, int passes,
+                                                    uint32_t *__restrict__ hist) {
+    __shared__ uint32_t sh[4 * kRadix];
+    for (int k = threadIdx.x; k < 4 * kRadix; k += blockDim.x) sh[k] = 0;
+    __syncthreads();
+    const int n = *d_n;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t k = keys[i];
+        for (int p = 0; p < passes; ++p) atomicAdd(&sh[p * kRadix + ((k >> (kRadixBits * p)) & (kRadix - 1))], 1u);
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < passes * kRadix; k += blockDim.x)
+        if (sh[k]) atomicAdd(&hist[k], sh[k]);
+}
+
+__global__ void __launch_bounds__(kSortThreads) k_onesweep(
+    const uint32_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint32_t *__restrict__ kout,
+    uint32_t *__restrict__ vout, const int *__restrict__ d_n, int shift,
+    const uint32_t *__restrict__ hist, uint32_t *status, int *ticket) {
+    __shared__ uint32_t s_wh[8][kRadix];
+    __shared__ uint32_t s_base[kRadix];
+    __shared__ uint32_t s_w[8];
+    __shared__ int s_tile;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_tile = atomicAdd(ticket, 1);
+#pragma unroll
+    for (int w = 0; w < 8; ++w) s_wh[w][tid] = 0;
+    __syncthreads();
+    const int tile = s_tile;
+    const int n = *d_n;
+    const int start = tile * kSortTile;
+    if (start >= n) return;
+    const int wbase = start + warp * 32 * kSortItems;
+    uint32_t key[kSortItems];
+    uint32_t pos[kSortItems];
+#pragma unroll
+    for (int r = 0; r < kSortItems; ++r) {
+        const int idx = wbase + r * 32 + lane;
+        key[r] = idx < n ? kin[idx] : 0u;
+    }
+    const uint32_t lt = lanemask_lt();
+#pragma unroll
+    for (int r = 0; r < kSortItems; ++r) {
+        const int idx = wbase + r * 32 + lane;
+        const bool valid = idx < n;
+        const uint32_t d = (key[r] >> shift) & (kRadix - 1);
+        const uint32_t peers = __match_any_sync(kFull, valid ? d : (kRadix + lane));
+        const uint32_t rank = __popc(peers & lt);
+        const uint32_t b = valid ? s_wh[warp][d] : 0u;
+        __syncwarp();
+        if (valid && rank == 0) s_wh[warp][d] = b + __popc(peers);
+        __syncwarp();
+        pos[r] = b + rank;
+    }
+    __syncthreads();
+    // per digit: exclusive over warps (warp-major = input order), block total
+    uint32_t run = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+        const uint32_t c = s_wh[w][tid];
+        s_wh[w][tid] = run;
+        run += c;
+    }
+    // global start of each digit (exclusive scan of the pass histogram)
+    uint32_t htot;
+    const uint32_t dstart = block_exclusive_scan_256(hist[tid], s_w, &htot);
+    const uint32_t prefix = lookback_exclusive(status + tid, kRadix, tile, run);
+    s_base[tid] = dstart + prefix;
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kSortItems; ++r) {
+        const int idx = wbase + r * 32 + lane;
+        if (idx < n) {
+            const uint32_t d = (key[r] >> shift) & (kRadix - 1);
+            const uint32_t o = s_base[d] + s_wh[warp][d] + pos[r];
+            kout[o] = key[r];
+            vout[o] = vin[idx];
+        }
+    }
+}
+
+// Runs of equal (upper-32-bit) depth keys: restore (z64, index) order.
+__global__ void __launch_bounds__(256) k_tie_fix(const uint32_t *__restrict__ keys,
+                                                 uint32_t *vals, const double *__restrict__ z64,
+                                                 const int *__restrict__ d_n, uint32_t *claim) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    const int n = *d_n;
+    if (r <= 0 || r >= n) return;
+    const uint32_t k = keys[r];
+    if (keys[r - 1] != k) return;
+    const uint32_t a = vals[r - 1], b = vals[r];
+    const double za = z64[a], zb = z64[b];
+    if (!(za > zb || (za == zb && a > b))) return;
+    int s = r - 1;
+    while (s > 0 && keys[s - 1] == k) --s;
+    if (atomicExch(&claim[s], 1u) != 0u) return;
+    int e = r + 1;
+    while (e < n && keys[e] == k) ++e;
+    for (int j = s + 1; j < e; ++j) {
+        const uint32_t v = vals[j];
+        const double zv = z64[v];
+        int t = j - 1;
+        while (t >= s) {
+            const uint32_t u = vals[t];
+            const double zu = z64[u];
+            if (zu > zv || (zu == zv && u > v)) {
+                vals[t + 1] = u;
+                --t;
+            } else {
+                break;
+            }
+        }
+        vals[t + 1] = v;
+    }
+}
+
+// ----------------------------------------------------------- scan + emission
+
+__global__ void __launch_bounds__(256) k_scan_emit(const EmitArgs a) {
+    __shared__ int s_tile;
+    __shared__ uint32_t s_w[8];
+    __shared__ uint32_t s_base;
+    __shared__ uint32_t s_hist[2 * kRadix];
+    const int tid = threadIdx.x;
+    if (tid == 0) s_tile = atomicAdd(a.ticket, 1);
+    for (int k = tid; k < 2 * kRadix; k += 256) s_hist[k] = 0;
+    __syncthreads();
+    const int tile = s_tile;
+    const int nv = *a.d_v;
+    const int start = tile * kEmitTile;
+    if (start >= nv) return;
+    const int r0 = start + tid * kEmitItems;
+    uint32_t ids[kEmitItems];
+    short4 rc[kEmitItems];
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int j = 0; j < kEmitItems; ++j) {
+        const int r = r0 + j;
+        ids[j] = r < nv ? a.order[r] : 0u;
+        rc[j] = r < nv ? a.rect[ids[j]] : make_short4(1, 0, 1, 0);
+        const int tx0 = rc[j].x >> 4, tx1 = rc[j].y >> 4, ty0 = rc[j].z >> 4, ty1 = rc[j].w >> 4;
+        if (rc[j].x <= rc[j].y && rc[j].z <= rc[j].w) cnt += (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
+    }
+    uint32_t tot;
+    const uint32_t ex = block_exclusive_scan_256(cnt, s_w, &tot);
+    if (tid == 0) {
+        s_base = lookback_exclusive(a.status, 1, tile, tot);
+        const int ntiles = (nv + kEmitTile - 1) / kEmitTile;
+        if (tile == ntiles - 1) {
+            const uint32_t total = s_base + tot;
+            a.stats->pairs = (int)total;
+            a.stats->pairs_stored = (int)(total < a.pcap ? total : a.pcap);
+            if (total > a.pcap) a.stats->overflow = 1;
+        }
+    }
+    __syncthreads();
+    uint32_t off = s_base + ex;
+#pragma unroll
+    for (int j = 0; j < kEmitItems; ++j) {
+        if (!(rc[j].x <= rc[j].y && rc[j].z <= rc[j].w)) continue;
+        const int tx0 = rc[j].x >> 4, tx1 = rc[j].y >> 4, ty0 = rc[j].z >> 4, ty1 = rc[j].w >> 4;
+        for (int ty = ty0; ty <= ty1; ++ty)
+            for (int tx = tx0; tx <= tx1; ++tx) {
+                const uint32_t t = (uint32_t)(ty * a.ntx + tx);
+                if (off < a.pcap) {
+                    a.pkeys[off] = t;
+                    a.pvals[off] = ids[j];
+                }
+                ++off;
+                atomicAdd(&s_hist[t & (kRadix - 1)], 1u);
+                if (a.pair_passes > 1) atomicAdd(&s_hist[kRadix + ((t >> kRadixBits) & (kRadix - 1))], 1u);
+            }
+    }
+    __syncthreads();
+    for (int k = tid; k < a.pair_passes * kRadix; k += 256)
+        if (s_hist[k]) atomicAdd(&a.pair_hist[k], s_hist[k]);
+}
+
+__global__ void __launch_bounds__(256) k_tile_ranges(const uint32_t *__restrict__ pkeys,
+                                                     const int *__restrict__ d_p, uint32_t pcap,
+                                                     int2 *ranges) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    int np = *d_p;
+    if ((uint32_t)np > pcap) return;  // overflow: leave all tiles empty
+    if (i >= np) return;
+    const uint32_t k = pkeys[i];
+    if (i == 0 || pkeys[i - 1] != k) ranges[k].x = i;
+    if (i == np - 1 || pkeys[i + 1] != k) ranges[k].y = i + 1;
+}
+
+}  // namespace
+
+void launch_project(const ProjectArgs &a, cudaStream_t s) {
+    const int blocks = (int)((a.P.n + kProjThreads - 1) / kProjThreads);
+    if (blocks > 0) k_project<<<blocks, kProjThreads, 0, s>>>(a);
+}
+
+void launch_radix_hist(const uint32_t *keys, const int *d_n, int cap, int passes, uint32_t *hist,
+                       cudaStream_t s) {
+    int blocks = (cap + 255) / 256;
+    if (blocks > 592) blocks = 592;
+    if (blocks < 1) blocks = 1;
+    k_radix_hist<<<blocks, 256, 0, s>>>(keys, d_n, passes, hist);
+}
+
+void launch_onesweep(const uint32_t *kin, const uint32_t *vin, uint32_t *kout, uint32_t *vout,
+                     const int *d_n, int cap, int shift, const uint32_t *hist_pass,
+                     uint32_t *status, int *ticket, cudaStream_t s) {
+    const int blocks = (cap + kSortTile - 1) / kSortTile;
+    if (blocks > 0) k_onesweep<<<blocks, kSortThreads, 0, s>>>(kin, vin, kout, vout, d_n, shift, hist_pass, status, ticket);
+}
+
+void launch_tie_fix(const uint32_t *keys, uint32_t *vals, const double *z64, const int *d_n, int cap,
+                    uint32_t *claim, cudaStream_t s) {
+    const int blocks = (cap + 255) / 256;
+    if (blocks > 0) k_tie_fix<<<blocks, 256, 0, s>>>(keys, vals, z64, d_n, claim);
+}
+
+void launch_scan_emit(const EmitArgs &a, cudaStream_t s) {
+    const int blocks = (a.cap_v + kEmitTile - 1) / kEmitTile;
+    if (blocks > 0) k_scan_emit<<<blocks, 256, 0, s>>>(a);
+}
+
+void launch_tile_ranges(const uint32_t *pkeys, const int *d_p, uint32_t pcap, int2 *ranges,
+                        cudaStream_t s) {
+    const int blocks = (int)((pcap + 255) / 256);
+    if (blocks > 0) k_tile_ranges<<<blocks, 256, 0, s>>>(pkeys, d_p, pcap, ranges);
+}
+
+}  // namespace s2d

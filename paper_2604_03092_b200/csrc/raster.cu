@@ -1,0 +1,526 @@
+// raster.cu — per-tile front-to-back compositing and its reverse-order backward
+// (SURVEY.md §8(a) A7-A9, N1-N3).
+//
+// One 256-thread CTA per 16x16 tile.  Warp w owns an 8x4 pixel block
+// (2 columns x 4 rows of warps); lane l owns pixel (l & 7, l >> 3) of it.
+// The tile's depth-ordered list is staged 256 records at a time into shared
+// memory with cp.async (double buffered, ids prefetched two batches ahead).
+// Each warp then ballots which staged records' integer bboxes touch its 8x4
+// block and walks only those, in list order, so per-pixel work is spent on
+// in-bbox pairs instead of the whole tile list.  A warp stops when every lane's
+// transmittance is below the termination threshold (ballot), the CTA when all
+// warps have (barrier count).
+//
+// Semantics follow blend_forward (_raster_kernels.py:22-55) exactly: the
+// termination test precedes blending, pixel (row y, col x) samples (x, y),
+// the Mahalanobis cut is `m > sigma^2` on the integer bbox, weights clamp at
+// weight_clamp, `w <= 0` skips.  m and the weight clamp are evaluated in
+// float32; inside a per-surfel guard band around the cut and around the clamp
+// the decision is re-taken in float64 with the reference's formula, so the
+// set of blended pairs equals the reference's.
+#include <cuda_fp16.h>
+
+#include "s2d_kernels.h"
+
+namespace s2d {
+
+namespace {
+
+constexpr uint32_t kFull = 0xffffffffu;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void cp_async16(void *smem, const void *g) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void *smem, const void *g) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Reference Mahalanobis distance of pixel (x, y) to surfel `id`, float64 (guard band path).
+__device__ __noinline__ double exact_m_at(const ViewParams &P, const float *params, uint32_t id,
+                                          int x, int y) {
+    const ParamView pv(params, P.n);
+    ExactProj e;
+    project_exact(P, pv, id, e);
+    return exact_maha(e, x, y);
+}
+
+struct Stage {
+    SplatRecord rec[2][kRasterThreads];
+    short4 rect[2][kRasterThreads];
+    uint32_t id[2][kRasterThreads];
+};
+
+__device__ __forceinline__ void stage_issue(Stage &st, int buf, int k, uint32_t id, bool valid,
+                                            const SplatRecord *rec, const short4 *rect) {
+    if (valid) {
+        const float4 *g = reinterpret_cast<const float4 *>(rec + id);
+        float4 *d = reinterpret_cast<float4 *>(&st.rec[buf][k]);
+        cp_async16(d + 0, g + 0);
+        cp_async16(d + 1, g + 1);
+        cp_async16(d + 2, g + 2);
+        cp_async16(d + 3, g + 3);
+        cp_async8(&st.rect[buf][k], rect + id);
+    }
+    st.id[buf][k] = id;
+}
+
+// Per-pixel evaluation shared by forward and backward (must make identical decisions).
+// Returns false if the pair does not blend.  Outputs m-space intermediates.
+struct PairEval {
+    float dx, dy, u, v, g, w;
+    bool clamped;
+};
+
+__device__ __forceinline__ bool eval_pair(const ViewParams &P, const float *params, const SplatRecord &r,
+                                          const short4 &bb, uint32_t id, int px, int py, PairEval &o,
+                                          int &guard_hits) {
+    if (px < bb.x || px > bb.y || py < bb.z || py > bb.w) return false;
+    const uint32_t lob = __float_as_uint(r.q0.z);
+    const __half2 lo = *reinterpret_cast<const __half2 *>(&lob);
+    // explicit round-to-nearest intrinsics: forward and backward must take
+    // bit-identical decisions, so nothing here may be contracted differently
+    o.dx = __fsub_rn(__fsub_rn((float)px, r.q0.x), __low2float(lo));
+    o.dy = __fsub_rn(__fsub_rn((float)py, r.q0.y), __high2float(lo));
+    o.u = __fmaf_rn(r.q1.x, o.dx, __fmul_rn(r.q1.y, o.dy));
+    o.v = __fmaf_rn(r.q1.z, o.dx, __fmul_rn(r.q1.w, o.dy));
+    const float m = __fmaf_rn(o.u, o.u, __fmul_rn(o.v, o.v));
+    const float gb = r.q3.w;
+    if (m > P.maha_cut_f + gb) return false;
+    double m64 = -1.0;
+    if (m >= P.maha_cut_f - gb) {
+        ++guard_hits;
+        m64 = exact_m_at(P, params, id, px, py);
+        if (m64 > P.maha_cut) return false;
+    }
+    o.g = __expf(__fmul_rn(-0.5f, m));
+    float w = __fmul_rn(r.q0.w, o.g);
+    o.clamped = false;
+    if (fabsf(w - P.w_clamp_f) <= 4e-6f) {
+        ++guard_hits;
+        if (m64 < 0.0) m64 = exact_m_at(P, params, id, px, py);
+        o.clamped = (double)r.q0.w * exp(-0.5 * m64) > P.w_clamp;
+    } else {
+        o.clamped = w > P.w_clamp_f;
+    }
+    if (o.clamped) w = P.w_clamp_f;
+    o.w = w;
+    return w > 0.0f;
+}
+
+template <bool kArg, bool kMaxW>
+__global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(const RasterArgs a) {
+    __shared__ Stage st;
+    const ViewParams &P = a.P;
+    const int tile = blockIdx.x;
+    const int tx = tile % P.ntx, ty = tile / P.ntx;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int wx0 = tx * kTile + (warp & 1) * 8, wy0 = ty * kTile + (warp >> 1) * 4;
+    const int wx1 = min(wx0 + 7, P.W - 1), wy1 = min(wy0 + 3, P.H - 1);
+    const int px = wx0 + (lane & 7), py = wy0 + (lane >> 3);
+    const bool inside = px < P.W && py < P.H;
+    const int2 rg = a.ranges[tile];
+    const int cnt = rg.y - rg.x;
+
+    float T = 1.0f, Tpre = 1.0f;
+    float c0 = 0.f, c1 = 0.f, c2 = 0.f, dep = 0.f, n0 = 0.f, n1 = 0.f, n2 = 0.f;
+    float maxw = 0.f;
+    int argw = -1, last = -1, guard = 0;
+    bool done = !inside || (T < P.term_t_f);
+    const float term_t = P.term_t_f;
+
+    const int nb = (cnt + kRasterThreads - 1) / kRasterThreads;
+    if (nb > 0) {
+        uint32_t id_next = tid < cnt ? a.pair_ids[rg.x + tid] : 0u;
+        stage_issue(st, 0, tid, id_next, tid < cnt, a.rec, a.rect);
+        cp_commit();
+        id_next = (kRasterThreads + tid < cnt) ? a.pair_ids[rg.x + kRasterThreads + tid] : 0u;
+        for (int b = 0; b < nb; ++b) {
+            const int buf = b & 1;
+            if (b + 1 < nb) {
+                const int k1 = (b + 1) * kRasterThreads + tid;
+                stage_issue(st, buf ^ 1, tid, id_next, k1 < cnt, a.rec, a.rect);
+                const int k2 = (b + 2) * kRasterThreads + tid;
+                id_next = k2 < cnt ? a.pair_ids[rg.x + k2] : 0u;
+            }
+            cp_commit();
+            cp_wait<1>();
+            __syncthreads();
+            const int base = b * kRasterThreads;
+            const int nrec = min(kRasterThreads, cnt - base);
+            if (!__all_sync(kFull, done)) {
+                uint32_t mask[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int k = q * 32 + lane;
+                    bool hit = false;
+                    if (k < nrec) {
+                        const short4 r = st.rect[buf][k];
+                        hit = (r.x <= wx1) & (r.y >= wx0) & (r.z <= wy1) & (r.w >= wy0);
+                    }
+                    mask[q] = __ballot_sync(kFull, hit);
+                }
+#pragma unroll 1
+                for (int q = 0; q < 8; ++q) {
+                    uint32_t m = mask[q];
+                    while (m) {
+                        const int k = q * 32 + __ffs(m) - 1;
+                        m &= m - 1;
+                        const uint32_t id = st.id[buf][k];
+                        float contrib = 0.f;
+                        if (!done) {
+                            PairEval e;
+                            const SplatRecord &r = st.rec[buf][k];
+                            if (eval_pair(P, a.params, r, st.rect[buf][k], id, px, py, e, guard)) {
+                                contrib = e.w * T;
+                                const float4 q2 = r.q2, q3 = r.q3;
+                                c0 = fmaf(contrib, q2.x, c0);
+                                c1 = fmaf(contrib, q2.y, c1);
+                                c2 = fmaf(contrib, q2.z, c2);
+                                dep = fmaf(contrib, q2.w, dep);
+                                n0 = fmaf(contrib, q3.x, n0);
+                                n1 = fmaf(contrib, q3.y, n1);
+                                n2 = fmaf(contrib, q3.z, n2);
+                                if (kArg && contrib > maxw) {
+                                    maxw = contrib;
+                                    argw = (int)id;
+                                }
+                                Tpre = T;
+                                T = T * (1.0f - e.w);
+                                last = rg.x + base + k;
+                                done = T < term_t;
+                            }
+                        }
+                        if (kMaxW) {
+                            float mx = contrib;
+                            float mm = (a.mask != nullptr && inside && a.mask[py * P.W + px]) ? contrib : 0.f;
+#pragma unroll
+                            for (int o = 16; o > 0; o >>= 1) {
+                                mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
+                                mm = fmaxf(mm, __shfl_xor_sync(kFull, mm, o));
+                            }
+                            if (lane == 0) {
+                                if (mx > 0.f) atomicMax(reinterpret_cast<int *>(a.max_all + id), __float_as_int(mx));
+                                if (mm > 0.f && a.max_marked)
+                                    atomicMax(reinterpret_cast<int *>(a.max_marked + id), __float_as_int(mm));
+                            }
+                        }
+                        if (__all_sync(kFull, done)) {
+                            m = 0;
+                            q = 8;
+                        }
+                    }
+                }
+            }
+            if (__syncthreads_and(done)) break;
+        }
+        cp_wait<0>();
+    }
+    if (inside) {
+        const int p = py * P.W + px;
+        if (a.color) {
+            a.color[3 * p] = c0;
+            a.color[3 * p + 1] = c1;
+            a.color[3 * p + 2] = c2;
+        }
+        if (a.depth) a.depth[p] = dep;
+        if (a.accum) a.accum[p] = 1.0f - T;
+        if (a.normal) {
+            a.normal[3 * p] = n0;
+            a.normal[3 * p + 1] = n1;
+            a.normal[3 * p + 2] = n2;
+        }
+        if (kArg) {
+            if (a.max_w) a.max_w[p] = maxw;
+            if (a.arg_w) a.arg_w[p] = argw;
+        }
+        a.aux[p] = make_int2(last, __float_as_int(Tpre));
+    }
+    const int nm = __syncthreads_count(inside && (1.0f - T) > 0.5f);
+    int gsum = guard;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) gsum += __shfl_xor_sync(kFull, gsum, o);
+    if (lane == 0 && gsum) atomicAdd(&a.stats->guard_hits, gsum);
+    if (tid == 0 && nm) atomicAdd(&a.stats->n_mask, nm);
+}
+
+// 16 values per lane -> lane l (l even or odd) holds the warp sum of value (l >> 1).
+__device__ __forceinline__ float warp_reduce16(float (&v)[16], int lane) {
+    {
+        const bool up = lane & 16;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const float send = up ? v[j] : v[j + 8];
+            const float keep = up ? v[j + 8] : v[j];
+            v[j] = keep + __shfl_xor_sync(kFull, send, 16);
+        }
+    }
+    {
+        const bool up = lane & 8;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float send = up ? v[j] : v[j + 4];
+            const float keep = up ? v[j + 4] : v[j];
+            v[j] = keep + __shfl_xor_sync(kFull, send, 8);
+        }
+    }
+    {
+        const bool up = lane & 4;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const float send = up ? v[j] : v[j + 2];
+            const float keep = up ? v[j + 2] : v[j];
+            v[j] = keep + __shfl_xor_sync(kFull, send, 4);
+        }
+    }
+    {
+        const bool up = lane & 2;
+        const float send = up ? v[0] : v[1];
+        const float keep = up ? v[1] : v[0];
+        v[0] = keep + __shfl_xor_sync(kFull, send, 2);
+    }
+    return v[0] + __shfl_xor_sync(kFull, v[0], 1);
+}
+
+__device__ __forceinline__ float sgnf(float x) { return x > 0.f ? 1.f : (x < 0.f ? -1.f : 0.f); }
+
+__global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(const RasterArgs a) {
+    __shared__ Stage st;
+    __shared__ int s_lmax[8];
+    __shared__ float s_loss[8];
+    const ViewParams &P = a.P;
+    const int tile = blockIdx.x;
+    const int tx = tile % P.ntx, ty = tile / P.ntx;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int wx0 = tx * kTile + (warp & 1) * 8, wy0 = ty * kTile + (warp >> 1) * 4;
+    const int wx1 = min(wx0 + 7, P.W - 1), wy1 = min(wy0 + 3, P.H - 1);
+    const int px = wx0 + (lane & 7), py = wy0 + (lane >> 3);
+    const bool inside = px < P.W && py < P.H;
+    const int2 rg = a.ranges[tile];
+    const int p = py * P.W + px;
+
+    // ---- loss seeds (rasterizer.py:375-380 for MSE; L1; external) ----
+    float gc0 = 0.f, gc1 = 0.f, gc2 = 0.f, gd = 0.f, gn0 = 0.f, gn1 = 0.f, gn2 = 0.f, ga = 0.f;
+    float lpx = 0.f;
+    int last = -1;
+    float Tlast = 1.f;
+    if (inside) {
+        const int2 ax = a.aux[p];
+        last = ax.x;
+        Tlast = __int_as_float(ax.y);
+        const double npx = (double)P.W * (double)P.H;
+        if (a.loss_kind == S2D_LOSS_EXTERNAL) {
+            if (a.d_color) {
+                gc0 = a.d_color[3 * p];
+                gc1 = a.d_color[3 * p + 1];
+                gc2 = a.d_color[3 * p + 2];
+            }
+            if (a.d_depth) gd = a.d_depth[p];
+            if (a.d_normal) {
+                gn0 = a.d_normal[3 * p];
+                gn1 = a.d_normal[3 * p + 1];
+                gn2 = a.d_normal[3 * p + 2];
+            }
+            if (a.d_accum) ga = a.d_accum[p];
+        } else {
+            const float e0 = a.color[3 * p] - a.target_rgb[3 * p];
+            const float e1 = a.color[3 * p + 1] - a.target_rgb[3 * p + 1];
+            const float e2 = a.color[3 * p + 2] - a.target_rgb[3 * p + 2];
+            const float ed = a.depth[p] - a.target_depth[p];
+            const int nm = a.stats->n_mask;
+            const bool masked = a.accum[p] > 0.5f;
+            if (a.loss_kind == S2D_LOSS_MSE) {
+                const float k = (float)(a.w_rgb * (2.0 / (3.0 * npx)));
+                gc0 = k * e0;
+                gc1 = k * e1;
+                gc2 = k * e2;
+                lpx = (float)(a.w_rgb / (3.0 * npx)) * (e0 * e0 + e1 * e1 + e2 * e2);
+                if (a.w_depth != 0.0 && nm > 0 && masked) {
+                    gd = (float)(a.w_depth * (2.0 / nm)) * ed;
+                    lpx += (float)(a.w_depth / nm) * ed * ed;
+                }
+            } else {  // L1
+                const float k = (float)(a.w_rgb / (3.0 * npx));
+                gc0 = k * sgnf(e0);
+                gc1 = k * sgnf(e1);
+                gc2 = k * sgnf(e2);
+                lpx = k * (fabsf(e0) + fabsf(e1) + fabsf(e2));
+                const bool use = a.depth_mask ? masked : true;
+                const double nd = a.depth_mask ? (double)nm : npx;
+                if (use && nd > 0.0) {
+                    const float kd = (float)(a.w_depth / nd);
+                    gd = kd * sgnf(ed);
+                    lpx += kd * fabsf(ed);
+                }
+            }
+        }
+    }
+    // block reductions: loss, max(last)
+    {
+        float l = lpx;
+        int lm = last;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            l += __shfl_xor_sync(kFull, l, o);
+            lm = max(lm, __shfl_xor_sync(kFull, lm, o));
+        }
+        if (lane == 0) {
+            s_loss[warp] = l;
+            s_lmax[warp] = lm;
+        }
+    }
+    __syncthreads();
+    int lmax = -1;
+    int wlast = s_lmax[warp];
+    if (tid == 0 && a.loss_accum) {
+        float l = 0.f;
+        for (int w = 0; w < 8; ++w) l += s_loss[w];
+        if (l != 0.f) atomicAdd(a.loss_accum, (double)l);
+    }
+#pragma unroll
+    for (int w = 0; w < 8; ++w) lmax = max(lmax, s_lmax[w]);
+    if (lmax < rg.x) return;  // nothing blended in this tile (uniform)
+
+    // ---- reverse traversal ----
+    float Tn = Tlast;          // transmittance before the later contributor
+    bool first = true;
+    float R = 1.f;             // prod_{j later} (1 - w_j)
+    float S0 = 0.f, S1 = 0.f, S2 = 0.f, Sd = 0.f, Sn0 = 0.f, Sn1 = 0.f, Sn2 = 0.f;
+    int guard = 0;
+    const int cnt = lmax + 1 - rg.x;   // list prefix that matters
+    const int nb = (cnt + kRasterThreads - 1) / kRasterThreads;
+    // batch b covers list positions [rg.x + b*256, ...); traverse b = nb-1 .. 0
+    {
+        int b = nb - 1;
+        int k0 = b * kRasterThreads + tid;
+        uint32_t id0 = k0 < cnt ? a.pair_ids[rg.x + k0] : 0u;
+        stage_issue(st, b & 1, tid, id0, k0 < cnt, a.rec, a.rect);
+        cp_commit();
+        int kn = (b - 1) * kRasterThreads + tid;
+        uint32_t id_next = (b >= 1) ? a.pair_ids[rg.x + kn] : 0u;
+        for (; b >= 0; --b) {
+            const int buf = b & 1;
+            if (b >= 1) {
+                stage_issue(st, buf ^ 1, tid, id_next, true, a.rec, a.rect);
+                const int k2 = (b - 2) * kRasterThreads + tid;
+                id_next = (b >= 2) ? a.pair_ids[rg.x + k2] : 0u;
+            }
+            cp_commit();
+            cp_wait<1>();
+            __syncthreads();
+            const int base = b * kRasterThreads;
+            const int nrec = min(kRasterThreads, cnt - base);
+            uint32_t mask[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int k = q * 32 + lane;
+                bool hit = false;
+                if (k < nrec && rg.x + base + k <= wlast) {
+                    const short4 r = st.rect[buf][k];
+                    hit = (r.x <= wx1) & (r.y >= wx0) & (r.z <= wy1) & (r.w >= wy0);
+                }
+                mask[q] = __ballot_sync(kFull, hit);
+            }
+#pragma unroll 1
+            for (int q = 7; q >= 0; --q) {
+                uint32_t m = mask[q];
+                while (m) {
+                    const int bit = 31 - __clz(m);
+                    m &= ~(1u << bit);
+                    const int k = q * 32 + bit;
+                    const int pos = rg.x + base + k;
+                    const uint32_t id = st.id[buf][k];
+                    float v[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) v[j] = 0.f;
+                    bool contrib = false;
+                    if (pos <= last) {
+                        PairEval e;
+                        const SplatRecord &r = st.rec[buf][k];
+                        if (eval_pair(P, a.params, r, st.rect[buf][k], id, px, py, e, guard)) {
+                            contrib = true;
+                            const float4 q1 = r.q1, q2 = r.q2, q3 = r.q3;
+                            float Ti;
+                            if (first) {
+                                Ti = Tlast;
+                                first = false;
+                            } else {
+                                Ti = Tn / (1.0f - e.w);
+                            }
+                            Tn = Ti;
+                            const float alpha = e.w * Ti;
+                            v[1] = gc0 * alpha;
+                            v[2] = gc1 * alpha;
+                            v[3] = gc2 * alpha;
+                            v[4] = gd * alpha;
+                            v[5] = gn0 * alpha;
+                            v[6] = gn1 * alpha;
+                            v[7] = gn2 * alpha;
+                            // dL/dw = T_i [ G.(c - S) + gd (z - Sd) + Gn.(n - Sn) ] + ga T_i R
+                            float dLdw = gc0 * (q2.x - S0) + gc1 * (q2.y - S1) + gc2 * (q2.z - S2) +
+                                         gd * (q2.w - Sd) + gn0 * (q3.x - Sn0) + gn1 * (q3.y - Sn1) +
+                                         gn2 * (q3.z - Sn2) + ga * R;
+                            dLdw *= Ti;
+                            if (!e.clamped) {
+                                v[0] = dLdw * e.g;
+                                const float gm = -0.5f * e.w * dLdw;  // dL/dm
+                                const float gu = 2.f * gm * e.u, gv = 2.f * gm * e.v;
+                                v[8] = gu * e.dx;
+                                v[9] = gu * e.dy;
+                                v[10] = gv * e.dx;
+                                v[11] = gv * e.dy;
+                                v[12] = -(gu * q1.x + gv * q1.z);
+                                v[13] = -(gu * q1.y + gv * q1.w);
+                            }
+                            const float omw = 1.0f - e.w;
+                            S0 = e.w * q2.x + omw * S0;
+                            S1 = e.w * q2.y + omw * S1;
+                            S2 = e.w * q2.z + omw * S2;
+                            Sd = e.w * q2.w + omw * Sd;
+                            Sn0 = e.w * q3.x + omw * Sn0;
+                            Sn1 = e.w * q3.y + omw * Sn1;
+                            Sn2 = e.w * q3.z + omw * Sn2;
+                            R *= omw;
+                        }
+                    }
+                    if (__any_sync(kFull, contrib)) {
+                        const float s = warp_reduce16(v, lane);
+                        if (!(lane & 1) && lane < 28 && s != 0.f) atomicAdd(a.grad2d + (size_t)id * 16 + (lane >> 1), s);
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        cp_wait<0>();
+    }
+    int gsum = guard;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) gsum += __shfl_xor_sync(kFull, gsum, o);
+    if (lane == 0 && gsum) atomicAdd(&a.stats->guard_hits, gsum);
+}
+
+}  // namespace
+
+void launch_raster_forward(const RasterArgs &a, cudaStream_t s) {
+    const int tiles = a.P.ntx * a.P.nty;
+    const bool arg = a.max_w != nullptr || a.arg_w != nullptr;
+    const bool mw = a.max_all != nullptr;
+    if (arg && mw) k_raster_fwd<true, true><<<tiles, kRasterThreads, 0, s>>>(a);
+    else if (arg) k_raster_fwd<true, false><<<tiles, kRasterThreads, 0, s>>>(a);
+    else if (mw) k_raster_fwd<false, true><<<tiles, kRasterThreads, 0, s>>>(a);
+    else k_raster_fwd<false, false><<<tiles, kRasterThreads, 0, s>>>(a);
+}
+
+void launch_raster_backward(const RasterArgs &a, cudaStream_t s) {
+    const int tiles = a.P.ntx * a.P.nty;
+    k_raster_bwd<<<tiles, kRasterThreads, 0, s>>>(a);
+}
+
+}  // namespace s2d

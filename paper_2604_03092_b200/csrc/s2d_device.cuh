@@ -1,0 +1,260 @@
+// s2d_device.cuh — device-side data layout and the exact float64 projection.
+//
+// Every per-surfel geometry quantity that decides WHICH pixels a surfel
+// touches and in WHICH order (z, centre, inverse covariance, integer bbox,
+// validity) is evaluated in float64 with the reference's operation order,
+// using round-to-nearest intrinsics (__dmul_rn/__dadd_rn/...) that the
+// compiler never contracts.  This makes z, centres, bbox, on-screen flags and
+// hence the depth order and tile lists bit-identical to the reference
+// (rasterizer.py:201-281, 318-320).  Per-pixel blending then runs in float32
+// with float64 re-checks inside guard bands (see raster.cu).
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace s2d {
+
+constexpr int kTile = 16;          // 16x16 pixel tiles, one CTA each
+constexpr int kRasterThreads = 256;
+
+// Per-view constants, passed by value as a kernel parameter.
+struct ViewParams {
+    double inv[8];   // pk_inverse(pose) = [s_inv, t_inv(3), q_inv(4)]  (geometry.py:188-195)
+    double m_cw[9];  // inv[0] * quat_to_matrix(q_inv)                  (rasterizer.py:214)
+    double r_cw[9];  // quat_to_matrix(q_inv) (rotation only; normals)
+    double fx, fy, cx, cy;
+    double near_plane, tan_max, max_cond, sigma;
+    double mx, my, wmax, hmax;  // centre-margin gate (rasterizer.py:231-236)
+    double wm1, hm1;            // W-1, H-1 (rasterizer.py:278-279)
+    double w_clamp, maha_cut;   // 0.999, sigma^2
+    float w_clamp_f, term_t_f, maha_cut_f;
+    int W, H, ntx, nty;
+    int64_t n;
+};
+
+// 64-byte splat record, one per on-screen surfel, indexed by input index.
+//   q0: cx_hi, cy_hi, half2(cx_lo, cy_lo) bits, opacity
+//   q1: Minv = (A, B, C, D): (u, v) = (A dx + B dy, C dx + D dy), m = u^2 + v^2
+//   q2: r, g, b, z
+//   q3: nx, ny, nz, guard band of m around the 3-sigma cut
+struct __align__(16) SplatRecord {
+    float4 q0, q1, q2, q3;
+};
+
+// ---------------------------------------------------------------- exact ops
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ double dfma(double a, double b, double c) { return __fma_rn(a, b, c); }
+
+// numpy float64 -> int64 cast on x86-64 (cvttsd2si): NaN / out of range -> INT64_MIN
+__device__ __forceinline__ int64_t f2i_x86(double v) {
+    if (!(v > -9223372036854775808.0 && v < 9223372036854775808.0)) return INT64_MIN;
+    return (int64_t)v;
+}
+__device__ __forceinline__ int64_t clip64(int64_t v, int64_t lo, int64_t hi) {
+    return v < lo ? lo : (v > hi ? hi : v);
+}
+
+// quat_rotate (geometry.py:59-64), numpy.cross association
+__device__ __forceinline__ void quat_rotate_exact(const double q[4], const double v[3], double o[3]) {
+    const double w = q[0], u0 = q[1], u1 = q[2], u2 = q[3];
+    const double uv0 = dsub(dmul(u1, v[2]), dmul(u2, v[1]));
+    const double uv1 = dsub(dmul(u2, v[0]), dmul(u0, v[2]));
+    const double uv2 = dsub(dmul(u0, v[1]), dmul(u1, v[0]));
+    const double uu0 = dsub(dmul(u1, uv2), dmul(u2, uv1));
+    const double uu1 = dsub(dmul(u2, uv0), dmul(u0, uv2));
+    const double uu2 = dsub(dmul(u0, uv1), dmul(u1, uv0));
+    o[0] = dadd(v[0], dmul(2.0, dadd(dmul(w, uv0), uu0)));
+    o[1] = dadd(v[1], dmul(2.0, dadd(dmul(w, uv1), uu1)));
+    o[2] = dadd(v[2], dmul(2.0, dadd(dmul(w, uv2), uu2)));
+}
+
+// quat_to_matrix (geometry.py:132-142), raw quaternion
+__device__ __forceinline__ void quat_to_matrix_exact(const double q[4], double r[9]) {
+    const double w = q[0], x = q[1], y = q[2], z = q[3];
+    r[0] = dsub(1.0, dmul(2.0, dadd(dmul(y, y), dmul(z, z))));
+    r[1] = dmul(2.0, dsub(dmul(x, y), dmul(w, z)));
+    r[2] = dmul(2.0, dadd(dmul(x, z), dmul(w, y)));
+    r[3] = dmul(2.0, dadd(dmul(x, y), dmul(w, z)));
+    r[4] = dsub(1.0, dmul(2.0, dadd(dmul(x, x), dmul(z, z))));
+    r[5] = dmul(2.0, dsub(dmul(y, z), dmul(w, x)));
+    r[6] = dmul(2.0, dsub(dmul(x, z), dmul(w, y)));
+    r[7] = dmul(2.0, dadd(dmul(y, z), dmul(w, x)));
+    r[8] = dsub(1.0, dmul(2.0, dadd(dmul(x, x), dmul(y, y))));
+}
+
+// Packed parameter block accessors: [means 3n | quats 4n | scales 2n | opac n | colors 3n]
+struct ParamView {
+    const float *means, *quats, *scales, *opac, *colors;
+    __host__ __device__ ParamView(const float *base, int64_t n)
+        : means(base), quats(base + 3 * n), scales(base + 7 * n), opac(base + 9 * n),
+          colors(base + 10 * n) {}
+};
+
+struct ExactProj {
+    double p[3];        // camera-frame mean
+    double R[9];        // quat_to_matrix(q)
+    double Bc[3][2];    // basis_cam
+    double J[2][3];     // projection Jacobian at p
+    double a, b, c;     // cov2
+    double cx, cy;      // pixel centre
+    double ia, ib, ic;  // inv_abc
+    double lmin, lmax;
+    double rx, ry;
+    int64_t x0, x1, y0, y1;
+    bool in_front, valid, on_screen;
+};
+
+// _project_batch (rasterizer.py:201-249) + _footprint_boxes (rasterizer.py:262-281)
+// for one surfel, bit-exact with the reference (see header comment).
+__device__ __forceinline__ void project_exact(const ViewParams &P, const ParamView &pv, int64_t i,
+                                              ExactProj &o) {
+    const double mu[3] = {(double)pv.means[3 * i], (double)pv.means[3 * i + 1],
+                          (double)pv.means[3 * i + 2]};
+    double r[3];
+    quat_rotate_exact(P.inv + 4, mu, r);
+    o.p[0] = dadd(dmul(P.inv[0], r[0]), P.inv[1]);
+    o.p[1] = dadd(dmul(P.inv[0], r[1]), P.inv[2]);
+    o.p[2] = dadd(dmul(P.inv[0], r[2]), P.inv[3]);
+    const double z = o.p[2];
+    bool in_front = (z > P.near_plane) && (hypot(o.p[0], o.p[1]) <= dmul(P.tan_max, z));
+
+    const double q[4] = {(double)pv.quats[4 * i], (double)pv.quats[4 * i + 1],
+                         (double)pv.quats[4 * i + 2], (double)pv.quats[4 * i + 3]};
+    quat_to_matrix_exact(q, o.R);
+    const double s0 = (double)pv.scales[2 * i], s1 = (double)pv.scales[2 * i + 1];
+    double B[3][2];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        B[a][0] = dmul(o.R[3 * a], s0);
+        B[a][1] = dmul(o.R[3 * a + 1], s1);
+    }
+    // einsum("ij,njk->nik") : plain sequential sum (rasterizer.py:215)
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+            o.Bc[a][k] = dadd(dadd(dmul(P.m_cw[3 * a], B[0][k]), dmul(P.m_cw[3 * a + 1], B[1][k])),
+                              dmul(P.m_cw[3 * a + 2], B[2][k]));
+    // basis_cam @ basis_cam^T (rasterizer.py:216): BLAS dot = a0*b0, then fma
+    double C[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) C[a][b] = dfma(o.Bc[a][1], o.Bc[b][1], dmul(o.Bc[a][0], o.Bc[b][0]));
+    const double zs = in_front ? z : 1.0;
+    const double zz = dmul(zs, zs);
+    o.J[0][0] = ddiv(P.fx, zs);
+    o.J[0][1] = 0.0;
+    o.J[0][2] = ddiv(dmul(-P.fx, o.p[0]), zz);
+    o.J[1][0] = 0.0;
+    o.J[1][1] = ddiv(P.fy, zs);
+    o.J[1][2] = ddiv(dmul(-P.fy, o.p[1]), zz);
+    // (jac @ cov_cam) @ jac^T (rasterizer.py:224)
+    double T1[2][3], X[2][2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+            T1[a][c] = dfma(o.J[a][2], C[2][c], dfma(o.J[a][1], C[1][c], dmul(o.J[a][0], C[0][c])));
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+            X[a][c] = dfma(T1[a][2], o.J[c][2], dfma(T1[a][1], o.J[c][1], dmul(T1[a][0], o.J[c][0])));
+    o.a = dmul(0.5, dadd(X[0][0], X[0][0]));
+    o.b = dmul(0.5, dadd(X[0][1], X[1][0]));
+    o.c = dmul(0.5, dadd(X[1][1], X[1][1]));
+    o.cx = dadd(ddiv(dmul(P.fx, o.p[0]), zs), P.cx);
+    o.cy = dadd(ddiv(dmul(P.fy, o.p[1]), zs), P.cy);
+    in_front = in_front && (o.cx >= -P.mx) && (o.cx <= P.wmax) && (o.cy >= -P.my) && (o.cy <= P.hmax);
+
+    const double half_tr = dmul(0.5, dadd(o.a, o.c));
+    const double amc = dsub(o.a, o.c);
+    double d2 = dadd(dmul(0.25, dmul(amc, amc)), dmul(o.b, o.b));
+    if (d2 < 0.0) d2 = 0.0;  // np.maximum(x, 0.0); NaN propagates
+    const double dev = __dsqrt_rn(d2);
+    o.lmin = dsub(half_tr, dev);
+    o.lmax = dadd(half_tr, dev);
+    const bool well = (o.lmin > 0.0) && (o.lmax <= dmul(P.max_cond, o.lmin));
+    o.in_front = in_front;
+    o.valid = in_front && well;
+    const double det = o.valid ? dsub(dmul(o.a, o.c), dmul(o.b, o.b)) : 1.0;
+    o.ia = ddiv(o.c, det);
+    o.ib = ddiv(-o.b, det);
+    o.ic = ddiv(o.a, det);
+
+    double dinv = dsub(dmul(o.ia, o.ic), dmul(o.ib, o.ib));
+    if (!(dinv > 0.0)) dinv = 1.0;
+    double qx = ddiv(o.ic, dinv), qy = ddiv(o.ia, dinv);
+    if (qx < 0.0) qx = 0.0;
+    if (qy < 0.0) qy = 0.0;
+    o.rx = dmul(P.sigma, __dsqrt_rn(qx));
+    o.ry = dmul(P.sigma, __dsqrt_rn(qy));
+    o.x0 = clip64(f2i_x86(ceil(dsub(o.cx, o.rx))), 0, P.W - 1);
+    o.x1 = clip64(f2i_x86(floor(dadd(o.cx, o.rx))), 0, P.W - 1);
+    o.y0 = clip64(f2i_x86(ceil(dsub(o.cy, o.ry))), 0, P.H - 1);
+    o.y1 = clip64(f2i_x86(floor(dadd(o.cy, o.ry))), 0, P.H - 1);
+    o.on_screen = o.valid && (dadd(o.cx, o.rx) >= 0.0) && (dsub(o.cx, o.rx) <= P.wm1) &&
+                  (dadd(o.cy, o.ry) >= 0.0) && (dsub(o.cy, o.ry) <= P.hm1);
+}
+
+// Reference Mahalanobis distance at integer pixel (x, y), float64 with the
+// reference's association (_raster_kernels.py:38-39), for guard-band re-checks.
+__device__ __forceinline__ double exact_maha(const ExactProj &e, int x, int y) {
+    const double dx = dsub((double)x, e.cx);
+    const double dy = dsub((double)y, e.cy);
+    return dadd(dadd(dmul(dmul(e.ia, dx), dx), dmul(dmul(dmul(2.0, e.ib), dx), dy)),
+                dmul(dmul(e.ic, dy), dy));
+}
+
+// ---------------------------------------------------------- small utilities
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__device__ __forceinline__ void st_relaxed_u32(uint32_t *p, uint32_t v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Decoupled look-back status word: [flag:2 | value:30]
+constexpr uint32_t kFlagAgg = 1u << 30;
+constexpr uint32_t kFlagInc = 2u << 30;
+constexpr uint32_t kValMask = (1u << 30) - 1;
+
+// Exclusive prefix of `agg` over preceding tiles of a chained scan; tile order is
+// the dynamic ticket order so predecessors are always running (no deadlock).
+// Called by ONE thread per (tile, lane-of-status).
+__device__ __forceinline__ uint32_t lookback_exclusive(uint32_t *status, int stride, int tile,
+                                                       uint32_t agg) {
+    if (tile == 0) {
+        st_relaxed_u32(status, kFlagInc | agg);
+        return 0;
+    }
+    st_relaxed_u32(status + (size_t)tile * stride, kFlagAgg | agg);
+    uint32_t prefix = 0;
+    int j = tile - 1;
+    while (true) {
+        const uint32_t s = ld_relaxed_u32(status + (size_t)j * stride);
+        const uint32_t f = s & ~kValMask;
+        if (f == 0) continue;  // predecessor not published yet
+        prefix += s & kValMask;
+        if (f == kFlagInc) break;
+        --j;
+    }
+    st_relaxed_u32(status + (size_t)tile * stride, kFlagInc | (prefix + agg));
+    return prefix;
+}
+
+}  // namespace s2d

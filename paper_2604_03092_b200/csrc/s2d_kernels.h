@@ -1,0 +1,119 @@
+// s2d_kernels.h — host-callable launchers for the device kernels (internal).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/surfel2d.h"
+#include "s2d_device.cuh"
+
+namespace s2d {
+
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = 16;
+constexpr int kSortTile = kSortThreads * kSortItems;  // keys per onesweep CTA
+constexpr int kRadixBits = 8;
+constexpr int kRadix = 1 << kRadixBits;
+constexpr int kProjThreads = 256;   // surfels per projection CTA (one per thread)
+constexpr int kEmitItems = 8;
+constexpr int kEmitTile = 256 * kEmitItems;
+
+// Zeroed-per-view scratch ("sync region"): look-back status words, tickets,
+// radix histograms, tile ranges, stats.  One memset per view.
+struct SyncRegion {
+    s2d_view_stats *stats;     // device stats (first, 32 B)
+    int *tickets;              // [16]
+    uint32_t *proj_status;     // [ceil(n / kProjThreads)]
+    uint32_t *depth_hist;      // [4 * kRadix]
+    uint32_t *depth_status;    // [4][ceil(n / kSortTile) * kRadix]
+    uint32_t *emit_status;     // [ceil(n / kEmitTile)]
+    uint32_t *pair_hist;       // [2 * kRadix]
+    uint32_t *pair_status;     // [2][ceil(pcap / kSortTile) * kRadix]
+    uint32_t *tie_claim;       // [n]
+    int2 *ranges;              // [ntiles]
+    size_t bytes;
+};
+
+struct ProjectArgs {
+    ViewParams P;
+    const float *params;
+    SplatRecord *rec;
+    short4 *rect;
+    double *z64;
+    uint8_t *flags;
+    uint32_t *keys;
+    uint32_t *vals;
+    s2d_view_stats *stats;
+    uint32_t *status;
+    int *ticket;
+};
+void launch_project(const ProjectArgs &a, cudaStream_t s);
+
+void launch_radix_hist(const uint32_t *keys, const int *d_n, int cap, int passes, uint32_t *hist,
+                       cudaStream_t s);
+void launch_onesweep(const uint32_t *kin, const uint32_t *vin, uint32_t *kout, uint32_t *vout,
+                     const int *d_n, int cap, int shift, const uint32_t *hist_pass,
+                     uint32_t *status, int *ticket, cudaStream_t s);
+void launch_tie_fix(const uint32_t *keys, uint32_t *vals, const double *z64, const int *d_n, int cap,
+                    uint32_t *claim, cudaStream_t s);
+
+struct EmitArgs {
+    const uint32_t *order;
+    const short4 *rect;
+    const int *d_v;
+    int cap_v;
+    int ntx;
+    int pair_passes;
+    uint32_t *pkeys;
+    uint32_t *pvals;
+    uint32_t pcap;
+    s2d_view_stats *stats;
+    uint32_t *status;
+    int *ticket;
+    uint32_t *pair_hist;
+};
+void launch_scan_emit(const EmitArgs &a, cudaStream_t s);
+void launch_tile_ranges(const uint32_t *pkeys, const int *d_p, uint32_t pcap, int2 *ranges,
+                        cudaStream_t s);
+
+struct RasterArgs {
+    ViewParams P;
+    const float *params;
+    const int2 *ranges;
+    const uint32_t *pair_ids;
+    const SplatRecord *rec;
+    const short4 *rect;
+    int2 *aux;  // per pixel (last list position, float bits of T before it)
+    // forward outputs (forward writes, backward reads)
+    float *color, *depth, *accum, *normal, *max_w;
+    int32_t *arg_w;
+    float *max_all, *max_marked;
+    const uint8_t *mask;
+    s2d_view_stats *stats;
+    // backward
+    int loss_kind, depth_mask;
+    double w_rgb, w_depth;
+    const float *target_rgb, *target_depth;
+    const float *d_color, *d_depth, *d_normal, *d_accum;
+    float *grad2d;  // [n][16]
+    double *loss_accum;
+};
+void launch_raster_forward(const RasterArgs &a, cudaStream_t s);
+void launch_raster_backward(const RasterArgs &a, cudaStream_t s);
+
+struct ProjectBwdArgs {
+    ViewParams P;
+    const float *params;
+    const uint8_t *flags;
+    float *grad2d;
+    float *grads;
+};
+void launch_project_backward(const ProjectBwdArgs &a, cudaStream_t s);
+
+void launch_adam(float *params, const float *grads, float *m1, float *m2, int64_t n, int64_t step,
+                 const s2d_adam_config &cfg, const uint8_t *mask, cudaStream_t s);
+
+// number of 8-bit digit passes needed for keys < 2^bits
+inline int passes_for_bits(int bits) { return bits <= 0 ? 1 : (bits + kRadixBits - 1) / kRadixBits; }
+
+}  // namespace s2d
