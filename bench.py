@@ -1,0 +1,349 @@
+#!/usr/bin/env python
+"""Benchmark: BASELINE config 4 refine iterations (1M surfels, 32 views 640x480, fp32).
+
+One step = one refine iteration: this rank's share of the 32 views forward+backward
+(projection, depth order, tile binning, compositing, L1 RGB + 0.1 L1 depth seeds,
+reverse-order backward, projection backward), the NCCL all-reduce of the packed
+surfel gradients (N>1), and the fused Adam step.  Views are sharded over ranks
+(strong scaling: 32 views total at every N).
+
+  value  = whole-job Mpix/s = 32 views * 640*480 px / step time (device-resident targets)
+  e2e    = the same through the public API with the targets copied in from pinned host
+           memory every step and the loss read back (AdamRefiner(host_targets=True))
+  refine_iters_per_s = 1 / step time
+  roofline = the dominant kernel's algorithmic bytes / its CUDA-event duration vs measured HBM
+  cpu_baseline = the float64 CPU port (oracle/) on a bounded sample of views, host threads
+
+``--impl reference`` times the CPU port of the reference path (the reference itself is
+Python+numba and not on the GPU box) on the same config/metric: each step is one
+fwd+bwd view per host thread.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "2DGS fwd+bwd Mpix/s at 1M surfels; refine iters/s at 1/2/4/8 GPU"
+WORKLOAD = "config4: 1,000,000 surfels, 32 views 640x480 fx=fy=500, L1 RGB + 0.1 L1 depth, Adam"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-views", type=int, default=0, help="views in the CPU baseline sample (0 = auto)")
+    ap.add_argument("--small", action="store_true", help="reduced workload for quick checks (not a bench value)")
+    return ap.parse_args()
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, f[2:6]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def make_workload(seed, small=False):
+    import numpy as np
+    from paper_2604_03092_b200 import scenes
+    if small:
+        sc = scenes.config4(seed, n_keyframes=2, per_keyframe=50_000, n_views=8)
+    else:
+        sc = scenes.config4(seed)
+    return sc
+
+
+def render_targets(sc, device):
+    """Targets = renders of the unperturbed map (GPU), kept on device and as pinned host copies."""
+    import torch
+    from paper_2604_03092_b200.engine import (DeviceContext, ImageBuffers, View, camera_struct, config_struct,
+                                              forward_checked, pack_params)
+    from paper_2604_03092_b200.rasterizer import DEFAULT_RASTER_CONFIG
+    ctx = DeviceContext.get(device)
+    view = View(ctx)
+    params = pack_params(sc.surfels, ctx.device)
+    cam, cfg = camera_struct(sc.intr), config_struct(DEFAULT_RASTER_CONFIG)
+    rgbs, deps = [], []
+    for pose in sc.poses:
+        img = ImageBuffers.allocate(sc.intr.height, sc.intr.width, ctx.device, normal=False)
+        forward_checked(view, params, len(sc.surfels), pose, cam, cfg, img)
+        rgbs.append(img.color.clone())
+        deps.append(img.depth.clone())
+    del params, view
+    return rgbs, deps
+
+
+# algorithmic bytes per launch of each phase
+def phase_bytes(n, v, p, x):
+    return {
+        "project": 52 * n + n + 88 * v,                       # params in; flags, record 64, rect 8, z64 8, key/val 8
+        "depth_sort": 4 * v + 4 * 16 * v + 12 * v,            # hist read + 4 passes x (r+w keys+vals) + tie fix
+        "tile_bin": 12 * v + 8 * p + 2 * 16 * p + 4 * p,      # order+rect in, pairs out, 2 sort passes, ranges
+        "raster_fwd": 4 * p + 72 * p + 28 * x,                # ids + (record, rect) per pair; rgb, depth, acc, aux out
+        "raster_bwd": 4 * p + 72 * p + 44 * x + 64 * v,       # ids + records; pixel outputs/aux/targets; 2D grads
+        "project_bwd": n + 64 * v + 52 * v + 104 * v + 64 * v,  # flags; 2D grads in; params in; grads r+w; zero
+    }
+
+
+def run_cpu_port(sc, targets, views, threads):
+    """Time the float64 CPU port (oracle) fwd+bwd of `views` views on `threads` host threads."""
+    import numpy as np
+    from concurrent.futures import ThreadPoolExecutor
+    import oracle as O
+    O.load()
+    surf = sc.extra["perturbed"]
+
+    def one(v):
+        rgb, dep = targets[v]
+        O.loss_and_grads(surf, sc.poses[v], sc.intr, rgb, dep, "l1", 1.0, 0.1, mask_depth=False)
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        list(ex.map(one, views))
+    return time.perf_counter() - t0
+
+
+def reference_arm(args):
+    """--impl reference: the CPU port of the reference path on all host threads."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+    from paper_2604_03092_b200 import scenes
+    import oracle as O
+    sc = make_workload(args.seed, args.small)
+    # targets: CPU port render of the unperturbed map (no GPU on this arm)
+    threads = len(os.sched_getaffinity(0))
+    nv = min(threads, len(sc.poses))
+    targets = {}
+    for v in range(nv):
+        b = O.render(sc.surfels, sc.poses[v], sc.intr, with_normal=False)
+        targets[v] = (b.color, b.depth)
+    px = sc.intr.width * sc.intr.height
+    for _ in range(args.warmup):
+        run_cpu_port(sc, targets, list(range(nv)), threads)
+    times = [run_cpu_port(sc, targets, list(range(nv)), threads) for _ in range(args.steps)]
+    tot = sum(times)
+    val = nv * px * args.steps / tot / 1e6
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "Mpix/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded config-4 generator)",
+            "config": {"workload": WORKLOAD, "sample": f"{nv} views fwd+bwd per step, one per thread"},
+            "cpu_baseline": {"value": val, "unit": "Mpix/s", "cores": threads, "kind": "port",
+                             "sample": f"{nv} config-4 views fwd+bwd (float64 C port of the reference path, oracle/)"},
+            "e2e": {"value": val, "unit": "Mpix/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        reference_arm(args)
+        return
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2604_03092_b200 import _native as N
+    from paper_2604_03092_b200.distributed import init_from_env
+    from paper_2604_03092_b200.mapper import AdamConfig, AdamRefiner, ViewLoss
+
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    rank, world = init_from_env("nccl") if args.gpus > 1 else (0, 1)
+    dev = torch.device("cuda", local_rank)
+
+    sc = make_workload(args.seed, args.small)
+    rgbs, deps = render_targets(sc, dev)
+    n_views = len(sc.poses)
+    px = sc.intr.width * sc.intr.height
+    loss = ViewLoss("l1", 1.0, 0.1, False)
+
+    # ---- device-resident run (value) ----
+    ref = AdamRefiner(sc.extra["perturbed"], sc.intr, sc.poses, rgbs, deps, loss, AdamConfig(), device=dev)
+    for _ in range(args.warmup):
+        ref.step()
+    clocks = ClockSampler(local_rank)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = N.lib().s2d_launch_count()
+    clocks.start()
+    time.sleep(0.2)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    losses = [ref.step() for _ in range(args.steps)]
+    e1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    launches = N.lib().s2d_launch_count() - launches0
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    ms_step = ms / args.steps
+    value = n_views * px / (ms_step * 1e-3) / 1e6
+
+    # ---- per-phase breakdown (separate timed pass with events between kernels) ----
+    ref.view.set_timing(True)
+    ref.view.timing(reset=True)
+    tb0 = torch.cuda.Event(enable_timing=True)
+    tb1 = torch.cuda.Event(enable_timing=True)
+    tb0.record()
+    nb_steps = max(3, min(args.steps, 10))
+    for _ in range(nb_steps):
+        ref.step()
+    tb1.record()
+    torch.cuda.synchronize()
+    ph = ref.view.timing(reset=True)
+    ref.view.set_timing(False)
+    st = ref.view.stats()
+    nfw = max(ph["n_forward"], 1)
+    per_launch_ms = {k: ph[k] / nfw for k in ref.view.PHASES}
+    nvis, npairs = st.visible, st.pairs
+    pb = phase_bytes(ref.n, nvis, npairs, px)
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except Exception:
+        pass
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    dom = max(per_launch_ms, key=per_launch_ms.get)
+    achieved = pb[dom] / (per_launch_ms[dom] * 1e-3) / 1e9
+    view_bytes = 104 * ref.n + 312 * nvis + 180 * npairs + 88 * px
+    view_ms = sum(per_launch_ms.values())
+    phases = {k: {"ms": round(per_launch_ms[k], 4), "gbs": round(pb[k] / (per_launch_ms[k] * 1e-3) / 1e9, 1)
+                  if per_launch_ms[k] > 0 else None} for k in per_launch_ms}
+
+    # ---- end-to-end run through the public API with host (pinned) targets ----
+    host_rgb = [r.cpu() for r in rgbs]
+    host_dep = [d.cpu() for d in deps]
+    del ref
+    torch.cuda.empty_cache()
+    ref2 = AdamRefiner(sc.extra["perturbed"], sc.intr, sc.poses, host_rgb, host_dep, loss, AdamConfig(), device=dev,
+                       host_targets=True)
+    for _ in range(args.warmup):
+        ref2.step()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record()
+    for _ in range(args.steps):
+        ref2.step()
+    e3.record()
+    torch.cuda.synchronize()
+    t2 = torch.tensor([e2.elapsed_time(e3)], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+    e2e_ms_step = float(t2.item()) / args.steps
+    e2e_value = n_views * px / (e2e_ms_step * 1e-3) / 1e6
+    h2d = ref2.h2d_bytes_per_step
+    del ref2
+
+    # ---- CPU baseline (rank 0, N=1 only) ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = len(os.sched_getaffinity(0))
+        nv = args.cpu_views or min(max(threads, 1), n_views)
+        targets = {v: (rgbs[v].double().cpu().numpy(), deps[v].double().cpu().numpy()) for v in range(nv)}
+        secs = run_cpu_port(sc, targets, list(range(nv)), threads)
+        cpu = {"value": nv * px / secs / 1e6, "unit": "Mpix/s", "cores": min(threads, nv), "kind": "port",
+               "sample": f"{nv} config-4 views fwd+bwd in {secs:.1f}s (float64 C port of the reference path, oracle/)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "Mpix/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded config-4 generator; targets = renders of the unperturbed map)",
+            "config": {"workload": WORKLOAD + (" [SMALL]" if args.small else ""), "surfels": ref_n(sc),
+                       "views": n_views, "image": [sc.intr.width, sc.intr.height],
+                       "parallelism": f"view-sharded dp{world}",
+                       "l2": "working set per step > L2 (params+grads+moments 208 MB, targets 157 MB)",
+                       "visible_last_view": nvis, "pairs_last_view": npairs},
+            "refine_iters_per_s": round(1000.0 / ms_step, 3),
+            "fwd_bwd_mpix_per_s_per_view": round(px / (view_ms * 1e-3) / 1e6, 2) if view_ms > 0 else None,
+            "loss_first_last": [losses[0], losses[-1]],
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm,
+                         "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": None,
+                         "peak_source": peak_src, "algorithmic_bytes_per_launch": pb[dom],
+                         "launch_ms": round(per_launch_ms[dom], 4)},
+            "roofline_view": {"bytes": view_bytes, "ms": round(view_ms, 4),
+                              "achieved_gbs": round(view_bytes / (view_ms * 1e-3) / 1e9, 1) if view_ms > 0 else None,
+                              "frac": round(view_bytes / (view_ms * 1e-3) / 1e9 / hbm, 4) if view_ms > 0 else None},
+            "phases_per_view": phases,
+            "e2e": {"value": round(e2e_value, 3), "unit": "Mpix/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": 8 + 32, "ms_per_step": round(e2e_ms_step, 4)},
+            "gpu_launches": int(launches),
+            "clocks": clk,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def ref_n(sc):
+    return len(sc.surfels)
+
+
+if __name__ == "__main__":
+    main()

@@ -139,6 +139,18 @@ int s2d_view_stats_accumulate(s2d_view *view, void *stream, s2d_view_stats *acc_
 int s2d_view_reserve_pairs(s2d_view *view, int64_t pairs);
 int s2d_view_inspect(s2d_view *view, s2d_view_debug *out);
 
+/* Number of kernels this library has launched in this process (all devices). */
+int64_t s2d_launch_count(void);
+
+/* Phase timing: when enabled, s2d_forward/s2d_backward record CUDA events between
+ * their kernels on the launching stream; s2d_view_timing synchronises and returns
+ * the accumulated milliseconds per phase since the last reset:
+ *  [0] project  [1] depth sort (hist, 4 passes, tie fix)  [2] scan+emit, tile sort, ranges
+ *  [3] raster forward  [4] raster backward  [5] projection backward
+ * and the number of timed forwards in out[6], backwards in out[7]. */
+int s2d_view_set_timing(s2d_view *view, int32_t enable);
+int s2d_view_timing(s2d_view *view, double out[8], int32_t reset);
+
 /* float64 pose inverse exactly as pk_inverse (geometry.py:188-195); out[8] */
 int s2d_pose_inverse(const double pose_c2w[8], double out[8]);
 

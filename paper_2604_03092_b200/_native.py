@@ -92,6 +92,9 @@ _SIGNATURES = {
     "s2d_view_stats_accumulate": (ctypes.c_int, [c_p, c_p, c_p]),
     "s2d_view_reserve_pairs": (ctypes.c_int, [c_p, ctypes.c_int64]),
     "s2d_view_inspect": (ctypes.c_int, [c_p, ctypes.POINTER(ViewDebug)]),
+    "s2d_launch_count": (ctypes.c_int64, []),
+    "s2d_view_set_timing": (ctypes.c_int, [c_p, ctypes.c_int32]),
+    "s2d_view_timing": (ctypes.c_int, [c_p, ctypes.POINTER(ctypes.c_double), ctypes.c_int32]),
     "s2d_pose_inverse": (ctypes.c_int, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
     "s2d_forward": (ctypes.c_int, [c_p, c_p, c_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_double),
                                    ctypes.POINTER(Camera), ctypes.POINTER(RasterCfg),

@@ -313,7 +313,10 @@ __global__ void __launch_bounds__(256) k_tile_ranges(const uint32_t *__restrict_
 
 void launch_project(const ProjectArgs &a, cudaStream_t s) {
     const int blocks = (int)((a.P.n + kProjThreads - 1) / kProjThreads);
-    if (blocks > 0) k_project<<<blocks, kProjThreads, 0, s>>>(a);
+    if (blocks > 0) {
+        count_launch();
+        k_project<<<blocks, kProjThreads, 0, s>>>(a);
+    }
 }
 
 void launch_radix_hist(const uint32_t *keys, const int *d_n, int cap, int passes, uint32_t *hist,
@@ -321,6 +324,7 @@ void launch_radix_hist(const uint32_t *keys, const int *d_n, int cap, int passes
     int blocks = (cap + 255) / 256;
     if (blocks > 592) blocks = 592;
     if (blocks < 1) blocks = 1;
+    count_launch();
     k_radix_hist<<<blocks, 256, 0, s>>>(keys, d_n, passes, hist);
 }
 
@@ -328,24 +332,36 @@ void launch_onesweep(const uint32_t *kin, const uint32_t *vin, uint32_t *kout, u
                      const int *d_n, int cap, int shift, const uint32_t *hist_pass,
                      uint32_t *status, int *ticket, cudaStream_t s) {
     const int blocks = (cap + kSortTile - 1) / kSortTile;
-    if (blocks > 0) k_onesweep<<<blocks, kSortThreads, 0, s>>>(kin, vin, kout, vout, d_n, shift, hist_pass, status, ticket);
+    if (blocks > 0) {
+        count_launch();
+        k_onesweep<<<blocks, kSortThreads, 0, s>>>(kin, vin, kout, vout, d_n, shift, hist_pass, status, ticket);
+    }
 }
 
 void launch_tie_fix(const uint32_t *keys, uint32_t *vals, const double *z64, const int *d_n, int cap,
                     uint32_t *claim, cudaStream_t s) {
     const int blocks = (cap + 255) / 256;
-    if (blocks > 0) k_tie_fix<<<blocks, 256, 0, s>>>(keys, vals, z64, d_n, claim);
+    if (blocks > 0) {
+        count_launch();
+        k_tie_fix<<<blocks, 256, 0, s>>>(keys, vals, z64, d_n, claim);
+    }
 }
 
 void launch_scan_emit(const EmitArgs &a, cudaStream_t s) {
     const int blocks = (a.cap_v + kEmitTile - 1) / kEmitTile;
-    if (blocks > 0) k_scan_emit<<<blocks, 256, 0, s>>>(a);
+    if (blocks > 0) {
+        count_launch();
+        k_scan_emit<<<blocks, 256, 0, s>>>(a);
+    }
 }
 
 void launch_tile_ranges(const uint32_t *pkeys, const int *d_p, uint32_t pcap, int2 *ranges,
                         cudaStream_t s) {
     const int blocks = (int)((pcap + 255) / 256);
-    if (blocks > 0) k_tile_ranges<<<blocks, 256, 0, s>>>(pkeys, d_p, pcap, ranges);
+    if (blocks > 0) {
+        count_launch();
+        k_tile_ranges<<<blocks, 256, 0, s>>>(pkeys, d_p, pcap, ranges);
+    }
 }
 
 }  // namespace s2d

@@ -11,7 +11,9 @@
 // capturable).  Pair capacity overflow is reported in s2d_view_stats.overflow.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cmath>
+#include <vector>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -170,6 +172,10 @@ struct s2d_ctx {
     int device;
 };
 
+namespace s2d {
+std::atomic<int64_t> g_launches{0};
+}
+
 struct s2d_view {
     s2d_ctx *ctx = nullptr;
     // capacities (elements)
@@ -194,6 +200,27 @@ struct s2d_view {
     int pair_buf = 0;   // which pkeys/pvals buffer holds the sorted pairs
     int order_buf = 0;  // which vals buffer holds the depth order
     cudaStream_t last_stream = nullptr;
+    // phase timing (events recorded between kernels, resolved in s2d_view_timing)
+    struct TimedCall {
+        cudaEvent_t e[5];
+        int n;
+        int kind;  // 0 forward, 1 backward
+    };
+    bool timing = false;
+    std::vector<TimedCall> timed;
+    std::vector<cudaEvent_t> free_events;
+    double phase_ms[6] = {0, 0, 0, 0, 0, 0};
+    int64_t n_fwd_timed = 0, n_bwd_timed = 0;
+    cudaEvent_t take_event() {
+        if (free_events.empty()) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            return e;
+        }
+        cudaEvent_t e = free_events.back();
+        free_events.pop_back();
+        return e;
+    }
     // scratch for the host-buffer entry point
     int64_t cap_hp = 0, cap_himg = 0;
     float *h_params_dev = nullptr, *h_img_dev = nullptr;
@@ -281,6 +308,15 @@ int view_forward(s2d_view *v, cudaStream_t s, const float *params, int64_t n, co
     if ((rc = ensure_capacity(v, n, npx, ntiles))) return rc;
     v->has_fwd = false;
     S2D_CUDA(cudaMemsetAsync(v->sync, 0, v->sr.bytes, s));
+    s2d_view::TimedCall tc{};
+    tc.kind = 0;
+    auto mark = [&]() {
+        if (v->timing && tc.n < 5) {
+            tc.e[tc.n] = v->take_event();
+            cudaEventRecord(tc.e[tc.n++], s);
+        }
+    };
+    mark();
     SyncRegion &sr = v->sr;
     int *d_v = &sr.stats->visible;
     if (n > 0) {
@@ -297,6 +333,7 @@ int view_forward(s2d_view *v, cudaStream_t s, const float *params, int64_t n, co
         pa.status = sr.proj_status;
         pa.ticket = sr.tickets + 0;
         launch_project(pa, s);
+        mark();
         // depth order: 4 stable 8-bit passes over the upper 32 bits of float64 z
         launch_radix_hist(v->keys[0], d_v, (int)n, 4, sr.depth_hist, s);
         const int64_t sort_tiles = (n + kSortTile - 1) / kSortTile + 1;
@@ -309,6 +346,7 @@ int view_forward(s2d_view *v, cudaStream_t s, const float *params, int64_t n, co
         }
         launch_tie_fix(v->keys[cur], v->vals[cur], v->z64, d_v, (int)n, sr.tie_claim, s);
         v->order_buf = cur;
+        mark();
         // tile binning: pairs emitted in depth order, then stable sort by tile id
         const int tbits = bits_for(ntiles);
         const int ppass = passes_for_bits(tbits);
@@ -338,7 +376,11 @@ int view_forward(s2d_view *v, cudaStream_t s, const float *params, int64_t n, co
         v->pair_buf = pc;
         launch_tile_ranges(v->pkeys[pc], &sr.stats->pairs, (uint32_t)v->pcap, sr.ranges, s);
         S2D_CHECK_LAUNCH();
+    } else {
+        mark();
+        mark();
     }
+    mark();
     RasterArgs ra;
     memset(&ra, 0, sizeof(ra));
     ra.P = P;
@@ -360,6 +402,8 @@ int view_forward(s2d_view *v, cudaStream_t s, const float *params, int64_t n, co
     ra.stats = sr.stats;
     launch_raster_forward(ra, s);
     S2D_CHECK_LAUNCH();
+    mark();
+    if (v->timing) v->timed.push_back(tc);
     v->P = P;
     v->n = n;
     v->has_fwd = true;
@@ -407,6 +451,9 @@ int s2d_view_destroy(s2d_view *v) {
                     v->h_params_dev, v->h_img_dev};
     for (void *p : ptrs)
         if (p) cudaFree(p);
+    for (auto &tc : v->timed)
+        for (int k = 0; k < tc.n; ++k) cudaEventDestroy(tc.e[k]);
+    for (cudaEvent_t e : v->free_events) cudaEventDestroy(e);
     delete v;
     return S2D_OK;
 }
@@ -432,6 +479,7 @@ int s2d_view_stats_host(s2d_view *v, s2d_view_stats *out) {
 int s2d_view_stats_accumulate(s2d_view *v, void *stream, s2d_view_stats *acc_device) {
     if (!v || !acc_device) return fail(S2D_ERR_INVALID, "NULL argument");
     if (!v->sync) return fail(S2D_ERR_STATE, "view has no forward yet");
+    count_launch();
     k_stats_accumulate<<<1, 1, 0, (cudaStream_t)stream>>>(v->sr.stats, acc_device);
     S2D_CHECK_LAUNCH();
     return S2D_OK;
@@ -441,6 +489,40 @@ int s2d_view_reserve_pairs(s2d_view *v, int64_t pairs) {
     if (!v) return fail(S2D_ERR_INVALID, "NULL view");
     if (pairs > ((int64_t)1 << 30)) return fail(S2D_ERR_INVALID, "pair capacity too large");
     if (pairs > v->pcap) v->pcap = pairs;
+    return S2D_OK;
+}
+
+int64_t s2d_launch_count(void) { return s2d::g_launches.load(); }
+
+int s2d_view_set_timing(s2d_view *v, int32_t enable) {
+    if (!v) return fail(S2D_ERR_INVALID, "NULL view");
+    v->timing = enable != 0;
+    return S2D_OK;
+}
+
+int s2d_view_timing(s2d_view *v, double out[8], int32_t reset) {
+    if (!v || !out) return fail(S2D_ERR_INVALID, "NULL argument");
+    for (auto &tc : v->timed) {
+        if (tc.n < 2) continue;
+        S2D_CUDA(cudaEventSynchronize(tc.e[tc.n - 1]));
+        for (int k = 0; k + 1 < tc.n; ++k) {
+            float ms = 0.f;
+            S2D_CUDA(cudaEventElapsedTime(&ms, tc.e[k], tc.e[k + 1]));
+            const int phase = tc.kind == 0 ? k : 4 + k;
+            if (phase < 6) v->phase_ms[phase] += ms;
+        }
+        if (tc.kind == 0) v->n_fwd_timed++;
+        else v->n_bwd_timed++;
+        for (int k = 0; k < tc.n; ++k) v->free_events.push_back(tc.e[k]);
+    }
+    v->timed.clear();
+    for (int k = 0; k < 6; ++k) out[k] = v->phase_ms[k];
+    out[6] = (double)v->n_fwd_timed;
+    out[7] = (double)v->n_bwd_timed;
+    if (reset) {
+        for (int k = 0; k < 6; ++k) v->phase_ms[k] = 0;
+        v->n_fwd_timed = v->n_bwd_timed = 0;
+    }
     return S2D_OK;
 }
 
@@ -473,6 +555,15 @@ int s2d_backward(s2d_view *v, void *stream, const float *params, int64_t n, cons
             return fail(S2D_ERR_INVALID, "unknown loss kind");
     }
     cudaStream_t s = (cudaStream_t)stream;
+    s2d_view::TimedCall tc{};
+    tc.kind = 1;
+    auto mark = [&]() {
+        if (v->timing && tc.n < 5) {
+            tc.e[tc.n] = v->take_event();
+            cudaEventRecord(tc.e[tc.n++], s);
+        }
+    };
+    mark();
     RasterArgs ra;
     memset(&ra, 0, sizeof(ra));
     ra.P = v->P;
@@ -500,6 +591,7 @@ int s2d_backward(s2d_view *v, void *stream, const float *params, int64_t n, cons
     ra.grad2d = v->grad2d;
     ra.loss_accum = loss_accum;
     launch_raster_backward(ra, s);
+    mark();
     if (n > 0) {
         ProjectBwdArgs pb;
         pb.P = v->P;
@@ -510,6 +602,8 @@ int s2d_backward(s2d_view *v, void *stream, const float *params, int64_t n, cons
         launch_project_backward(pb, s);
     }
     S2D_CHECK_LAUNCH();
+    mark();
+    if (v->timing) v->timed.push_back(tc);
     v->last_stream = s;
     return S2D_OK;
 }

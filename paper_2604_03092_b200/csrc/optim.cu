@@ -216,7 +216,10 @@ __global__ void __launch_bounds__(256) k_adam(float *__restrict__ params, const 
 
 void launch_project_backward(const ProjectBwdArgs &a, cudaStream_t s) {
     const int64_t blocks = (a.P.n + 127) / 128;
-    if (blocks > 0) k_project_bwd<<<(unsigned)blocks, 128, 0, s>>>(a);
+    if (blocks > 0) {
+        count_launch();
+        k_project_bwd<<<(unsigned)blocks, 128, 0, s>>>(a);
+    }
 }
 
 void launch_adam(float *params, const float *grads, float *m1, float *m2, int64_t n, int64_t step,
@@ -234,7 +237,10 @@ void launch_adam(float *params, const float *grads, float *m1, float *m2, int64_
     k.step_rest = (float)(cfg.lr_rest / bc1);
     k.inv_sqrt_bc2 = (float)(1.0 / sqrt(bc2));
     const int64_t blocks = (n + 255) / 256;
-    if (blocks > 0) k_adam<<<(unsigned)blocks, 256, 0, s>>>(params, grads, m1, m2, n, k, mask);
+    if (blocks > 0) {
+        count_launch();
+        k_adam<<<(unsigned)blocks, 256, 0, s>>>(params, grads, m1, m2, n, k, mask);
+    }
 }
 
 }  // namespace s2d

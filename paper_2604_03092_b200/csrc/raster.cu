@@ -512,6 +512,7 @@ void launch_raster_forward(const RasterArgs &a, cudaStream_t s) {
     const int tiles = a.P.ntx * a.P.nty;
     const bool arg = a.max_w != nullptr || a.arg_w != nullptr;
     const bool mw = a.max_all != nullptr;
+    count_launch();
     if (arg && mw) k_raster_fwd<true, true><<<tiles, kRasterThreads, 0, s>>>(a);
     else if (arg) k_raster_fwd<true, false><<<tiles, kRasterThreads, 0, s>>>(a);
     else if (mw) k_raster_fwd<false, true><<<tiles, kRasterThreads, 0, s>>>(a);
@@ -520,6 +521,7 @@ void launch_raster_forward(const RasterArgs &a, cudaStream_t s) {
 
 void launch_raster_backward(const RasterArgs &a, cudaStream_t s) {
     const int tiles = a.P.ntx * a.P.nty;
+    count_launch();
     k_raster_bwd<<<tiles, kRasterThreads, 0, s>>>(a);
 }
 

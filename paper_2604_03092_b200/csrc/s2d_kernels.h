@@ -4,10 +4,15 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "../../include/surfel2d.h"
 #include "s2d_device.cuh"
 
 namespace s2d {
+
+extern std::atomic<int64_t> g_launches;
+inline void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 constexpr int kSortThreads = 256;
 constexpr int kSortItems = 16;

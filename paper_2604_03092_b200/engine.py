@@ -189,6 +189,20 @@ class View:
         N.check(N.lib().s2d_view_stats_accumulate(self.handle, self._stream(stream), N.dptr(acc)),
                 "s2d_view_stats_accumulate")
 
+    def set_timing(self, enable: bool):
+        N.check(N.lib().s2d_view_set_timing(self.handle, int(bool(enable))), "s2d_view_set_timing")
+
+    PHASES = ("project", "depth_sort", "tile_bin", "raster_fwd", "raster_bwd", "project_bwd")
+
+    def timing(self, reset: bool = True) -> dict:
+        """Accumulated per-phase milliseconds (synchronises)."""
+        out = (ctypes.c_double * 8)()
+        N.check(N.lib().s2d_view_timing(self.handle, out, int(reset)), "s2d_view_timing")
+        d = {k: out[i] for i, k in enumerate(self.PHASES)}
+        d["n_forward"] = int(out[6])
+        d["n_backward"] = int(out[7])
+        return d
+
     def reserve_pairs(self, pairs: int):
         N.check(N.lib().s2d_view_reserve_pairs(self.handle, int(pairs)), "s2d_view_reserve_pairs")
 

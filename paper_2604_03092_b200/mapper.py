@@ -1,0 +1,343 @@
+"""Refinement on the GPU path.
+
+* :func:`refine` — drop-in for ``surfelslam.mapper.refine`` (mapper.py:276-349):
+  backtracking gradient descent on the colours/opacities of the surfels bound
+  to the given keyframes, L-inf normalised step, halving, clip to [0, 1],
+  warm-started step; the summed loss never increases.  The map stays resident
+  on the device for the whole call; every trial is V x (forward + backward)
+  through the fused kernels.
+* :class:`AdamRefiner` — the multi-view refinement of BASELINE configs 4-5:
+  every iteration renders this rank's views forward+backward (L1 RGB + depth),
+  all-reduces the packed 13N gradient block over NCCL, and applies the fused
+  Adam step (lr 1e-3 means, 5e-3 the rest) to all surfel parameters.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .distributed import allreduce_grads, shard_views, world
+from .engine import (DeviceContext, ImageBuffers, View, camera_struct, config_struct, forward_checked,
+                     pack_params, unpack_params)
+from .geometry import as_packed_pose
+from .rasterizer import (DEFAULT_RASTER_CONFIG, CameraIntrinsics, LossWeights, RasterConfig, SurfelArrays,
+                         loss_struct)
+
+__all__ = ["RefinementConfig", "RefinementReport", "GlobalSurfelMap", "refine", "psnr", "AdamConfig",
+           "ViewLoss", "AdamRefiner"]
+
+PSNR_EXACT = float("inf")
+
+
+def psnr(rendered, target) -> float:
+    """10 log10(1/MSE) over all channels of [0,1] images; inf on MSE=0 (evaluation.py:63-72)."""
+    rendered = np.asarray(rendered, dtype=float)
+    target = np.asarray(target, dtype=float)
+    if rendered.shape != target.shape:
+        raise ValueError("image dimensions differ")
+    mse = float(np.mean((rendered - target) ** 2))
+    if mse == 0.0:
+        return PSNR_EXACT
+    return 10.0 * math.log10(1.0 / mse)
+
+
+@dataclass(frozen=True)
+class RefinementConfig:
+    """mapper.py:64-70"""
+
+    iterations: int = 20
+    keyframes: int = 4
+    initial_step: float = 0.1
+    min_step: float = 1e-6
+    loss: LossWeights = field(default_factory=LossWeights)
+
+
+@dataclass
+class RefinementReport:
+    """mapper.py:268-273"""
+
+    losses: list
+    psnr_before: float
+    psnr_after: float
+    accepted_steps: int
+
+
+@dataclass
+class GlobalSurfelMap:
+    """World-frame surfel store with keyframe bindings (mapper.py:73-103)."""
+
+    surfels: SurfelArrays = field(default_factory=SurfelArrays.empty)
+    keyframe_poses: dict = field(default_factory=dict)
+
+    def __len__(self):
+        return len(self.surfels)
+
+
+class _ViewSet:
+    """Device-resident targets + one reusable workspace for a list of views."""
+
+    def __init__(self, intr, poses, rgbs, depths, raster_cfg, device):
+        self.ctx = DeviceContext.get(device)
+        self.dev = self.ctx.device
+        self.intr = intr
+        self.cam = camera_struct(intr)
+        self.cfg = config_struct(raster_cfg)
+        self.poses = [as_packed_pose(p) for p in poses]
+        self.rgb = [torch.from_numpy(np.asarray(r, dtype=np.float32)).to(self.dev) for r in rgbs]
+        self.depth = [torch.from_numpy(np.asarray(d, dtype=np.float32)).to(self.dev) for d in depths]
+        self.view = View(self.ctx)
+        self.img = ImageBuffers.allocate(intr.height, intr.width, self.dev, normal=False)
+
+
+def refine(map_: GlobalSurfelMap, keyframe_ids, observations, intr: CameraIntrinsics,
+           cfg: RefinementConfig = RefinementConfig(),
+           raster_cfg: RasterConfig = DEFAULT_RASTER_CONFIG) -> RefinementReport:
+    """Backtracking GD on colours/opacities of the surfels bound to ``keyframe_ids``
+    (mapper.py:276-349).  ``observations`` maps keyframe_id -> (rgb, depth)."""
+    keyframe_ids = [k for k in keyframe_ids if k in observations]
+    poses = [map_.keyframe_poses[k] for k in keyframe_ids]
+    target_mask = np.isin(np.asarray(map_.surfels.keyframe_ids), np.asarray(keyframe_ids, dtype=np.int64))
+    n = len(map_.surfels)
+    if not keyframe_ids:
+        return RefinementReport([], float("inf"), float("inf"), 0)
+    vs = _ViewSet(intr, poses, [observations[k][0] for k in keyframe_ids],
+                  [observations[k][1] for k in keyframe_ids], raster_cfg, None)
+    dev = vs.dev
+    params = pack_params(map_.surfels, dev) if n else torch.zeros(13, device=dev)
+    P = unpack_params(params, n) if n else None
+    grads = torch.zeros_like(params)
+    loss_acc = torch.zeros(1, dtype=torch.float64, device=dev)
+    lw = cfg.loss
+
+    def view_psnrs():
+        vals = []
+        for v in range(len(poses)):
+            forward_checked(vs.view, params, n, vs.poses[v], vs.cam, vs.cfg, vs.img)
+            vals.append(psnr(vs.img.color.cpu().numpy(), observations[keyframe_ids[v]][0]))
+        finite = [x for x in vals if math.isfinite(x)]
+        return float(np.mean(finite)) if finite else float("inf")
+
+    def total_loss_and_grads():
+        grads.zero_()
+        loss_acc.zero_()
+        for v in range(len(poses)):
+            forward_checked(vs.view, params, n, vs.poses[v], vs.cam, vs.cfg, vs.img)
+            vs.view.backward(params, n, vs.img,
+                             loss_struct(N.LOSS_MSE, lw.mse, lw.depth, True, vs.rgb[v], vs.depth[v]),
+                             grads, loss_acc)
+        G = unpack_params(grads, n)
+        return float(loss_acc.item()), G["colors"].clone(), G["opacities"].clone()
+
+    psnr_before = view_psnrs()
+    if cfg.iterations == 0 or not target_mask.any() or n == 0:
+        return RefinementReport([], psnr_before, psnr_before, 0)
+    mask_t = torch.from_numpy(target_mask).to(dev)
+    loss, gc, go = total_loss_and_grads()
+    losses = [loss]
+    accepted = 0
+    step_scale = cfg.initial_step
+    for _ in range(cfg.iterations):
+        gc[~mask_t] = 0.0
+        go[~mask_t] = 0.0
+        gnorm = max(float(gc.abs().max()), float(go.abs().max()))
+        if gnorm < 1e-14:
+            break
+        step = step_scale / gnorm
+        colors0 = P["colors"].clone()
+        opac0 = P["opacities"].clone()
+        improved = False
+        while step >= cfg.min_step / gnorm:
+            P["colors"].copy_(torch.clamp(colors0 - step * gc, 0.0, 1.0))
+            P["opacities"].copy_(torch.clamp(opac0 - step * go, 0.0, 1.0))
+            new_loss, new_gc, new_go = total_loss_and_grads()
+            if new_loss < loss:
+                loss, gc, go = new_loss, new_gc, new_go
+                losses.append(loss)
+                accepted += 1
+                improved = True
+                step_scale = min(2.0 * step * gnorm, cfg.initial_step)
+                break
+            step *= 0.5
+        if not improved:
+            P["colors"].copy_(colors0)
+            P["opacities"].copy_(opac0)
+            break
+    if accepted:
+        idx = np.flatnonzero(target_mask)
+        cols = P["colors"].double().cpu().numpy()
+        ops = P["opacities"].double().cpu().numpy()
+        map_.surfels.colors = np.array(map_.surfels.colors, dtype=float, copy=True)
+        map_.surfels.opacities = np.array(map_.surfels.opacities, dtype=float, copy=True)
+        map_.surfels.colors[idx] = cols[idx]
+        map_.surfels.opacities[idx] = ops[idx]
+    return RefinementReport(losses, psnr_before, view_psnrs(), accepted)
+
+
+# --------------------------------------------------------------------------- Adam refinement
+
+
+@dataclass(frozen=True)
+class AdamConfig:
+    lr_means: float = 1e-3
+    lr_rest: float = 5e-3
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    scale_min: float = 1e-7
+
+    def struct(self) -> N.AdamCfg:
+        return N.AdamCfg(self.lr_means, self.lr_rest, self.beta1, self.beta2, self.eps, self.scale_min)
+
+
+@dataclass(frozen=True)
+class ViewLoss:
+    """Per-view loss of the Adam refinement: L1 RGB + w_depth * L1 depth (BASELINE config 4)."""
+
+    kind: str = "l1"
+    w_rgb: float = 1.0
+    w_depth: float = 0.1
+    depth_mask: bool = False
+
+    def code(self) -> int:
+        return {"l1": N.LOSS_L1, "mse": N.LOSS_MSE}[self.kind]
+
+
+class AdamRefiner:
+    """Multi-view fused-Adam refinement of all surfel parameters, views sharded over ranks.
+
+    ``targets_rgb[v]`` (H,W,3) / ``targets_depth[v]`` (H,W) may be numpy arrays, device
+    tensors, or pinned host tensors (then each step copies them in on a side stream,
+    overlapped with the previous view's compute — the end-to-end path).
+    """
+
+    def __init__(self, surfels, intr: CameraIntrinsics, poses, targets_rgb, targets_depth,
+                 loss: ViewLoss = ViewLoss(), adam: AdamConfig = AdamConfig(),
+                 raster_cfg: RasterConfig = DEFAULT_RASTER_CONFIG, mask=None, group=None, device=None,
+                 host_targets: bool = False):
+        self.ctx = DeviceContext.get(device)
+        self.dev = self.ctx.device
+        self.group = group
+        self.rank, self.world_size = world(group)
+        self.intr = intr
+        self.cam = camera_struct(intr)
+        self.cfg = config_struct(raster_cfg)
+        if isinstance(surfels, torch.Tensor):
+            self.params = surfels.to(self.dev, torch.float32).contiguous()
+            self.n = self.params.numel() // 13
+        else:
+            self.n = len(surfels)
+            self.params = pack_params(surfels, self.dev)
+        self.grads = torch.zeros_like(self.params)
+        self.m1 = torch.zeros_like(self.params)
+        self.m2 = torch.zeros_like(self.params)
+        self.mask = None if mask is None else torch.as_tensor(np.asarray(mask, dtype=np.uint8)).to(self.dev)
+        self.all_poses = [as_packed_pose(p) for p in poses]
+        self.my_views = shard_views(len(self.all_poses), self.rank, self.world_size)
+        self.loss_cfg = loss
+        self.adam = adam.struct()
+        self.host_targets = host_targets
+        h, w = intr.height, intr.width
+        self.rgb, self.depth = {}, {}
+        for v in self.my_views:
+            r, d = targets_rgb[v], targets_depth[v]
+            if host_targets:
+                r = torch.as_tensor(np.asarray(r, dtype=np.float32)) if not isinstance(r, torch.Tensor) else r
+                d = torch.as_tensor(np.asarray(d, dtype=np.float32)) if not isinstance(d, torch.Tensor) else d
+                self.rgb[v] = r.float().contiguous().pin_memory()
+                self.depth[v] = d.float().contiguous().pin_memory()
+            else:
+                self.rgb[v] = torch.as_tensor(np.asarray(r, dtype=np.float32) if not isinstance(r, torch.Tensor) else r).to(self.dev, torch.float32)
+                self.depth[v] = torch.as_tensor(np.asarray(d, dtype=np.float32) if not isinstance(d, torch.Tensor) else d).to(self.dev, torch.float32)
+        if host_targets:
+            self.stage_rgb = [torch.empty((h, w, 3), device=self.dev) for _ in range(2)]
+            self.stage_depth = [torch.empty((h, w), device=self.dev) for _ in range(2)]
+            self.copy_stream = torch.cuda.Stream(self.dev)
+            self.copy_done = [torch.cuda.Event() for _ in range(2)]
+            self.stage_free = [torch.cuda.Event() for _ in range(2)]
+        self.view = View(self.ctx)
+        self.img = ImageBuffers.allocate(h, w, self.dev, normal=False)
+        self.loss_acc = torch.zeros(1, dtype=torch.float64, device=self.dev)
+        self.stats_acc = torch.zeros(8, dtype=torch.int32, device=self.dev)
+        self.host_stats = torch.zeros(8, dtype=torch.int32).pin_memory()
+        self.host_loss = torch.zeros(1, dtype=torch.float64).pin_memory()
+        self.step_count = 0
+        self.h2d_bytes_per_step = (sum(self.rgb[v].numel() + self.depth[v].numel() for v in self.my_views) * 4
+                                   if host_targets else 0)
+        self._size_pairs()
+
+    def _size_pairs(self):
+        """One forward per view to size the pair capacity (1.3 x the largest view)."""
+        mx = 0
+        for v in self.my_views:
+            st = forward_checked(self.view, self.params, self.n, self.all_poses[v], self.cam, self.cfg, self.img)
+            mx = max(mx, st.pairs)
+        self.view.reserve_pairs(int(mx * 1.3) + 4096)
+
+    def _targets(self, j, v):
+        if not self.host_targets:
+            return self.rgb[v], self.depth[v]
+        return self.stage_rgb[j & 1], self.stage_depth[j & 1]
+
+    def _issue_copy(self, j, v):
+        b = j & 1
+        cs = self.copy_stream
+        cs.wait_event(self.stage_free[b])
+        with torch.cuda.stream(cs):
+            self.stage_rgb[b].copy_(self.rgb[v], non_blocking=True)
+            self.stage_depth[b].copy_(self.depth[v], non_blocking=True)
+            self.copy_done[b].record(cs)
+
+    def compute_grads(self):
+        """grads <- sum over this rank's views of d(loss)/d(params); loss_acc <- sum of losses."""
+        stream = torch.cuda.current_stream(self.dev)
+        self.grads.zero_()
+        self.loss_acc.zero_()
+        self.stats_acc.zero_()
+        lc = self.loss_cfg
+        views = self.my_views
+        if self.host_targets:
+            for b in range(2):
+                self.stage_free[b].record(stream)
+            if views:
+                self._issue_copy(0, views[0])
+        for j, v in enumerate(views):
+            if self.host_targets:
+                if j + 1 < len(views):
+                    self._issue_copy(j + 1, views[j + 1])
+                stream.wait_event(self.copy_done[j & 1])
+            trgb, tdep = self._targets(j, v)
+            self.view.forward(self.params, self.n, self.all_poses[v], self.cam, self.cfg, self.img)
+            self.view.accumulate_stats(self.stats_acc)
+            self.view.backward(self.params, self.n, self.img,
+                               loss_struct(lc.code(), lc.w_rgb, lc.w_depth, lc.depth_mask, trgb, tdep),
+                               self.grads, self.loss_acc)
+            if self.host_targets:
+                self.stage_free[j & 1].record(stream)
+
+    def step(self) -> float:
+        """One refine iteration; returns the total loss over ALL views (all ranks)."""
+        for _ in range(3):
+            self.compute_grads()
+            self.host_stats.copy_(self.stats_acc, non_blocking=True)
+            torch.cuda.current_stream(self.dev).synchronize()
+            if not int(self.host_stats[4]):
+                break
+            self.view.reserve_pairs(int(self.host_stats[1]) * 5 // 4 + 4096)
+        allreduce_grads(self.grads, self.loss_acc, self.group)
+        self.step_count += 1
+        N.check(N.lib().s2d_adam_step(torch.cuda.current_stream(self.dev).cuda_stream, N.dptr(self.params),
+                                      N.dptr(self.grads), N.dptr(self.m1), N.dptr(self.m2), self.n,
+                                      self.step_count, self.adam, N.dptr(self.mask)), "s2d_adam_step")
+        self.host_loss.copy_(self.loss_acc, non_blocking=True)
+        torch.cuda.current_stream(self.dev).synchronize()
+        return float(self.host_loss[0])
+
+    def surfel_arrays(self) -> SurfelArrays:
+        P = unpack_params(self.params, self.n)
+        return SurfelArrays(*[P[k].double().cpu().numpy() for k in ("means", "quats", "scales", "opacities",
+                                                                     "colors")])
