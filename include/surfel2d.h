@@ -135,7 +135,8 @@ int s2d_view_stats_host(s2d_view *view, s2d_view_stats *out);
  * visible/pairs/pairs_stored = max, degenerate/n_mask/guard_hits = sum, overflow = or.
  * Lets a multi-view step check capacity once per iteration instead of per view. */
 int s2d_view_stats_accumulate(s2d_view *view, void *stream, s2d_view_stats *acc_device);
-/* grow the pair capacity used by the next forward (after stats.overflow) */
+/* set the (tile, surfel) pair capacity used by the next forward (>= 1024); after
+ * stats.overflow the caller re-runs the view with a larger capacity */
 int s2d_view_reserve_pairs(s2d_view *view, int64_t pairs);
 int s2d_view_inspect(s2d_view *view, s2d_view_debug *out);
 

@@ -280,9 +280,7 @@ int ensure_capacity(s2d_view *v, int64_t n, int64_t npx, int ntiles) {
     }
     if ((rc = grow(v->grad2d, v->cap_grad, nn * 16, /*zero=*/true))) return rc;
     if ((rc = grow(v->aux, v->cap_aux, npx))) return rc;
-    int64_t want = 4 * nn;
-    if (want < 65536) want = 65536;
-    if (v->pcap < want) v->pcap = want;
+    if (v->pcap == 0) v->pcap = 4 * nn < 65536 ? 65536 : 4 * nn;  // first guess; regrown on overflow
     for (int b = 0; b < 2; ++b) {
         if ((rc = grow(v->pkeys[b], v->cap_pk[b], v->pcap))) return rc;
         if ((rc = grow(v->pvals[b], v->cap_pv[b], v->pcap))) return rc;
@@ -488,7 +486,7 @@ int s2d_view_stats_accumulate(s2d_view *v, void *stream, s2d_view_stats *acc_dev
 int s2d_view_reserve_pairs(s2d_view *v, int64_t pairs) {
     if (!v) return fail(S2D_ERR_INVALID, "NULL view");
     if (pairs > ((int64_t)1 << 30)) return fail(S2D_ERR_INVALID, "pair capacity too large");
-    if (pairs > v->pcap) v->pcap = pairs;
+    v->pcap = pairs < 1024 ? 1024 : pairs;
     return S2D_OK;
 }
 

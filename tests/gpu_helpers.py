@@ -1,0 +1,68 @@
+"""Helpers shared by the GPU tests (call the product through the C ABI)."""
+import numpy as np
+import torch
+
+from paper_2604_03092_b200 import _native as N
+from paper_2604_03092_b200.engine import (DeviceContext, ImageBuffers, View, camera_struct, config_struct,
+                                          forward_checked, pack_params, unpack_params)
+from paper_2604_03092_b200.rasterizer import DEFAULT_RASTER_CONFIG
+
+
+class Run:
+    """One forward (and optionally backward) of a scene on the GPU, with introspection."""
+
+    def __init__(self, surfels, pose, intr, cfg=DEFAULT_RASTER_CONFIG, normal=True, argmax=True, view=None):
+        self.ctx = DeviceContext.get()
+        self.dev = self.ctx.device
+        self.view = view or View(self.ctx)
+        self.n = len(surfels)
+        self.params = pack_params(surfels, self.dev) if self.n else torch.zeros(13, device=self.dev)
+        self.intr = intr
+        self.img = ImageBuffers.allocate(intr.height, intr.width, self.dev, normal=normal, argmax=argmax)
+        self.stats = forward_checked(self.view, self.params, self.n, pose, camera_struct(intr), config_struct(cfg),
+                                     self.img)
+
+    def images(self):
+        out = {k: getattr(self.img, k).double().cpu().numpy() for k in ("color", "depth", "accumulation")}
+        if self.img.normal is not None:
+            out["normal"] = self.img.normal.double().cpu().numpy()
+        if self.img.arg_w is not None:
+            out["arg_w"] = self.img.arg_w.cpu().numpy().astype(np.int64)
+            out["max_w"] = self.img.max_w.double().cpu().numpy()
+        return out
+
+    def inspect(self):
+        return self.view.inspect()
+
+    def backward(self, kind="mse", trgb=None, tdep=None, w_rgb=1.0, w_depth=0.05, depth_mask=True,
+                 d_color=None, d_depth=None, d_normal=None, d_acc=None):
+        grads = torch.zeros_like(self.params)
+        loss = torch.zeros(1, dtype=torch.float64, device=self.dev)
+        t = lambda a: None if a is None else torch.as_tensor(np.asarray(a, dtype=np.float32)).to(self.dev)  # noqa: E731
+        keep = [t(trgb), t(tdep), t(d_color), t(d_depth), t(d_normal), t(d_acc)]
+        code = {"mse": N.LOSS_MSE, "l1": N.LOSS_L1, "external": N.LOSS_EXTERNAL}[kind]
+        ls = N.Loss(code, int(depth_mask), float(w_rgb), float(w_depth), *[N.dptr(k) for k in keep])
+        self.view.backward(self.params, self.n, self.img, ls, grads, loss)
+        torch.cuda.synchronize()
+        g = {k: v.double().cpu().numpy() for k, v in unpack_params(grads, self.n).items()}
+        return g, float(loss.item())
+
+
+def far_targets(ref_color, ref_depth, rng, gap=0.05):
+    """Targets bounded away from the render (|C - C*| >= gap): L1 seeds have no sign ambiguity."""
+    s = rng.choice([-1.0, 1.0], size=ref_color.shape)
+    trgb = ref_color + s * (gap + np.abs(rng.normal(0, 0.02, ref_color.shape)))
+    sd = rng.choice([-1.0, 1.0], size=ref_depth.shape)
+    tdep = ref_depth + sd * (gap + np.abs(rng.normal(0, 0.02, ref_depth.shape)))
+    return trgb, tdep
+
+
+def gate(a, b, tol=1e-4):
+    """Parity gate: max|d| <= tol*max|ref| and ||d||/||ref|| <= tol."""
+    a = np.asarray(a, dtype=float)
+    b = np.asarray(b, dtype=float)
+    if b.size == 0:
+        return True, 0.0, 0.0
+    mx = np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
+    l2 = np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+    return (mx <= tol and l2 <= tol), mx, l2

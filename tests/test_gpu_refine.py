@@ -1,0 +1,140 @@
+"""refine (reference semantics, mapper.py:276-349) and the multi-view AdamRefiner on the GPU."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from gpu_helpers import Run, gate
+from paper_2604_03092_b200 import rasterizer as R
+from paper_2604_03092_b200 import scenes
+from paper_2604_03092_b200.engine import unpack_params
+from paper_2604_03092_b200.geometry import Sim3Transform
+from paper_2604_03092_b200.mapper import (AdamConfig, AdamRefiner, GlobalSurfelMap, RefinementConfig, ViewLoss,
+                                          refine)
+
+pytestmark = pytest.mark.gpu
+
+
+def small_map(seed=0):
+    rng = np.random.default_rng(seed)
+    intr = R.CameraIntrinsics(75.0, 75.0, 48.0, 36.0, 96, 72)
+    surf, _ = scenes.depth_field_surfels(rng, intr)
+    poses = {0: Sim3Transform.identity(), 6: scenes._small_pose(rng, 4.0, 0.1)}
+    surf.keyframe_ids = np.array([(0, 6)[i % 2] for i in range(len(surf))], dtype=np.int64)
+    m = GlobalSurfelMap(surf, dict(poses))
+    return m, intr, rng
+
+
+def observations(m, intr, frames):
+    obs = {}
+    for f in frames:
+        b = R.render(m.surfels, m.keyframe_poses[f], intr)
+        obs[f] = (b.color, b.depth / np.maximum(b.accumulation, 1e-12))
+    return obs
+
+
+def test_refine_recovers_psnr_with_decreasing_loss():
+    m, intr, rng = small_map(0)
+    obs = observations(m, intr, [0, 6])
+    m.surfels.colors = np.clip(m.surfels.colors + rng.uniform(-0.15, 0.15, m.surfels.colors.shape), 0, 1)
+    rep = refine(m, [0, 6], obs, intr, RefinementConfig(iterations=10))
+    assert rep.psnr_after - rep.psnr_before >= 1.0, (rep.psnr_before, rep.psnr_after)
+    assert all(b < a for a, b in zip(rep.losses, rep.losses[1:]))
+    assert rep.accepted_steps >= 1
+
+
+def test_refine_zero_iterations_bitwise_noop():
+    m, intr, rng = small_map(1)
+    obs = observations(m, intr, [0])
+    c0, o0 = m.surfels.colors.tobytes(), m.surfels.opacities.tobytes()
+    refine(m, [0], obs, intr, RefinementConfig(iterations=0))
+    assert m.surfels.colors.tobytes() == c0 and m.surfels.opacities.tobytes() == o0
+
+
+def test_refine_untargeted_untouched_and_stationary():
+    m, intr, rng = small_map(2)
+    m.surfels.colors = np.clip(m.surfels.colors + rng.uniform(-0.2, 0.2, m.surfels.colors.shape), 0, 1)
+    outside = m.surfels.keyframe_ids == 6
+    before = m.surfels.colors[outside].copy()
+    obs = observations(m, intr, [0])
+    obs = {0: (np.clip(obs[0][0] + 0.05, 0, 1), obs[0][1])}
+    refine(m, [0], obs, intr, RefinementConfig(iterations=3))
+    assert np.array_equal(m.surfels.colors[outside], before)
+    # targets = the map's own renders: exact stationary point (no accepted step changes the loss)
+    m2, intr2, _ = small_map(3)
+    own = {}
+    for f in (0, 6):
+        b = R.render(m2.surfels, m2.keyframe_poses[f], intr2)
+        own[f] = (b.color, b.depth)
+    rep = refine(m2, [0, 6], own, intr2, RefinementConfig(iterations=3, loss=R.LossWeights(1.0, 0.0)))
+    assert len(rep.losses) <= 1 or rep.losses[-1] - rep.losses[0] < 1e-10
+
+
+def _c4_small(seed=0, views=4):
+    sc = scenes.config4(seed, n_keyframes=2, per_keyframe=20_000, n_views=views)
+    dev = torch.device("cuda", 0)
+    import bench
+    rgbs, deps = bench.render_targets(sc, dev)
+    return sc, rgbs, deps
+
+
+def test_adam_refiner_grads_are_sum_of_views_and_step_matches_oracle_adam():
+    sc, rgbs, deps = _c4_small(0, 3)
+    ref = AdamRefiner(sc.extra["perturbed"], sc.intr, sc.poses, rgbs, deps, ViewLoss("mse", 1.0, 0.1, True),
+                      AdamConfig())
+    ref.compute_grads()
+    torch.cuda.synchronize()
+    total = ref.grads.double().cpu().numpy().copy()
+    acc = np.zeros_like(total)
+    for v, pose in enumerate(sc.poses):
+        run = Run(sc.extra["perturbed"], pose, sc.intr, normal=False, argmax=False)
+        g, _ = run.backward("mse", rgbs[v].cpu().numpy(), deps[v].cpu().numpy(), 1.0, 0.1, True)
+        acc += np.concatenate([g[k].ravel() for k in ("means", "quats", "scales", "opacities", "colors")])
+    ok, mx, l2 = gate(total, acc, tol=1e-5)
+    assert ok, (mx, l2)
+    # one fused Adam step vs the float64 oracle Adam on the same gradients
+    p0 = ref.params.double().cpu().numpy().copy()
+    ref.step()
+    p = p0.copy()
+    g = ref.grads.double().cpu().numpy()
+    m1 = np.zeros_like(p)
+    m2 = np.zeros_like(p)
+    O.adam_step(p, g, m1, m2, 1, 1e-3, 5e-3, 0.9, 0.999, 1e-8, 1e-7)
+    got = ref.params.double().cpu().numpy()
+    assert np.max(np.abs(got - p)) <= 2e-6, np.max(np.abs(got - p))
+
+
+def test_adam_refiner_loss_decreases_and_mask_freezes():
+    sc, rgbs, deps = _c4_small(1, 4)
+    n = len(sc.surfels)
+    mask = np.zeros(n, bool)
+    mask[: n // 2] = True
+    ref = AdamRefiner(sc.extra["perturbed"], sc.intr, sc.poses, rgbs, deps, ViewLoss(), AdamConfig(), mask=mask)
+    frozen0 = ref.params.view(13, -1) if False else None
+    P0 = {k: v.clone() for k, v in unpack_params(ref.params, n).items()}
+    losses = [ref.step() for _ in range(8)]
+    assert losses[-1] < losses[0]
+    P1 = unpack_params(ref.params, n)
+    for k in P0:
+        assert torch.equal(P0[k][n // 2:], P1[k][n // 2:]), k
+        assert not torch.equal(P0[k][: n // 2], P1[k][: n // 2]), k
+    q = P1["quats"][: n // 2]
+    assert torch.allclose(q.norm(dim=1), torch.ones_like(q[:, 0]), atol=1e-5)
+    assert float(P1["opacities"].min()) >= 0 and float(P1["opacities"].max()) <= 1
+    assert frozen0 is None
+
+
+def test_host_target_path_matches_device_path():
+    sc, rgbs, deps = _c4_small(2, 3)
+    a = AdamRefiner(sc.extra["perturbed"], sc.intr, sc.poses, rgbs, deps)
+    b = AdamRefiner(sc.extra["perturbed"], sc.intr, sc.poses, [r.cpu() for r in rgbs], [d.cpu() for d in deps],
+                    host_targets=True)
+    assert b.h2d_bytes_per_step == sum(r.numel() + d.numel() for r, d in zip(rgbs, deps)) * 4
+    for _ in range(3):
+        la, lb = a.step(), b.step()
+        assert abs(la - lb) <= 1e-6 * abs(la)
+    # float atomics reorder sums; Adam maps a near-zero gradient's sign to a full lr step, so
+    # compare statistically: almost all parameters agree to 1e-6, none by more than 3 steps
+    d = (a.params - b.params).abs()
+    assert float((d > 1e-6).float().mean()) < 1e-3
+    assert float(d.max()) <= 3 * 2 * 5e-3

@@ -1,0 +1,21 @@
+"""Short config-4 refine workload for ncu (profiled region = one refine iteration over 4 views)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2604_03092_b200 import scenes
+from paper_2604_03092_b200.mapper import AdamRefiner, ViewLoss, AdamConfig
+import bench
+
+nviews = int(os.environ.get("PROFILE_VIEWS", "4"))
+sc = scenes.config4(0)
+sc.poses = sc.poses[12:12 + nviews]
+rgbs, deps = bench.render_targets(sc, torch.device("cuda", 0))
+ref = AdamRefiner(sc.extra["perturbed"], sc.intr, sc.poses, rgbs, deps, ViewLoss(), AdamConfig())
+for _ in range(2):
+    ref.step()
+torch.cuda.synchronize()
+torch.cuda.profiler.start()
+ref.step()
+torch.cuda.synchronize()
+torch.cuda.profiler.stop()
+print("profile_view done")
