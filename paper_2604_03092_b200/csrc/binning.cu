@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(kProjThreads) k_project(const ProjectArgs a) {
     const int tile = s_tile;
     const int64_t i = (int64_t)tile * kProjThreads + threadIdx.x;
     const ViewParams &P = a.P;
+    if (tile == 0 && threadIdx.x == 0) *a.P_out = a.P;
     bool on = false, degen = false;
     ExactProj e;
     if (i < P.n) {

@@ -249,6 +249,7 @@ int layout_sync(s2d_view *v, int64_t n, int64_t pcap, int ntiles) {
     const size_t o_pstat = take((size_t)2 * psort_tiles * kRadix * 4);
     const size_t o_claim = take((size_t)(n + 1) * 4);
     const size_t o_ranges = take((size_t)ntiles * sizeof(int2));
+    const size_t o_params = take(sizeof(ViewParams));
     int64_t need = (int64_t)off;
     int rc = grow(v->sync, v->cap_sync, need);
     if (rc) return rc;
@@ -263,6 +264,7 @@ int layout_sync(s2d_view *v, int64_t n, int64_t pcap, int ntiles) {
     v->sr.pair_status = reinterpret_cast<uint32_t *>(b + o_pstat);
     v->sr.tie_claim = reinterpret_cast<uint32_t *>(b + o_claim);
     v->sr.ranges = reinterpret_cast<int2 *>(b + o_ranges);
+    v->sr.params = reinterpret_cast<ViewParams *>(b + o_params);
     v->sr.bytes = off;
     return S2D_OK;
 }
@@ -320,6 +322,7 @@ int view_forward(s2d_view *v, cudaStream_t s, const float *params, int64_t n, co
     if (n > 0) {
         ProjectArgs pa;
         pa.P = P;
+        pa.P_out = sr.params;
         pa.params = params;
         pa.rec = v->rec;
         pa.rect = v->rect;
@@ -382,6 +385,7 @@ int view_forward(s2d_view *v, cudaStream_t s, const float *params, int64_t n, co
     RasterArgs ra;
     memset(&ra, 0, sizeof(ra));
     ra.P = P;
+    ra.Pg = sr.params;
     ra.params = params;
     ra.ranges = sr.ranges;
     ra.pair_ids = v->pvals[v->pair_buf];
@@ -565,6 +569,7 @@ int s2d_backward(s2d_view *v, void *stream, const float *params, int64_t n, cons
     RasterArgs ra;
     memset(&ra, 0, sizeof(ra));
     ra.P = v->P;
+    ra.Pg = v->sr.params;
     ra.params = params;
     ra.ranges = v->sr.ranges;
     ra.pair_ids = v->pvals[v->pair_buf];

@@ -1,7 +1,7 @@
 // optim.cu — projection backward (N2) and the fused Adam step (N4).
 //
 // k_project_bwd: per on-screen surfel, chains the per-view 2D gradients
-//   [dL/d opacity, dL/d rgb(3), dL/dz, dL/d normal(3), dL/d Minv(4), dL/d centre(2)]
+//   [dL/d opacity, dL/d rgb(3), dL/dz, dL/d Minv(4), dL/d centre(2), dL/d normal(3)]
 // through Minv = (J(p) Bc)^-1, centre(p), z, normal = R_cw R(q)[:,2] back to
 // the parameters (means, raw quats, scales, opacity, colours), in float64, and
 // ACCUMULATES into the packed gradient block (views sum with no extra pass,
@@ -65,7 +65,8 @@ __global__ void __launch_bounds__(128) k_project_bwd(const ProjectBwdArgs a) {
     const double M11 = e.J[1][1] * e.Bc[1][1] + e.J[1][2] * e.Bc[2][1];
     const double id = 1.0 / (M00 * M11 - M01 * M10);
     const double N[2][2] = {{M11 * id, -M01 * id}, {-M10 * id, M00 * id}};
-    const double GN[2][2] = {{G2.x, G2.y}, {G2.z, G2.w}};
+    // 2D gradient record: [opacity, rgb(3), z, Minv A,B,C,D, centre x,y, normal(3), -, -]
+    const double GN[2][2] = {{G1.y, G1.z}, {G1.w, G2.x}};
     // dL/dM = -N^T GN N^T
     double T[2][2], GM[2][2];
 #pragma unroll
@@ -110,7 +111,7 @@ __global__ void __launch_bounds__(128) k_project_bwd(const ProjectBwdArgs a) {
         for (int k = 0; k < 3; ++k)
             nn[k] = P.r_cw[3 * k] * e.R[2] + P.r_cw[3 * k + 1] * e.R[5] + P.r_cw[3 * k + 2] * e.R[8];
         const double sg = (nn[0] * e.p[0] + nn[1] * e.p[1] + nn[2] * e.p[2]) > 0.0 ? -1.0 : 1.0;
-        const double gn[3] = {G1.y, G1.z, G1.w};
+        const double gn[3] = {G2.w, G3.x, G3.y};
 #pragma unroll
         for (int b = 0; b < 3; ++b)
             gR[3 * b + 2] = sg * (P.r_cw[b] * gn[0] + P.r_cw[3 + b] * gn[1] + P.r_cw[6 + b] * gn[2]);
@@ -128,10 +129,10 @@ __global__ void __launch_bounds__(128) k_project_bwd(const ProjectBwdArgs a) {
     gp2 += gJ[0][0] * (-fx * iz2) + gJ[0][2] * (2.0 * fx * x * iz3);
     gp1 += gJ[1][2] * (-fy * iz2);
     gp2 += gJ[1][1] * (-fy * iz2) + gJ[1][2] * (2.0 * fy * y * iz3);
-    gp0 += (double)G3.x * (fx * iz);
-    gp2 += (double)G3.x * (-fx * x * iz2);
-    gp1 += (double)G3.y * (fy * iz);
-    gp2 += (double)G3.y * (-fy * y * iz2);
+    gp0 += (double)G2.y * (fx * iz);
+    gp2 += (double)G2.y * (-fx * x * iz2);
+    gp1 += (double)G2.z * (fy * iz);
+    gp2 += (double)G2.z * (-fy * y * iz2);
     // p = s_inv R(q_inv) mu + t_inv
 #pragma unroll
     for (int b = 0; b < 3; ++b)

@@ -43,13 +43,29 @@ __device__ __forceinline__ void cp_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// Reference Mahalanobis distance of pixel (x, y) to surfel `id`, float64 (guard band path).
-__device__ __noinline__ double exact_m_at(const ViewParams &P, const float *params, uint32_t id,
+// Guard-band resolution (rare path, kept out of line so the hot loop stays lean):
+// re-takes the reference's decisions for pixel (x, y) and surfel `id` in float64 with the
+// reference's own formulas.  bit0: the pair blends (pixel inside the reference bbox and
+// m <= sigma^2, _raster_kernels.py:32-41); bit1: the weight clamps (w > weight_clamp, :43-44).
+// Takes the view constants from GLOBAL memory: passing the by-value kernel parameter by
+// reference to an out-of-line function would force a copy of it to local memory in every thread.
+__device__ __noinline__ int guard_resolve(const ViewParams *__restrict__ Pg, const float *params, uint32_t id,
                                           int x, int y) {
+    const ViewParams &P = *Pg;
     const ParamView pv(params, P.n);
     ExactProj e;
     project_exact(P, pv, id, e);
-    return exact_maha(e, x, y);
+    if (x < e.x0 || x > e.x1 || y < e.y0 || y > e.y1) return 0;
+    const double m64 = exact_maha(e, x, y);
+    if (m64 > P.maha_cut) return 0;
+    const double w64 = (double)pv.opac[id] * exp(-0.5 * m64);
+    return 1 | (w64 > P.w_clamp ? 2 : 0);
+}
+
+__device__ __forceinline__ float fast_exp2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
 }
 
 struct Stage {
@@ -72,17 +88,19 @@ __device__ __forceinline__ void stage_issue(Stage &st, int buf, int k, uint32_t 
     st.id[buf][k] = id;
 }
 
-// Per-pixel evaluation shared by forward and backward (must make identical decisions).
-// Returns false if the pair does not blend.  Outputs m-space intermediates.
+// Per-pixel evaluation shared by forward and backward (must take identical decisions).
+// Fast path: m = |Minv d|^2 in float32.  m < cut - gb implies the reference's float64 m is
+// below the cut, hence the pixel lies inside the reference bbox (the bbox is the ellipse's
+// exact extent), so no bbox test is needed; m > cut + gb rejects.  Inside the band, or when
+// the weight is within 4e-6 of the clamp, guard_resolve decides in float64.
 struct PairEval {
     float dx, dy, u, v, g, w;
     bool clamped;
 };
 
-__device__ __forceinline__ bool eval_pair(const ViewParams &P, const float *params, const SplatRecord &r,
-                                          const short4 &bb, uint32_t id, int px, int py, PairEval &o,
+__device__ __forceinline__ bool eval_pair(const ViewParams &P, const ViewParams *Pg, const float *params,
+                                          const SplatRecord &r, uint32_t id, int px, int py, PairEval &o,
                                           int &guard_hits) {
-    if (px < bb.x || px > bb.y || py < bb.z || py > bb.w) return false;
     const uint32_t lob = __float_as_uint(r.q0.z);
     const __half2 lo = *reinterpret_cast<const __half2 *>(&lob);
     // explicit round-to-nearest intrinsics: forward and backward must take
@@ -94,19 +112,13 @@ __device__ __forceinline__ bool eval_pair(const ViewParams &P, const float *para
     const float m = __fmaf_rn(o.u, o.u, __fmul_rn(o.v, o.v));
     const float gb = r.q3.w;
     if (m > P.maha_cut_f + gb) return false;
-    double m64 = -1.0;
-    if (m >= P.maha_cut_f - gb) {
-        ++guard_hits;
-        m64 = exact_m_at(P, params, id, px, py);
-        if (m64 > P.maha_cut) return false;
-    }
-    o.g = __expf(__fmul_rn(-0.5f, m));
+    o.g = fast_exp2(__fmul_rn(m, -0.72134752044448170368f));  // exp(-m/2); m <= sigma^2 + gb keeps it normal
     float w = __fmul_rn(r.q0.w, o.g);
-    o.clamped = false;
-    if (fabsf(w - P.w_clamp_f) <= 4e-6f) {
+    if ((m >= P.maha_cut_f - gb) | (fabsf(w - P.w_clamp_f) <= 4e-6f)) {
         ++guard_hits;
-        if (m64 < 0.0) m64 = exact_m_at(P, params, id, px, py);
-        o.clamped = (double)r.q0.w * exp(-0.5 * m64) > P.w_clamp;
+        const int rr = guard_resolve(Pg, params, id, px, py);
+        if (!(rr & 1)) return false;
+        o.clamped = (rr & 2) != 0;
     } else {
         o.clamped = w > P.w_clamp_f;
     }
@@ -115,9 +127,32 @@ __device__ __forceinline__ bool eval_pair(const ViewParams &P, const float *para
     return w > 0.0f;
 }
 
-template <bool kArg, bool kMaxW>
-__global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(const RasterArgs a) {
+// Ordered list (into s_list) of the staged records whose integer bbox touches the warp's
+// 8x4 pixel block; returns its length.  `limit` excludes list positions > limit (backward).
+__device__ __forceinline__ int warp_cull(const short4 *rect, int nrec, int wx0, int wx1, int wy0, int wy1,
+                                         int lane, uint8_t *list, int base_pos, int limit) {
+    const uint32_t lt = lanemask_lt();
+    int cnt = 0;
+#pragma unroll
+    for (int q = 0; q < kRasterThreads / 32; ++q) {
+        const int k = q * 32 + lane;
+        bool hit = false;
+        if (k < nrec && base_pos + k <= limit) {
+            const short4 r = rect[k];
+            hit = (r.x <= wx1) & (r.y >= wx0) & (r.z <= wy1) & (r.w >= wy0);
+        }
+        const uint32_t m = __ballot_sync(kFull, hit);
+        if (hit) list[cnt + __popc(m & lt)] = (uint8_t)k;
+        cnt += __popc(m);
+    }
+    __syncwarp();
+    return cnt;
+}
+
+template <bool kArg, bool kMaxW, bool kNormal>
+__global__ void __launch_bounds__(kRasterThreads, 3) k_raster_fwd(const RasterArgs a) {
     __shared__ Stage st;
+    __shared__ uint8_t s_list[kRasterThreads / 32][kRasterThreads];
     const ViewParams &P = a.P;
     const int tile = blockIdx.x;
     const int tx = tile % P.ntx, ty = tile / P.ntx;
@@ -133,8 +168,9 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(const RasterArgs 
     float c0 = 0.f, c1 = 0.f, c2 = 0.f, dep = 0.f, n0 = 0.f, n1 = 0.f, n2 = 0.f;
     float maxw = 0.f;
     int argw = -1, last = -1, guard = 0;
-    bool done = !inside || (T < P.term_t_f);
+    bool done = !inside;
     const float term_t = P.term_t_f;
+    uint8_t *list = s_list[warp];
 
     const int nb = (cnt + kRasterThreads - 1) / kRasterThreads;
     if (nb > 0) {
@@ -156,72 +192,57 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(const RasterArgs 
             const int base = b * kRasterThreads;
             const int nrec = min(kRasterThreads, cnt - base);
             if (!__all_sync(kFull, done)) {
-                uint32_t mask[8];
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const int k = q * 32 + lane;
-                    bool hit = false;
-                    if (k < nrec) {
-                        const short4 r = st.rect[buf][k];
-                        hit = (r.x <= wx1) & (r.y >= wx0) & (r.z <= wy1) & (r.w >= wy0);
-                    }
-                    mask[q] = __ballot_sync(kFull, hit);
-                }
-#pragma unroll 1
-                for (int q = 0; q < 8; ++q) {
-                    uint32_t m = mask[q];
-                    while (m) {
-                        const int k = q * 32 + __ffs(m) - 1;
-                        m &= m - 1;
-                        const uint32_t id = st.id[buf][k];
-                        float contrib = 0.f;
-                        if (!done) {
-                            PairEval e;
-                            const SplatRecord &r = st.rec[buf][k];
-                            if (eval_pair(P, a.params, r, st.rect[buf][k], id, px, py, e, guard)) {
-                                contrib = e.w * T;
-                                const float4 q2 = r.q2, q3 = r.q3;
-                                c0 = fmaf(contrib, q2.x, c0);
-                                c1 = fmaf(contrib, q2.y, c1);
-                                c2 = fmaf(contrib, q2.z, c2);
-                                dep = fmaf(contrib, q2.w, dep);
+                const int nl = warp_cull(st.rect[buf], nrec, wx0, wx1, wy0, wy1, lane, list, 0, nrec);
+                for (int j = 0; j < nl; ++j) {
+                    const int k = list[j];
+                    const uint32_t id = st.id[buf][k];
+                    float contrib = 0.f;
+                    if (!done) {
+                        PairEval e;
+                        const SplatRecord &r = st.rec[buf][k];
+                        if (eval_pair(P, a.Pg, a.params, r, id, px, py, e, guard)) {
+                            contrib = e.w * T;
+                            const float4 q2 = r.q2;
+                            c0 = fmaf(contrib, q2.x, c0);
+                            c1 = fmaf(contrib, q2.y, c1);
+                            c2 = fmaf(contrib, q2.z, c2);
+                            dep = fmaf(contrib, q2.w, dep);
+                            if (kNormal) {
+                                const float4 q3 = r.q3;
                                 n0 = fmaf(contrib, q3.x, n0);
                                 n1 = fmaf(contrib, q3.y, n1);
                                 n2 = fmaf(contrib, q3.z, n2);
-                                if (kArg && contrib > maxw) {
-                                    maxw = contrib;
-                                    argw = (int)id;
-                                }
-                                Tpre = T;
-                                T = T * (1.0f - e.w);
-                                last = rg.x + base + k;
-                                done = T < term_t;
                             }
-                        }
-                        if (kMaxW) {
-                            float mx = contrib;
-                            float mm = (a.mask != nullptr && inside && a.mask[py * P.W + px]) ? contrib : 0.f;
-#pragma unroll
-                            for (int o = 16; o > 0; o >>= 1) {
-                                mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
-                                mm = fmaxf(mm, __shfl_xor_sync(kFull, mm, o));
+                            if (kArg && contrib > maxw) {
+                                maxw = contrib;
+                                argw = (int)id;
                             }
-                            if (lane == 0) {
-                                if (mx > 0.f) atomicMax(reinterpret_cast<int *>(a.max_all + id), __float_as_int(mx));
-                                if (mm > 0.f && a.max_marked)
-                                    atomicMax(reinterpret_cast<int *>(a.max_marked + id), __float_as_int(mm));
-                            }
-                        }
-                        if (__all_sync(kFull, done)) {
-                            m = 0;
-                            q = 8;
+                            Tpre = T;
+                            T = T * (1.0f - e.w);
+                            last = rg.x + base + k;
+                            done = T < term_t;
                         }
                     }
+                    if (kMaxW) {
+                        float mx = contrib;
+                        float mm = (a.mask != nullptr && inside && a.mask[py * P.W + px]) ? contrib : 0.f;
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) {
+                            mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
+                            mm = fmaxf(mm, __shfl_xor_sync(kFull, mm, o));
+                        }
+                        if (lane == 0) {
+                            if (mx > 0.f) atomicMax(reinterpret_cast<int *>(a.max_all + id), __float_as_int(mx));
+                            if (mm > 0.f && a.max_marked)
+                                atomicMax(reinterpret_cast<int *>(a.max_marked + id), __float_as_int(mm));
+                        }
+                    }
+                    if (__all_sync(kFull, done)) break;
                 }
             }
             if (__syncthreads_and(done)) break;
         }
-        cp_wait<0>();
+    cp_wait<0>();
     }
     if (inside) {
         const int p = py * P.W + px;
@@ -232,7 +253,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(const RasterArgs 
         }
         if (a.depth) a.depth[p] = dep;
         if (a.accum) a.accum[p] = 1.0f - T;
-        if (a.normal) {
+        if (kNormal) {
             a.normal[3 * p] = n0;
             a.normal[3 * p + 1] = n1;
             a.normal[3 * p + 2] = n2;
@@ -291,8 +312,10 @@ __device__ __forceinline__ float warp_reduce16(float (&v)[16], int lane) {
 
 __device__ __forceinline__ float sgnf(float x) { return x > 0.f ? 1.f : (x < 0.f ? -1.f : 0.f); }
 
-__global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(const RasterArgs a) {
+template <bool kFull>  // kFull: normal / accumulation seeds present (external loss)
+__global__ void __launch_bounds__(kRasterThreads, 3) k_raster_bwd(const RasterArgs a) {
     __shared__ Stage st;
+    __shared__ uint8_t s_list[kRasterThreads / 32][kRasterThreads];
     __shared__ int s_lmax[8];
     __shared__ float s_loss[8];
     const ViewParams &P = a.P;
@@ -417,83 +440,69 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(const RasterArgs 
             __syncthreads();
             const int base = b * kRasterThreads;
             const int nrec = min(kRasterThreads, cnt - base);
-            uint32_t mask[8];
+            const int nl = warp_cull(st.rect[buf], nrec, wx0, wx1, wy0, wy1, lane, s_list[warp], rg.x + base, wlast);
+            for (int j = nl - 1; j >= 0; --j) {
+                const int k = s_list[warp][j];
+                const int pos = rg.x + base + k;
+                const uint32_t id = st.id[buf][k];
+                float v[16];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int k = q * 32 + lane;
-                bool hit = false;
-                if (k < nrec && rg.x + base + k <= wlast) {
-                    const short4 r = st.rect[buf][k];
-                    hit = (r.x <= wx1) & (r.y >= wx0) & (r.z <= wy1) & (r.w >= wy0);
-                }
-                mask[q] = __ballot_sync(kFull, hit);
-            }
-#pragma unroll 1
-            for (int q = 7; q >= 0; --q) {
-                uint32_t m = mask[q];
-                while (m) {
-                    const int bit = 31 - __clz(m);
-                    m &= ~(1u << bit);
-                    const int k = q * 32 + bit;
-                    const int pos = rg.x + base + k;
-                    const uint32_t id = st.id[buf][k];
-                    float v[16];
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) v[j] = 0.f;
-                    bool contrib = false;
-                    if (pos <= last) {
-                        PairEval e;
-                        const SplatRecord &r = st.rec[buf][k];
-                        if (eval_pair(P, a.params, r, st.rect[buf][k], id, px, py, e, guard)) {
-                            contrib = true;
-                            const float4 q1 = r.q1, q2 = r.q2, q3 = r.q3;
-                            float Ti;
-                            if (first) {
-                                Ti = Tlast;
-                                first = false;
-                            } else {
-                                Ti = Tn / (1.0f - e.w);
-                            }
-                            Tn = Ti;
-                            const float alpha = e.w * Ti;
-                            v[1] = gc0 * alpha;
-                            v[2] = gc1 * alpha;
-                            v[3] = gc2 * alpha;
-                            v[4] = gd * alpha;
-                            v[5] = gn0 * alpha;
-                            v[6] = gn1 * alpha;
-                            v[7] = gn2 * alpha;
-                            // dL/dw = T_i [ G.(c - S) + gd (z - Sd) + Gn.(n - Sn) ] + ga T_i R
-                            float dLdw = gc0 * (q2.x - S0) + gc1 * (q2.y - S1) + gc2 * (q2.z - S2) +
-                                         gd * (q2.w - Sd) + gn0 * (q3.x - Sn0) + gn1 * (q3.y - Sn1) +
-                                         gn2 * (q3.z - Sn2) + ga * R;
-                            dLdw *= Ti;
-                            if (!e.clamped) {
-                                v[0] = dLdw * e.g;
-                                const float gm = -0.5f * e.w * dLdw;  // dL/dm
-                                const float gu = 2.f * gm * e.u, gv = 2.f * gm * e.v;
-                                v[8] = gu * e.dx;
-                                v[9] = gu * e.dy;
-                                v[10] = gv * e.dx;
-                                v[11] = gv * e.dy;
-                                v[12] = -(gu * q1.x + gv * q1.z);
-                                v[13] = -(gu * q1.y + gv * q1.w);
-                            }
-                            const float omw = 1.0f - e.w;
-                            S0 = e.w * q2.x + omw * S0;
-                            S1 = e.w * q2.y + omw * S1;
-                            S2 = e.w * q2.z + omw * S2;
-                            Sd = e.w * q2.w + omw * Sd;
+                for (int t = 0; t < 16; ++t) v[t] = 0.f;
+                bool contrib = false;
+                if (pos <= last) {
+                    PairEval e;
+                    const SplatRecord &r = st.rec[buf][k];
+                    if (eval_pair(P, a.Pg, a.params, r, id, px, py, e, guard)) {
+                        contrib = true;
+                        const float4 q1 = r.q1, q2 = r.q2;
+                        float Ti;
+                        if (first) {
+                            Ti = Tlast;
+                            first = false;
+                        } else {
+                            Ti = Tn / (1.0f - e.w);
+                        }
+                        Tn = Ti;
+                        const float alpha = e.w * Ti;
+                        v[1] = gc0 * alpha;
+                        v[2] = gc1 * alpha;
+                        v[3] = gc2 * alpha;
+                        v[4] = gd * alpha;
+                        // dL/dw = T_i [ G.(c - S) + gd (z - Sd) + Gn.(n - Sn) ] + ga T_i R
+                        float dLdw = gc0 * (q2.x - S0) + gc1 * (q2.y - S1) + gc2 * (q2.z - S2) + gd * (q2.w - Sd);
+                        const float omw = 1.0f - e.w;
+                        if (kFull) {
+                            const float4 q3 = r.q3;
+                            v[11] = gn0 * alpha;
+                            v[12] = gn1 * alpha;
+                            v[13] = gn2 * alpha;
+                            dLdw += gn0 * (q3.x - Sn0) + gn1 * (q3.y - Sn1) + gn2 * (q3.z - Sn2) + ga * R;
                             Sn0 = e.w * q3.x + omw * Sn0;
                             Sn1 = e.w * q3.y + omw * Sn1;
                             Sn2 = e.w * q3.z + omw * Sn2;
                             R *= omw;
                         }
+                        dLdw *= Ti;
+                        if (!e.clamped) {
+                            v[0] = dLdw * e.g;
+                            const float gm = -0.5f * e.w * dLdw;  // dL/dm
+                            const float gu = 2.f * gm * e.u, gv = 2.f * gm * e.v;
+                            v[5] = gu * e.dx;
+                            v[6] = gu * e.dy;
+                            v[7] = gv * e.dx;
+                            v[8] = gv * e.dy;
+                            v[9] = -(gu * q1.x + gv * q1.z);
+                            v[10] = -(gu * q1.y + gv * q1.w);
+                        }
+                        S0 = e.w * q2.x + omw * S0;
+                        S1 = e.w * q2.y + omw * S1;
+                        S2 = e.w * q2.z + omw * S2;
+                        Sd = e.w * q2.w + omw * Sd;
                     }
-                    if (__any_sync(kFull, contrib)) {
-                        const float s = warp_reduce16(v, lane);
-                        if (!(lane & 1) && lane < 28 && s != 0.f) atomicAdd(a.grad2d + (size_t)id * 16 + (lane >> 1), s);
-                    }
+                }
+                if (__any_sync(0xffffffffu, contrib)) {
+                    const float sum = warp_reduce16(v, lane);
+                    if (!(lane & 1) && lane < 28 && sum != 0.f) atomicAdd(a.grad2d + (size_t)id * 16 + (lane >> 1), sum);
                 }
             }
             __syncthreads();
@@ -508,21 +517,29 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(const RasterArgs 
 
 }  // namespace
 
+template <bool kArg, bool kMaxW>
+static void fwd_dispatch(const RasterArgs &a, int tiles, cudaStream_t s) {
+    if (a.normal) k_raster_fwd<kArg, kMaxW, true><<<tiles, kRasterThreads, 0, s>>>(a);
+    else k_raster_fwd<kArg, kMaxW, false><<<tiles, kRasterThreads, 0, s>>>(a);
+}
+
 void launch_raster_forward(const RasterArgs &a, cudaStream_t s) {
     const int tiles = a.P.ntx * a.P.nty;
     const bool arg = a.max_w != nullptr || a.arg_w != nullptr;
     const bool mw = a.max_all != nullptr;
     count_launch();
-    if (arg && mw) k_raster_fwd<true, true><<<tiles, kRasterThreads, 0, s>>>(a);
-    else if (arg) k_raster_fwd<true, false><<<tiles, kRasterThreads, 0, s>>>(a);
-    else if (mw) k_raster_fwd<false, true><<<tiles, kRasterThreads, 0, s>>>(a);
-    else k_raster_fwd<false, false><<<tiles, kRasterThreads, 0, s>>>(a);
+    if (arg && mw) fwd_dispatch<true, true>(a, tiles, s);
+    else if (arg) fwd_dispatch<true, false>(a, tiles, s);
+    else if (mw) fwd_dispatch<false, true>(a, tiles, s);
+    else fwd_dispatch<false, false>(a, tiles, s);
 }
 
 void launch_raster_backward(const RasterArgs &a, cudaStream_t s) {
     const int tiles = a.P.ntx * a.P.nty;
+    const bool full = a.loss_kind == S2D_LOSS_EXTERNAL && (a.d_normal != nullptr || a.d_accum != nullptr);
     count_launch();
-    k_raster_bwd<<<tiles, kRasterThreads, 0, s>>>(a);
+    if (full) k_raster_bwd<true><<<tiles, kRasterThreads, 0, s>>>(a);
+    else k_raster_bwd<false><<<tiles, kRasterThreads, 0, s>>>(a);
 }
 
 }  // namespace s2d

@@ -36,11 +36,13 @@ struct SyncRegion {
     uint32_t *pair_status;     // [2][ceil(pcap / kSortTile) * kRadix]
     uint32_t *tie_claim;       // [n]
     int2 *ranges;              // [ntiles]
+    ViewParams *params;        // device copy of the view constants (guard-band path)
     size_t bytes;
 };
 
 struct ProjectArgs {
     ViewParams P;
+    ViewParams *P_out;  // device copy written by block 0 (read by the raster guard path)
     const float *params;
     SplatRecord *rec;
     short4 *rect;
@@ -83,6 +85,7 @@ void launch_tile_ranges(const uint32_t *pkeys, const int *d_p, uint32_t pcap, in
 
 struct RasterArgs {
     ViewParams P;
+    const ViewParams *Pg;  // the same constants in global memory (rare float64 path)
     const float *params;
     const int2 *ranges;
     const uint32_t *pair_ids;
