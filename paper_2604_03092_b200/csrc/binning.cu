@@ -91,7 +91,9 @@ __global__ void __launch_bounds__(kProjThreads) k_project(const ProjectArgs a) {
             const double sg = (nn[0] * e.p[0] + nn[1] * e.p[1] + nn[2] * e.p[2]) > 0.0 ? -1.0 : 1.0;
             // guard band of the float32 Mahalanobis distance
             const double kappa = sqrt(e.lmax / e.lmin);
-            const double gb = 4e-5 * kappa + 6e-6 / sqrt(e.lmin) + 4e-6;
+            // (covers float32 rounding of Minv, of the pixel offset and of u, v, m; DESIGN.md
+            // "guard bands")
+            const double gb = 4e-5 * kappa + 1e-5 / sqrt(e.lmin) + 4e-6;
             r.q3 = make_float4((float)(sg * nn[0]), (float)(sg * nn[1]), (float)(sg * nn[2]), (float)gb);
             a.rec[i] = r;
             a.rect[i] = make_short4((short)e.x0, (short)e.x1, (short)e.y0, (short)e.y1);
@@ -104,10 +106,13 @@ __global__ void __launch_bounds__(kProjThreads) k_project(const ProjectArgs a) {
     // order-preserving compaction
     uint32_t tot;
     const uint32_t ex = block_exclusive_scan_256(on ? 1u : 0u, s_w, &tot);
-    if (threadIdx.x == 0) {
-        s_base = lookback_exclusive(a.status, 1, tile, tot);
-        const int ntiles = (int)((P.n + kProjThreads - 1) / kProjThreads);
-        if (tile == ntiles - 1) a.stats->visible = (int)(s_base + tot);
+    if (threadIdx.x < 32) {
+        const uint32_t pre = lookback_warp(a.status, tile, tot);
+        if (threadIdx.x == 0) {
+            s_base = pre;
+            const int ntiles = (int)((P.n + kProjThreads - 1) / kProjThreads);
+            if (tile == ntiles - 1) a.stats->visible = (int)(pre + tot);
+        }
     }
     __syncthreads();
     if (on) {
@@ -186,7 +191,7 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
     // global start of each digit (exclusive scan of the pass histogram)
     uint32_t htot;
     const uint32_t dstart = block_exclusive_scan_256(hist[tid], s_w, &htot);
-    const uint32_t prefix = lookback_exclusive(status + tid, kRadix, tile, run);
+    const uint32_t prefix = lookback_batched(status + tid, kRadix, tile, run);
     s_base[tid] = dstart + prefix;
     __syncthreads();
 #pragma unroll
@@ -265,11 +270,12 @@ __global__ void __launch_bounds__(256) k_scan_emit(const EmitArgs a) {
     }
     uint32_t tot;
     const uint32_t ex = block_exclusive_scan_256(cnt, s_w, &tot);
-    if (tid == 0) {
-        s_base = lookback_exclusive(a.status, 1, tile, tot);
+    if (tid < 32) {
+        const uint32_t pre = lookback_warp(a.status, tile, tot);
         const int ntiles = (nv + kEmitTile - 1) / kEmitTile;
-        if (tile == ntiles - 1) {
-            const uint32_t total = s_base + tot;
+        if (tid == 0) s_base = pre;
+        if (tid == 0 && tile == ntiles - 1) {
+            const uint32_t total = pre + tot;
             a.stats->pairs = (int)total;
             a.stats->pairs_stored = (int)(total < a.pcap ? total : a.pcap);
             if (total > a.pcap) a.stats->overflow = 1;

@@ -40,25 +40,57 @@ __global__ void __launch_bounds__(128) k_project_bwd(const ProjectBwdArgs a) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const ViewParams &P = a.P;
     if (i >= P.n) return;
-    if (!(a.flags[i] & 4)) return;
-    float4 *g4 = reinterpret_cast<float4 *>(a.grad2d + (size_t)i * 16);
-    const float4 G0 = g4[0], G1 = g4[1], G2 = g4[2], G3 = g4[3];
-    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-    g4[0] = z4;
-    g4[1] = z4;
-    g4[2] = z4;
-    g4[3] = z4;
+    const uint8_t fl = __ldg(a.flags + i);
+    if (!(fl & 4)) return;
+    // all independent loads are issued up front (one exposed memory latency); stores at the end
     const int64_t n = P.n;
-    float *gmeans = a.grads, *gquats = a.grads + 3 * n, *gscales = a.grads + 7 * n;
-    float *gopac = a.grads + 9 * n, *gcol = a.grads + 10 * n;
-    gopac[i] += G0.x;
-    gcol[3 * i] += G0.y;
-    gcol[3 * i + 1] += G0.z;
-    gcol[3 * i + 2] += G0.w;
+    const float4 *__restrict__ g4 = reinterpret_cast<const float4 *>(a.grad2d + (size_t)i * 16);
+    const float4 G0 = g4[0], G1 = g4[1], G2 = g4[2];
+    const float G3x = a.grad2d[(size_t)i * 16 + 12], G3y = a.grad2d[(size_t)i * 16 + 13];
+    float *__restrict__ gmeans = a.grads, *__restrict__ gquats = a.grads + 3 * n;
+    float *__restrict__ gscales = a.grads + 7 * n, *__restrict__ gopac = a.grads + 9 * n;
+    float *__restrict__ gcol = a.grads + 10 * n;
+    const float gm_old[3] = {gmeans[3 * i], gmeans[3 * i + 1], gmeans[3 * i + 2]};
+    const float gq_old[4] = {gquats[4 * i], gquats[4 * i + 1], gquats[4 * i + 2], gquats[4 * i + 3]};
+    const float gs_old[2] = {gscales[2 * i], gscales[2 * i + 1]};
+    const float go_old = gopac[i];
+    const float gc_old[3] = {gcol[3 * i], gcol[3 * i + 1], gcol[3 * i + 2]};
 
+    // Geometry for the chain rule: plain float64 (contractions allowed, one division for 1/z and
+    // one for 1/det M) — only the forward's decisions need the reference's exact arithmetic.
     const ParamView pv(a.params, n);
-    ExactProj e;
-    project_exact(P, pv, i, e);
+    struct {
+        double p[3], R[9], Bc[3][2], J[2][3];
+    } e;
+    {
+        const double mu[3] = {(double)pv.means[3 * i], (double)pv.means[3 * i + 1], (double)pv.means[3 * i + 2]};
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+            e.p[r] = P.m_cw[3 * r] * mu[0] + P.m_cw[3 * r + 1] * mu[1] + P.m_cw[3 * r + 2] * mu[2] + P.inv[1 + r];
+        const double w = pv.quats[4 * i], x = pv.quats[4 * i + 1], y = pv.quats[4 * i + 2], z = pv.quats[4 * i + 3];
+        e.R[0] = 1.0 - 2.0 * (y * y + z * z);
+        e.R[1] = 2.0 * (x * y - w * z);
+        e.R[2] = 2.0 * (x * z + w * y);
+        e.R[3] = 2.0 * (x * y + w * z);
+        e.R[4] = 1.0 - 2.0 * (x * x + z * z);
+        e.R[5] = 2.0 * (y * z - w * x);
+        e.R[6] = 2.0 * (x * z - w * y);
+        e.R[7] = 2.0 * (y * z + w * x);
+        e.R[8] = 1.0 - 2.0 * (x * x + y * y);
+        const double s0 = pv.scales[2 * i], s1 = pv.scales[2 * i + 1];
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+            e.Bc[r][0] = (P.m_cw[3 * r] * e.R[0] + P.m_cw[3 * r + 1] * e.R[3] + P.m_cw[3 * r + 2] * e.R[6]) * s0;
+            e.Bc[r][1] = (P.m_cw[3 * r] * e.R[1] + P.m_cw[3 * r + 1] * e.R[4] + P.m_cw[3 * r + 2] * e.R[7]) * s1;
+        }
+        const double iz = 1.0 / e.p[2];
+        e.J[0][0] = P.fx * iz;
+        e.J[0][1] = 0.0;
+        e.J[0][2] = -P.fx * e.p[0] * iz * iz;
+        e.J[1][0] = 0.0;
+        e.J[1][1] = P.fy * iz;
+        e.J[1][2] = -P.fy * e.p[1] * iz * iz;
+    }
     const double M00 = e.J[0][0] * e.Bc[0][0] + e.J[0][2] * e.Bc[2][0];
     const double M01 = e.J[0][0] * e.Bc[0][1] + e.J[0][2] * e.Bc[2][1];
     const double M10 = e.J[1][1] * e.Bc[1][0] + e.J[1][2] * e.Bc[2][0];
@@ -111,7 +143,7 @@ __global__ void __launch_bounds__(128) k_project_bwd(const ProjectBwdArgs a) {
         for (int k = 0; k < 3; ++k)
             nn[k] = P.r_cw[3 * k] * e.R[2] + P.r_cw[3 * k + 1] * e.R[5] + P.r_cw[3 * k + 2] * e.R[8];
         const double sg = (nn[0] * e.p[0] + nn[1] * e.p[1] + nn[2] * e.p[2]) > 0.0 ? -1.0 : 1.0;
-        const double gn[3] = {G2.w, G3.x, G3.y};
+        const double gn[3] = {G2.w, G3x, G3y};
 #pragma unroll
         for (int b = 0; b < 3; ++b)
             gR[3 * b + 2] = sg * (P.r_cw[b] * gn[0] + P.r_cw[3 + b] * gn[1] + P.r_cw[6 + b] * gn[2]);
@@ -136,11 +168,22 @@ __global__ void __launch_bounds__(128) k_project_bwd(const ProjectBwdArgs a) {
     // p = s_inv R(q_inv) mu + t_inv
 #pragma unroll
     for (int b = 0; b < 3; ++b)
-        gmeans[3 * i + b] += (float)(P.inv[0] * (P.r_cw[b] * gp0 + P.r_cw[3 + b] * gp1 + P.r_cw[6 + b] * gp2));
+        gmeans[3 * i + b] = gm_old[b] + (float)(P.inv[0] * (P.r_cw[b] * gp0 + P.r_cw[3 + b] * gp1 + P.r_cw[6 + b] * gp2));
 #pragma unroll
-    for (int k = 0; k < 4; ++k) gquats[4 * i + k] += (float)gq[k];
-    gscales[2 * i] += (float)gs0;
-    gscales[2 * i + 1] += (float)gs1;
+    for (int k = 0; k < 4; ++k) gquats[4 * i + k] = gq_old[k] + (float)gq[k];
+    gscales[2 * i] = gs_old[0] + (float)gs0;
+    gscales[2 * i + 1] = gs_old[1] + (float)gs1;
+    gopac[i] = go_old + G0.x;
+    gcol[3 * i] = gc_old[0] + G0.y;
+    gcol[3 * i + 1] = gc_old[1] + G0.z;
+    gcol[3 * i + 2] = gc_old[2] + G0.w;
+    // leave the per-view 2D gradient buffer zeroed for the next view
+    float4 *zero = reinterpret_cast<float4 *>(a.grad2d + (size_t)i * 16);
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    zero[0] = z4;
+    zero[1] = z4;
+    zero[2] = z4;
+    zero[3] = z4;
 }
 
 struct AdamK {

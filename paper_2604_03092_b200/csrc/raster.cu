@@ -99,32 +99,49 @@ struct PairEval {
 };
 
 __device__ __forceinline__ bool eval_pair(const ViewParams &P, const ViewParams *Pg, const float *params,
-                                          const SplatRecord &r, uint32_t id, int px, int py, PairEval &o,
-                                          int &guard_hits) {
-    const uint32_t lob = __float_as_uint(r.q0.z);
+                                          const SplatRecord &r, uint32_t id, float lx, float ly, int px, int py,
+                                          PairEval &o, int &guard_hits) {
+    // staged record: q0 = (cx_hi - tile_x0, cy_hi - tile_y0, half2 lo, opacity) — see stage_finish
+    const float4 q0 = r.q0;
+    const uint32_t lob = __float_as_uint(q0.z);
     const __half2 lo = *reinterpret_cast<const __half2 *>(&lob);
     // explicit round-to-nearest intrinsics: forward and backward must take
     // bit-identical decisions, so nothing here may be contracted differently
-    o.dx = __fsub_rn(__fsub_rn((float)px, r.q0.x), __low2float(lo));
-    o.dy = __fsub_rn(__fsub_rn((float)py, r.q0.y), __high2float(lo));
+    o.dx = __fsub_rn(__fsub_rn(lx, q0.x), __low2float(lo));
+    o.dy = __fsub_rn(__fsub_rn(ly, q0.y), __high2float(lo));
     o.u = __fmaf_rn(r.q1.x, o.dx, __fmul_rn(r.q1.y, o.dy));
     o.v = __fmaf_rn(r.q1.z, o.dx, __fmul_rn(r.q1.w, o.dy));
     const float m = __fmaf_rn(o.u, o.u, __fmul_rn(o.v, o.v));
-    const float gb = r.q3.w;
+    const float gbs = r.q3.w;  // guard band, negative when the weight can reach the clamp
+    const float gb = fabsf(gbs);
     if (m > P.maha_cut_f + gb) return false;
     o.g = fast_exp2(__fmul_rn(m, -0.72134752044448170368f));  // exp(-m/2); m <= sigma^2 + gb keeps it normal
-    float w = __fmul_rn(r.q0.w, o.g);
-    if ((m >= P.maha_cut_f - gb) | (fabsf(w - P.w_clamp_f) <= 4e-6f)) {
+    float w = __fmul_rn(q0.w, o.g);
+    bool band = m >= P.maha_cut_f - gb;
+    o.clamped = false;
+    if (gbs < 0.0f) {  // opacity close enough to the clamp for the weight to reach it
+        band |= fabsf(w - P.w_clamp_f) <= 4e-6f;
+        o.clamped = w > P.w_clamp_f;
+    }
+    if (band) {
         ++guard_hits;
         const int rr = guard_resolve(Pg, params, id, px, py);
         if (!(rr & 1)) return false;
         o.clamped = (rr & 2) != 0;
-    } else {
-        o.clamped = w > P.w_clamp_f;
     }
     if (o.clamped) w = P.w_clamp_f;
     o.w = w;
     return w > 0.0f;
+}
+
+// After this thread's cp.async copies of a batch landed: make its staged record's centre
+// tile-relative (cx_hi - tile_x0 is exact: tile_x0 is an integer no larger than the centre's
+// magnitude scale), and flag in the sign of the guard band whether the opacity can reach the
+// weight clamp.  Identical in forward and backward.
+__device__ __forceinline__ void stage_finish(SplatRecord &r, float tx0, float ty0, float clamp_f) {
+    r.q0.x = __fsub_rn(r.q0.x, tx0);
+    r.q0.y = __fsub_rn(r.q0.y, ty0);
+    if (r.q0.w > clamp_f - 8e-6f) r.q3.w = -r.q3.w;
 }
 
 // Ordered list (into s_list) of the staged records whose integer bbox touches the warp's
@@ -161,6 +178,8 @@ __global__ void __launch_bounds__(kRasterThreads, 3) k_raster_fwd(const RasterAr
     const int wx1 = min(wx0 + 7, P.W - 1), wy1 = min(wy0 + 3, P.H - 1);
     const int px = wx0 + (lane & 7), py = wy0 + (lane >> 3);
     const bool inside = px < P.W && py < P.H;
+    const float tx0f = (float)(tx * kTile), ty0f = (float)(ty * kTile);
+    const float lx = (float)(px - tx * kTile), ly = (float)(py - ty * kTile);
     const int2 rg = a.ranges[tile];
     const int cnt = rg.y - rg.x;
 
@@ -188,6 +207,7 @@ __global__ void __launch_bounds__(kRasterThreads, 3) k_raster_fwd(const RasterAr
             }
             cp_commit();
             cp_wait<1>();
+            if (b * kRasterThreads + tid < cnt) stage_finish(st.rec[buf][tid], tx0f, ty0f, P.w_clamp_f);
             __syncthreads();
             const int base = b * kRasterThreads;
             const int nrec = min(kRasterThreads, cnt - base);
@@ -200,7 +220,7 @@ __global__ void __launch_bounds__(kRasterThreads, 3) k_raster_fwd(const RasterAr
                     if (!done) {
                         PairEval e;
                         const SplatRecord &r = st.rec[buf][k];
-                        if (eval_pair(P, a.Pg, a.params, r, id, px, py, e, guard)) {
+                        if (eval_pair(P, a.Pg, a.params, r, id, lx, ly, px, py, e, guard)) {
                             contrib = e.w * T;
                             const float4 q2 = r.q2;
                             c0 = fmaf(contrib, q2.x, c0);
@@ -326,6 +346,8 @@ __global__ void __launch_bounds__(kRasterThreads, 3) k_raster_bwd(const RasterAr
     const int wx1 = min(wx0 + 7, P.W - 1), wy1 = min(wy0 + 3, P.H - 1);
     const int px = wx0 + (lane & 7), py = wy0 + (lane >> 3);
     const bool inside = px < P.W && py < P.H;
+    const float tx0f = (float)(tx * kTile), ty0f = (float)(ty * kTile);
+    const float lx = (float)(px - tx * kTile), ly = (float)(py - ty * kTile);
     const int2 rg = a.ranges[tile];
     const int p = py * P.W + px;
 
@@ -437,6 +459,7 @@ __global__ void __launch_bounds__(kRasterThreads, 3) k_raster_bwd(const RasterAr
             }
             cp_commit();
             cp_wait<1>();
+            if (b * kRasterThreads + tid < cnt) stage_finish(st.rec[buf][tid], tx0f, ty0f, P.w_clamp_f);
             __syncthreads();
             const int base = b * kRasterThreads;
             const int nrec = min(kRasterThreads, cnt - base);
@@ -452,7 +475,7 @@ __global__ void __launch_bounds__(kRasterThreads, 3) k_raster_bwd(const RasterAr
                 if (pos <= last) {
                     PairEval e;
                     const SplatRecord &r = st.rec[buf][k];
-                    if (eval_pair(P, a.Pg, a.params, r, id, px, py, e, guard)) {
+                    if (eval_pair(P, a.Pg, a.params, r, id, lx, ly, px, py, e, guard)) {
                         contrib = true;
                         const float4 q1 = r.q1, q2 = r.q2;
                         float Ti;

@@ -233,11 +233,44 @@ constexpr uint32_t kFlagAgg = 1u << 30;
 constexpr uint32_t kFlagInc = 2u << 30;
 constexpr uint32_t kValMask = (1u << 30) - 1;
 
-// Exclusive prefix of `agg` over preceding tiles of a chained scan; tile order is
-// the dynamic ticket order so predecessors are always running (no deadlock).
-// Called by ONE thread per (tile, lane-of-status).
-__device__ __forceinline__ uint32_t lookback_exclusive(uint32_t *status, int stride, int tile,
-                                                       uint32_t agg) {
+// Decoupled look-back (chained scan).  Tile order is the dynamic ticket order, so every
+// predecessor is already running and will publish (no deadlock).
+
+// Warp-cooperative look-back of ONE value: all 32 lanes of one warp call it; each round
+// reads 32 predecessors at once, so the walk costs ~1 round trip per 32 predecessors.
+// Returns the exclusive prefix (to every lane).
+__device__ __forceinline__ uint32_t lookback_warp(uint32_t *status, int tile, uint32_t agg) {
+    const int lane = threadIdx.x & 31;
+    if (tile == 0) {
+        if (lane == 0) st_relaxed_u32(status, kFlagInc | agg);
+        return 0;
+    }
+    if (lane == 0) st_relaxed_u32(status + tile, kFlagAgg | agg);
+    uint32_t prefix = 0;
+    int base = tile - 1;
+    while (true) {
+        const int j = base - lane;
+        const uint32_t s = j >= 0 ? ld_relaxed_u32(status + j) : kFlagInc;
+        const uint32_t f = s & ~kValMask;
+        const uint32_t inc = __ballot_sync(0xffffffffu, f == kFlagInc);
+        const uint32_t pend = __ballot_sync(0xffffffffu, f == 0);
+        const int first_inc = inc ? __ffs(inc) - 1 : 32;
+        const uint32_t range = first_inc >= 31 ? 0xffffffffu : ((2u << first_inc) - 1u);
+        if (pend & range) continue;  // a predecessor in the window has not published yet
+        uint32_t v = lane <= first_inc ? (s & kValMask) : 0u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        prefix += v;
+        if (first_inc < 32) break;
+        base -= 32;
+    }
+    if (lane == 0) st_relaxed_u32(status + tile, kFlagInc | (prefix + agg));
+    return prefix;
+}
+
+// Per-thread look-back of one column of a [tile][stride] status table (one thread per
+// digit): predecessors are read 16 at a time (independent loads in flight).
+__device__ __forceinline__ uint32_t lookback_batched(uint32_t *status, int stride, int tile, uint32_t agg) {
     if (tile == 0) {
         st_relaxed_u32(status, kFlagInc | agg);
         return 0;
@@ -246,12 +279,25 @@ __device__ __forceinline__ uint32_t lookback_exclusive(uint32_t *status, int str
     uint32_t prefix = 0;
     int j = tile - 1;
     while (true) {
-        const uint32_t s = ld_relaxed_u32(status + (size_t)j * stride);
-        const uint32_t f = s & ~kValMask;
-        if (f == 0) continue;  // predecessor not published yet
-        prefix += s & kValMask;
-        if (f == kFlagInc) break;
-        --j;
+        uint32_t s[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) s[k] = (j - k >= 0) ? ld_relaxed_u32(status + (size_t)(j - k) * stride) : kFlagInc;
+        int consumed = 0;
+        bool done = false, stall = false;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            if (done || stall) continue;
+            const uint32_t f = s[k] & ~kValMask;
+            if (f == 0) {
+                stall = true;
+                continue;
+            }
+            prefix += s[k] & kValMask;
+            ++consumed;
+            if (f == kFlagInc) done = true;
+        }
+        if (done) break;
+        j -= consumed;
     }
     st_relaxed_u32(status + (size_t)tile * stride, kFlagInc | (prefix + agg));
     return prefix;
