@@ -211,7 +211,9 @@ def main():
     loss = ViewLoss("l1", 1.0, 0.1, False)
 
     # ---- device-resident run (value) ----
-    ref = AdamRefiner(sc.extra["perturbed"], sc.intr, sc.poses, rgbs, deps, loss, AdamConfig(), device=dev)
+    inflight = int(os.environ.get("S2D_INFLIGHT", "3"))
+    ref = AdamRefiner(sc.extra["perturbed"], sc.intr, sc.poses, rgbs, deps, loss, AdamConfig(), device=dev,
+                      inflight=inflight)
     for _ in range(args.warmup):
         ref.step()
     clocks = ClockSampler(local_rank)
@@ -238,7 +240,9 @@ def main():
     ms_step = ms / args.steps
     value = n_views * px / (ms_step * 1e-3) / 1e6
 
-    # ---- per-phase breakdown (separate timed pass with events between kernels) ----
+    # ---- per-phase breakdown (separate timed pass with events between kernels; one stream,
+    # so the phases do not overlap) ----
+    ref.active_lanes = 1
     ref.view.set_timing(True)
     ref.view.timing(reset=True)
     tb0 = torch.cuda.Event(enable_timing=True)
@@ -251,6 +255,8 @@ def main():
     torch.cuda.synchronize()
     ph = ref.view.timing(reset=True)
     ref.view.set_timing(False)
+    ref.active_lanes = ref.inflight
+    inflight = ref.inflight
     st = ref.view.stats()
     nfw = max(ph["n_forward"], 1)
     per_launch_ms = {k: ph[k] / nfw for k in ref.view.PHASES}
@@ -277,7 +283,7 @@ def main():
     del ref
     torch.cuda.empty_cache()
     ref2 = AdamRefiner(sc.extra["perturbed"], sc.intr, sc.poses, host_rgb, host_dep, loss, AdamConfig(), device=dev,
-                       host_targets=True)
+                       host_targets=True, inflight=inflight)
     for _ in range(args.warmup):
         ref2.step()
     if world > 1:
@@ -320,6 +326,7 @@ def main():
                        "visible_last_view": nvis, "pairs_last_view": npairs},
             "refine_iters_per_s": round(1000.0 / ms_step, 3),
             "fwd_bwd_mpix_per_s_per_view": round(px / (view_ms * 1e-3) / 1e6, 2) if view_ms > 0 else None,
+            "views_in_flight": inflight,
             "loss_first_last": [losses[0], losses[-1]],
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm,
                          "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": None,

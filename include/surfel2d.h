@@ -172,8 +172,10 @@ int s2d_forward(s2d_view *view, void *stream, const float *params, int64_t n,
  * Backward of the last s2d_forward of `view`: loss seeds, reverse-order blend
  * backward, projection backward.  Replaces rasterizer.grad_color_opacity
  * (rasterizer.py:360-399, _k.blend_gradients _raster_kernels.py:58-113) and
- * adds the geometry gradients.  ACCUMULATES (+=) into grads (packed 13*n
- * float32, device), so summing views needs no extra pass (mapper.py:300-307).
+ * adds the geometry gradients.  ACCUMULATES (+=, atomically) into grads
+ * (packed 13*n float32, device), so summing views needs no extra pass
+ * (mapper.py:300-307) and views in flight on several streams, each with its
+ * own s2d_view, may share one gradient block.
  * loss_accum (device double, nullable) receives += the view's loss value.
  * `image` must be the forward's outputs (color/depth/accumulation/normal as
  * the loss needs them).

@@ -157,13 +157,14 @@ int grow(T *&p, int64_t &cap_elems, int64_t need, bool zero = false) {
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 __global__ void k_stats_accumulate(const s2d_view_stats *s, s2d_view_stats *acc) {
-    acc->visible = max(acc->visible, s->visible);
-    acc->pairs = max(acc->pairs, s->pairs);
-    acc->pairs_stored = max(acc->pairs_stored, s->pairs_stored);
-    acc->degenerate += s->degenerate;
-    acc->n_mask += s->n_mask;
-    acc->guard_hits += s->guard_hits;
-    acc->overflow |= s->overflow;
+    // atomic: views on concurrent streams may share one accumulator
+    atomicMax(&acc->visible, s->visible);
+    atomicMax(&acc->pairs, s->pairs);
+    atomicMax(&acc->pairs_stored, s->pairs_stored);
+    atomicAdd(&acc->degenerate, s->degenerate);
+    atomicAdd(&acc->n_mask, s->n_mask);
+    atomicAdd(&acc->guard_hits, s->guard_hits);
+    atomicOr(&acc->overflow, s->overflow);
 }
 
 }  // namespace

@@ -4,8 +4,8 @@
 //   [dL/d opacity, dL/d rgb(3), dL/dz, dL/d Minv(4), dL/d centre(2), dL/d normal(3)]
 // through Minv = (J(p) Bc)^-1, centre(p), z, normal = R_cw R(q)[:,2] back to
 // the parameters (means, raw quats, scales, opacity, colours), in float64, and
-// ACCUMULATES into the packed gradient block (views sum with no extra pass,
-// mapper.py:300-307).  It zeroes the consumed 2D gradients so the per-view
+// ACCUMULATES into the packed gradient block with atomic reductions (views sum with no
+// extra pass, mapper.py:300-307, and views in flight on several streams may share it).  It zeroes the consumed 2D gradients so the per-view
 // buffer is clean for the next view without a memset.
 // k_adam: torch.optim.Adam arithmetic on the packed block, one thread per
 // surfel (so the per-surfel mask and the quaternion renormalisation are
@@ -47,14 +47,9 @@ __global__ void __launch_bounds__(128) k_project_bwd(const ProjectBwdArgs a) {
     const float4 *__restrict__ g4 = reinterpret_cast<const float4 *>(a.grad2d + (size_t)i * 16);
     const float4 G0 = g4[0], G1 = g4[1], G2 = g4[2];
     const float G3x = a.grad2d[(size_t)i * 16 + 12], G3y = a.grad2d[(size_t)i * 16 + 13];
-    float *__restrict__ gmeans = a.grads, *__restrict__ gquats = a.grads + 3 * n;
-    float *__restrict__ gscales = a.grads + 7 * n, *__restrict__ gopac = a.grads + 9 * n;
-    float *__restrict__ gcol = a.grads + 10 * n;
-    const float gm_old[3] = {gmeans[3 * i], gmeans[3 * i + 1], gmeans[3 * i + 2]};
-    const float gq_old[4] = {gquats[4 * i], gquats[4 * i + 1], gquats[4 * i + 2], gquats[4 * i + 3]};
-    const float gs_old[2] = {gscales[2 * i], gscales[2 * i + 1]};
-    const float go_old = gopac[i];
-    const float gc_old[3] = {gcol[3 * i], gcol[3 * i + 1], gcol[3 * i + 2]};
+    float *gmeans = a.grads, *gquats = a.grads + 3 * n;
+    float *gscales = a.grads + 7 * n, *gopac = a.grads + 9 * n;
+    float *gcol = a.grads + 10 * n;
 
     // Geometry for the chain rule: plain float64 (contractions allowed, one division for 1/z and
     // one for 1/det M) — only the forward's decisions need the reference's exact arithmetic.
@@ -165,18 +160,19 @@ __global__ void __launch_bounds__(128) k_project_bwd(const ProjectBwdArgs a) {
     gp2 += (double)G2.y * (-fx * x * iz2);
     gp1 += (double)G2.z * (fy * iz);
     gp2 += (double)G2.z * (-fy * y * iz2);
-    // p = s_inv R(q_inv) mu + t_inv
+    // p = s_inv R(q_inv) mu + t_inv.  Accumulation is atomic (fire-and-forget reductions), so
+    // views running concurrently on different streams may share one gradient block.
 #pragma unroll
     for (int b = 0; b < 3; ++b)
-        gmeans[3 * i + b] = gm_old[b] + (float)(P.inv[0] * (P.r_cw[b] * gp0 + P.r_cw[3 + b] * gp1 + P.r_cw[6 + b] * gp2));
+        atomicAdd(gmeans + 3 * i + b, (float)(P.inv[0] * (P.r_cw[b] * gp0 + P.r_cw[3 + b] * gp1 + P.r_cw[6 + b] * gp2)));
 #pragma unroll
-    for (int k = 0; k < 4; ++k) gquats[4 * i + k] = gq_old[k] + (float)gq[k];
-    gscales[2 * i] = gs_old[0] + (float)gs0;
-    gscales[2 * i + 1] = gs_old[1] + (float)gs1;
-    gopac[i] = go_old + G0.x;
-    gcol[3 * i] = gc_old[0] + G0.y;
-    gcol[3 * i + 1] = gc_old[1] + G0.z;
-    gcol[3 * i + 2] = gc_old[2] + G0.w;
+    for (int k = 0; k < 4; ++k) atomicAdd(gquats + 4 * i + k, (float)gq[k]);
+    atomicAdd(gscales + 2 * i, (float)gs0);
+    atomicAdd(gscales + 2 * i + 1, (float)gs1);
+    atomicAdd(gopac + i, G0.x);
+    atomicAdd(gcol + 3 * i, G0.y);
+    atomicAdd(gcol + 3 * i + 1, G0.z);
+    atomicAdd(gcol + 3 * i + 2, G0.w);
     // leave the per-view 2D gradient buffer zeroed for the next view
     float4 *zero = reinterpret_cast<float4 *>(a.grad2d + (size_t)i * 16);
     const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);

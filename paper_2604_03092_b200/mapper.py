@@ -207,18 +207,31 @@ class ViewLoss:
         return {"l1": N.LOSS_L1, "mse": N.LOSS_MSE}[self.kind]
 
 
+class _Lane:
+    """One stream's worth of view state: workspace, render targets, host-target staging."""
+
+    def __init__(self, ctx, h, w, dev, host_targets):
+        self.stream = torch.cuda.Stream(dev)
+        self.view = View(ctx)
+        self.img = ImageBuffers.allocate(h, w, dev, normal=False)
+        if host_targets:
+            self.rgb = torch.empty((h, w, 3), device=dev)
+            self.depth = torch.empty((h, w), device=dev)
+
+
 class AdamRefiner:
     """Multi-view fused-Adam refinement of all surfel parameters, views sharded over ranks.
 
     ``targets_rgb[v]`` (H,W,3) / ``targets_depth[v]`` (H,W) may be numpy arrays, device
-    tensors, or pinned host tensors (then each step copies them in on a side stream,
-    overlapped with the previous view's compute — the end-to-end path).
+    tensors, or (``host_targets=True``) host tensors that are pinned and copied in every
+    step on the view's stream, overlapping the other streams' compute (the end-to-end path).
+    ``inflight`` views run concurrently on separate streams.
     """
 
     def __init__(self, surfels, intr: CameraIntrinsics, poses, targets_rgb, targets_depth,
                  loss: ViewLoss = ViewLoss(), adam: AdamConfig = AdamConfig(),
                  raster_cfg: RasterConfig = DEFAULT_RASTER_CONFIG, mask=None, group=None, device=None,
-                 host_targets: bool = False):
+                 host_targets: bool = False, inflight: int = 3):
         self.ctx = DeviceContext.get(device)
         self.dev = self.ctx.device
         self.group = group
@@ -253,14 +266,10 @@ class AdamRefiner:
             else:
                 self.rgb[v] = torch.as_tensor(np.asarray(r, dtype=np.float32) if not isinstance(r, torch.Tensor) else r).to(self.dev, torch.float32)
                 self.depth[v] = torch.as_tensor(np.asarray(d, dtype=np.float32) if not isinstance(d, torch.Tensor) else d).to(self.dev, torch.float32)
-        if host_targets:
-            self.stage_rgb = [torch.empty((h, w, 3), device=self.dev) for _ in range(2)]
-            self.stage_depth = [torch.empty((h, w), device=self.dev) for _ in range(2)]
-            self.copy_stream = torch.cuda.Stream(self.dev)
-            self.copy_done = [torch.cuda.Event() for _ in range(2)]
-            self.stage_free = [torch.cuda.Event() for _ in range(2)]
-        self.view = View(self.ctx)
-        self.img = ImageBuffers.allocate(h, w, self.dev, normal=False)
+        self.inflight = max(1, int(inflight))
+        self.active_lanes = self.inflight
+        self.lanes = [_Lane(self.ctx, h, w, self.dev, host_targets) for _ in range(self.inflight)]
+        self.view = self.lanes[0].view  # the first lane (phase timing / inspection)
         self.loss_acc = torch.zeros(1, dtype=torch.float64, device=self.dev)
         self.stats_acc = torch.zeros(8, dtype=torch.int32, device=self.dev)
         self.host_stats = torch.zeros(8, dtype=torch.int32).pin_memory()
@@ -273,51 +282,50 @@ class AdamRefiner:
     def _size_pairs(self):
         """One forward per view to size the pair capacity (1.3 x the largest view)."""
         mx = 0
+        lane = self.lanes[0]
         for v in self.my_views:
-            st = forward_checked(self.view, self.params, self.n, self.all_poses[v], self.cam, self.cfg, self.img)
+            st = forward_checked(lane.view, self.params, self.n, self.all_poses[v], self.cam, self.cfg, lane.img)
             mx = max(mx, st.pairs)
-        self.view.reserve_pairs(int(mx * 1.3) + 4096)
+        self._reserve(int(mx * 1.3) + 4096)
 
-    def _targets(self, j, v):
-        if not self.host_targets:
-            return self.rgb[v], self.depth[v]
-        return self.stage_rgb[j & 1], self.stage_depth[j & 1]
-
-    def _issue_copy(self, j, v):
-        b = j & 1
-        cs = self.copy_stream
-        cs.wait_event(self.stage_free[b])
-        with torch.cuda.stream(cs):
-            self.stage_rgb[b].copy_(self.rgb[v], non_blocking=True)
-            self.stage_depth[b].copy_(self.depth[v], non_blocking=True)
-            self.copy_done[b].record(cs)
+    def _reserve(self, pairs):
+        for lane in self.lanes:
+            lane.view.reserve_pairs(pairs)
 
     def compute_grads(self):
-        """grads <- sum over this rank's views of d(loss)/d(params); loss_acc <- sum of losses."""
-        stream = torch.cuda.current_stream(self.dev)
+        """grads <- sum over this rank's views of d(loss)/d(params); loss_acc <- sum of losses.
+
+        Views are dealt round-robin to `active_lanes` streams, each with its own workspace
+        and image buffers, so one view's projection/sort overlaps another's compositing;
+        gradients, loss and stats accumulate atomically into shared buffers.
+        """
+        main = torch.cuda.current_stream(self.dev)
         self.grads.zero_()
         self.loss_acc.zero_()
         self.stats_acc.zero_()
+        lanes = self.lanes[: self.active_lanes]
+        start = torch.cuda.Event()
+        start.record(main)
+        for lane in lanes:
+            lane.stream.wait_stream(main)
         lc = self.loss_cfg
-        views = self.my_views
-        if self.host_targets:
-            for b in range(2):
-                self.stage_free[b].record(stream)
-            if views:
-                self._issue_copy(0, views[0])
-        for j, v in enumerate(views):
+        for j, v in enumerate(self.my_views):
+            lane = lanes[j % len(lanes)]
+            s = lane.stream
             if self.host_targets:
-                if j + 1 < len(views):
-                    self._issue_copy(j + 1, views[j + 1])
-                stream.wait_event(self.copy_done[j & 1])
-            trgb, tdep = self._targets(j, v)
-            self.view.forward(self.params, self.n, self.all_poses[v], self.cam, self.cfg, self.img)
-            self.view.accumulate_stats(self.stats_acc)
-            self.view.backward(self.params, self.n, self.img,
+                with torch.cuda.stream(s):
+                    lane.rgb.copy_(self.rgb[v], non_blocking=True)
+                    lane.depth.copy_(self.depth[v], non_blocking=True)
+                trgb, tdep = lane.rgb, lane.depth
+            else:
+                trgb, tdep = self.rgb[v], self.depth[v]
+            lane.view.forward(self.params, self.n, self.all_poses[v], self.cam, self.cfg, lane.img, stream=s)
+            lane.view.accumulate_stats(self.stats_acc, stream=s)
+            lane.view.backward(self.params, self.n, lane.img,
                                loss_struct(lc.code(), lc.w_rgb, lc.w_depth, lc.depth_mask, trgb, tdep),
-                               self.grads, self.loss_acc)
-            if self.host_targets:
-                self.stage_free[j & 1].record(stream)
+                               self.grads, self.loss_acc, stream=s)
+        for lane in lanes:
+            main.wait_stream(lane.stream)
 
     def step(self) -> float:
         """One refine iteration; returns the total loss over ALL views (all ranks)."""
@@ -327,7 +335,7 @@ class AdamRefiner:
             torch.cuda.current_stream(self.dev).synchronize()
             if not int(self.host_stats[4]):
                 break
-            self.view.reserve_pairs(int(self.host_stats[1]) * 5 // 4 + 4096)
+            self._reserve(int(self.host_stats[1]) * 5 // 4 + 4096)
         allreduce_grads(self.grads, self.loss_acc, self.group)
         self.step_count += 1
         N.check(N.lib().s2d_adam_step(torch.cuda.current_stream(self.dev).cuda_stream, N.dptr(self.params),
