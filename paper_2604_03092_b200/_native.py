@@ -13,7 +13,7 @@ import os
 import re
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libsurfel2d.so")
+LIB_PATH = os.environ.get("S2D_LIB_PATH") or os.path.join(_HERE, "lib", "libsurfel2d.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "surfel2d.h")
 
 S2D_OK = 0

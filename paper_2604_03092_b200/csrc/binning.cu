@@ -1,13 +1,16 @@
 // binning.cu — projection, depth order and tile binning.
 //
 //   k_project     per-surfel float64 projection (bit-exact with rasterizer.py:201-281),
-//                 64-B splat record, bbox, and an ORDER-PRESERVING compaction of the
-//                 on-screen surfels (chained scan, decoupled look-back) so the sort
-//                 input is in input-index order.
-//   k_radix_hist  digit histograms of all passes in one read.
-//   k_onesweep    one stable LSD radix pass (8-bit digits) with decoupled look-back.
-//   k_tie_fix     the depth key is the upper 32 bits of the float64 z; runs of equal
-//                 keys whose z differ in the low bits are re-sorted by (z64, index),
+//                 64-B splat record, bbox; writes (depth key, index) for every surfel in
+//                 index order, off-screen surfels keyed by a sentinel; per-view min/max key.
+//   k_radix_hist  rebases the keys to 24 bits (key - min, shifted right only if the
+//                 depth range spans more than 2^24 key steps) and builds the digit
+//                 histograms of all 3 passes in one read.
+//   k_onesweep    one stable LSD radix pass (8-bit digits) with decoupled look-back; the
+//                 first depth pass drops sentinel keys, i.e. it also compacts the
+//                 on-screen surfels (order-preserving, so ties stay in index order).
+//   k_tie_fix     the depth key is the (rebased) upper 32 bits of the float64 z; runs of
+//                 equal keys whose z differ in the low bits are re-sorted by (z64, index),
 //                 giving exactly the reference order lexsort((index, z))
 //                 (rasterizer.py:318-320).
 //   k_scan_emit   chained scan of per-surfel tile counts in depth order, fused with
@@ -51,19 +54,14 @@ __device__ __forceinline__ uint32_t block_exclusive_scan_256(uint32_t v, uint32_
 // ------------------------------------------------------------------ projection
 
 __global__ void __launch_bounds__(kProjThreads) k_project(const ProjectArgs a) {
-    __shared__ int s_tile;
-    __shared__ uint32_t s_w[8];
-    __shared__ uint32_t s_base;
-    if (threadIdx.x == 0) s_tile = atomicAdd(a.ticket, 1);
-    __syncthreads();
-    const int tile = s_tile;
-    const int64_t i = (int64_t)tile * kProjThreads + threadIdx.x;
+    const int64_t i = (int64_t)blockIdx.x * kProjThreads + threadIdx.x;
     const ViewParams &P = a.P;
-    if (tile == 0 && threadIdx.x == 0) *a.P_out = a.P;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *a.P_out = a.P;
     bool on = false, degen = false;
-    ExactProj e;
+    uint32_t key = 0xffffffffu;
     if (i < P.n) {
         const ParamView pv(a.params, P.n);
+        ExactProj e;
         project_exact(P, pv, i, e);
         on = e.on_screen;
         degen = e.in_front && !e.valid;
@@ -89,60 +87,66 @@ __global__ void __launch_bounds__(kProjThreads) k_project(const ProjectArgs a) {
             for (int k = 0; k < 3; ++k)
                 nn[k] = P.r_cw[3 * k] * e.R[2] + P.r_cw[3 * k + 1] * e.R[5] + P.r_cw[3 * k + 2] * e.R[8];
             const double sg = (nn[0] * e.p[0] + nn[1] * e.p[1] + nn[2] * e.p[2]) > 0.0 ? -1.0 : 1.0;
-            // guard band of the float32 Mahalanobis distance
+            // guard band of the float32 Mahalanobis distance (covers float32 rounding of Minv,
+            // of the pixel offset and of u, v, m)
             const double kappa = sqrt(e.lmax / e.lmin);
-            // (covers float32 rounding of Minv, of the pixel offset and of u, v, m; DESIGN.md
-            // "guard bands")
             const double gb = 4e-5 * kappa + 1e-5 / sqrt(e.lmin) + 4e-6;
             r.q3 = make_float4((float)(sg * nn[0]), (float)(sg * nn[1]), (float)(sg * nn[2]), (float)gb);
             a.rec[i] = r;
             a.rect[i] = make_short4((short)e.x0, (short)e.x1, (short)e.y0, (short)e.y1);
             a.z64[i] = e.p[2];
+            key = (uint32_t)((uint64_t)__double_as_longlong(e.p[2]) >> 32);  // z > 0: monotone
         }
+        a.keys[i] = key;
+        a.vals[i] = (uint32_t)i;
     }
-    // degenerate count (rasterizer.py:244)
-    const uint32_t dm = __ballot_sync(kFull, degen);
-    if ((threadIdx.x & 31) == 0 && dm) atomicAdd(&a.stats->degenerate, __popc(dm));
-    // order-preserving compaction
-    uint32_t tot;
-    const uint32_t ex = block_exclusive_scan_256(on ? 1u : 0u, s_w, &tot);
-    if (threadIdx.x < 32) {
-        const uint32_t pre = lookback_warp(a.status, tile, tot);
-        if (threadIdx.x == 0) {
-            s_base = pre;
-            const int ntiles = (int)((P.n + kProjThreads - 1) / kProjThreads);
-            if (tile == ntiles - 1) a.stats->visible = (int)(pre + tot);
+    // per-view counters: visible, degenerate (rasterizer.py:244), key range
+    const uint32_t vm = __ballot_sync(kFull, on), dm = __ballot_sync(kFull, degen);
+    uint32_t kmin = on ? key : 0xffffffffu, kmax = on ? key : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        kmin = min(kmin, __shfl_xor_sync(kFull, kmin, o));
+        kmax = max(kmax, __shfl_xor_sync(kFull, kmax, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (vm) {
+            atomicAdd(&a.stats->visible, __popc(vm));
+            atomicMax(a.key_range, ~kmin);  // the sync region starts zeroed: store ~min
+            atomicMax(a.key_range + 1, kmax);
         }
-    }
-    __syncthreads();
-    if (on) {
-        const uint32_t pos = s_base + ex;
-        a.keys[pos] = (uint32_t)((uint64_t)__double_as_longlong(e.p[2]) >> 32);
-        a.vals[pos] = (uint32_t)i;
+        if (dm) atomicAdd(&a.stats->degenerate, __popc(dm));
     }
 }
 
 // --------------------------------------------------------------- radix sorting
 
-__global__ void __launch_bounds__(256) k_radix_hist(const uint32_t *__restrict__ keys,
-                                                    const int *__restrict__ d_n, int passes,
+// Depth keys: rebase to [0, 2^24) (shift only if the key range needs more bits; ties are
+// resolved by k_tie_fix) and histogram the three 8-bit digits.  Sentinels stay sentinels.
+__global__ void __launch_bounds__(256) k_radix_hist(uint32_t *__restrict__ keys, int n,
+                                                    const uint32_t *__restrict__ key_range,
                                                     uint32_t *__restrict__ hist) {
-    __shared__ uint32_t sh[4 * kRadix];
-    for (int k = threadIdx.x; k < 4 * kRadix; k += blockDim.x) sh[k] = 0;
+    __shared__ uint32_t sh[3 * kRadix];
+    for (int k = threadIdx.x; k < 3 * kRadix; k += blockDim.x) sh[k] = 0;
     __syncthreads();
-    const int n = *d_n;
+    const uint32_t kmin = ~key_range[0], kmax = key_range[1];
+    const uint32_t span = kmax >= kmin ? kmax - kmin : 0u;
+    const int shift = span >= (1u << 24) ? (32 - __clz(span)) - 24 : 0;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const uint32_t k = keys[i];
-        for (int p = 0; p < passes; ++p) atomicAdd(&sh[p * kRadix + ((k >> (kRadixBits * p)) & (kRadix - 1))], 1u);
+        uint32_t k = keys[i];
+        if (k == 0xffffffffu) continue;
+        k = (k - kmin) >> shift;
+        keys[i] = k;
+#pragma unroll
+        for (int p = 0; p < 3; ++p) atomicAdd(&sh[p * kRadix + ((k >> (kRadixBits * p)) & (kRadix - 1))], 1u);
     }
     __syncthreads();
-    for (int k = threadIdx.x; k < passes * kRadix; k += blockDim.x)
+    for (int k = threadIdx.x; k < 3 * kRadix; k += blockDim.x)
         if (sh[k]) atomicAdd(&hist[k], sh[k]);
 }
 
 __global__ void __launch_bounds__(kSortThreads) k_onesweep(
     const uint32_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint32_t *__restrict__ kout,
-    uint32_t *__restrict__ vout, const int *__restrict__ d_n, int shift,
+    uint32_t *__restrict__ vout, const int *__restrict__ d_n, int n_host, int shift,
     const uint32_t *__restrict__ hist, uint32_t *status, int *ticket) {
     __shared__ uint32_t s_wh[8][kRadix];
     __shared__ uint32_t s_base[kRadix];
@@ -154,7 +158,8 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
     for (int w = 0; w < 8; ++w) s_wh[w][tid] = 0;
     __syncthreads();
     const int tile = s_tile;
-    const int n = *d_n;
+    const bool drop = n_host >= 0;  // first pass over all surfels: sentinel keys are dropped
+    const int n = drop ? n_host : *d_n;
     const int start = tile * kSortTile;
     if (start >= n) return;
     const int wbase = start + warp * 32 * kSortItems;
@@ -169,7 +174,7 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
 #pragma unroll
     for (int r = 0; r < kSortItems; ++r) {
         const int idx = wbase + r * 32 + lane;
-        const bool valid = idx < n;
+        const bool valid = idx < n && !(drop && key[r] == 0xffffffffu);
         const uint32_t d = (key[r] >> shift) & (kRadix - 1);
         const uint32_t peers = __match_any_sync(kFull, valid ? d : (kRadix + lane));
         const uint32_t rank = __popc(peers & lt);
@@ -197,7 +202,7 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
 #pragma unroll
     for (int r = 0; r < kSortItems; ++r) {
         const int idx = wbase + r * 32 + lane;
-        if (idx < n) {
+        if (idx < n && !(drop && key[r] == 0xffffffffu)) {
             const uint32_t d = (key[r] >> shift) & (kRadix - 1);
             const uint32_t o = s_base[d] + s_wh[warp][d] + pos[r];
             kout[o] = key[r];
@@ -319,29 +324,29 @@ __global__ void __launch_bounds__(256) k_tile_ranges(const uint32_t *__restrict_
 }  // namespace
 
 void launch_project(const ProjectArgs &a, cudaStream_t s) {
-    const int blocks = (int)((a.P.n + kProjThreads - 1) / kProjThreads);
+    const int blocks = (int)((a.P.n + kProjThreads - 1) / kProjThreads);  // one surfel per thread
     if (blocks > 0) {
         count_launch();
         k_project<<<blocks, kProjThreads, 0, s>>>(a);
     }
 }
 
-void launch_radix_hist(const uint32_t *keys, const int *d_n, int cap, int passes, uint32_t *hist,
-                       cudaStream_t s) {
-    int blocks = (cap + 255) / 256;
+void launch_radix_hist(uint32_t *keys, int n, const uint32_t *key_range, uint32_t *hist, cudaStream_t s) {
+    int blocks = (n + 255) / 256;
     if (blocks > 592) blocks = 592;
     if (blocks < 1) blocks = 1;
     count_launch();
-    k_radix_hist<<<blocks, 256, 0, s>>>(keys, d_n, passes, hist);
+    k_radix_hist<<<blocks, 256, 0, s>>>(keys, n, key_range, hist);
 }
 
 void launch_onesweep(const uint32_t *kin, const uint32_t *vin, uint32_t *kout, uint32_t *vout,
-                     const int *d_n, int cap, int shift, const uint32_t *hist_pass,
+                     const int *d_n, int cap, int n_host, int shift, const uint32_t *hist_pass,
                      uint32_t *status, int *ticket, cudaStream_t s) {
     const int blocks = (cap + kSortTile - 1) / kSortTile;
     if (blocks > 0) {
         count_launch();
-        k_onesweep<<<blocks, kSortThreads, 0, s>>>(kin, vin, kout, vout, d_n, shift, hist_pass, status, ticket);
+        k_onesweep<<<blocks, kSortThreads, 0, s>>>(kin, vin, kout, vout, d_n, n_host, shift, hist_pass, status,
+                                                   ticket);
     }
 }
 

@@ -1,7 +1,7 @@
 // capi.cu — extern "C" boundary (include/surfel2d.h): per-view workspace arena,
 // host-side float64 pose math, and the launch sequence of one view:
 //
-//   memset(sync region) -> k_project -> k_radix_hist -> 4 x k_onesweep (depth)
+//   memset(sync region) -> k_project -> k_radix_hist -> 3 x k_onesweep (depth)
 //   -> k_tie_fix -> k_scan_emit -> 1..2 x k_onesweep (tile id) -> k_tile_ranges
 //   -> k_raster_fwd                       [s2d_forward]
 //   -> k_raster_bwd -> k_project_bwd      [s2d_backward]
@@ -230,7 +230,6 @@ struct s2d_view {
 namespace {
 
 int layout_sync(s2d_view *v, int64_t n, int64_t pcap, int ntiles) {
-    const int64_t proj_tiles = (n + kProjThreads - 1) / kProjThreads + 1;
     const int64_t sort_tiles = (n + kSortTile - 1) / kSortTile + 1;
     const int64_t emit_tiles = (n + kEmitTile - 1) / kEmitTile + 1;
     const int64_t psort_tiles = (pcap + kSortTile - 1) / kSortTile + 1;
@@ -242,9 +241,9 @@ int layout_sync(s2d_view *v, int64_t n, int64_t pcap, int ntiles) {
     };
     const size_t o_stats = take(sizeof(s2d_view_stats));
     const size_t o_tickets = take(16 * sizeof(int));
-    const size_t o_proj = take((size_t)proj_tiles * 4);
-    const size_t o_dhist = take(4 * kRadix * 4);
-    const size_t o_dstat = take((size_t)4 * sort_tiles * kRadix * 4);
+    const size_t o_krange = take(2 * 4);
+    const size_t o_dhist = take(3 * kRadix * 4);
+    const size_t o_dstat = take((size_t)3 * sort_tiles * kRadix * 4);
     const size_t o_emit = take((size_t)emit_tiles * 4);
     const size_t o_phist = take(2 * kRadix * 4);
     const size_t o_pstat = take((size_t)2 * psort_tiles * kRadix * 4);
@@ -257,7 +256,7 @@ int layout_sync(s2d_view *v, int64_t n, int64_t pcap, int ntiles) {
     uint8_t *b = v->sync;
     v->sr.stats = reinterpret_cast<s2d_view_stats *>(b + o_stats);
     v->sr.tickets = reinterpret_cast<int *>(b + o_tickets);
-    v->sr.proj_status = reinterpret_cast<uint32_t *>(b + o_proj);
+    v->sr.key_range = reinterpret_cast<uint32_t *>(b + o_krange);
     v->sr.depth_hist = reinterpret_cast<uint32_t *>(b + o_dhist);
     v->sr.depth_status = reinterpret_cast<uint32_t *>(b + o_dstat);
     v->sr.emit_status = reinterpret_cast<uint32_t *>(b + o_emit);
@@ -332,17 +331,17 @@ int view_forward(s2d_view *v, cudaStream_t s, const float *params, int64_t n, co
         pa.keys = v->keys[0];
         pa.vals = v->vals[0];
         pa.stats = sr.stats;
-        pa.status = sr.proj_status;
-        pa.ticket = sr.tickets + 0;
+        pa.key_range = sr.key_range;
         launch_project(pa, s);
         mark();
-        // depth order: 4 stable 8-bit passes over the upper 32 bits of float64 z
-        launch_radix_hist(v->keys[0], d_v, (int)n, 4, sr.depth_hist, s);
+        // depth order: keys rebased to 24 bits, 3 stable 8-bit passes; the first pass reads all
+        // n surfels in index order and drops the off-screen ones (order-preserving compaction)
+        launch_radix_hist(v->keys[0], (int)n, sr.key_range, sr.depth_hist, s);
         const int64_t sort_tiles = (n + kSortTile - 1) / kSortTile + 1;
         int cur = 0;
-        for (int p = 0; p < 4; ++p) {
+        for (int p = 0; p < 3; ++p) {
             launch_onesweep(v->keys[cur], v->vals[cur], v->keys[cur ^ 1], v->vals[cur ^ 1], d_v, (int)n,
-                            kRadixBits * p, sr.depth_hist + p * kRadix,
+                            p == 0 ? (int)n : -1, kRadixBits * p, sr.depth_hist + p * kRadix,
                             sr.depth_status + (size_t)p * sort_tiles * kRadix, sr.tickets + 1 + p, s);
             cur ^= 1;
         }
@@ -371,7 +370,7 @@ int view_forward(s2d_view *v, cudaStream_t s, const float *params, int64_t n, co
         int pc = 0;
         for (int p = 0; p < ppass; ++p) {
             launch_onesweep(v->pkeys[pc], v->pvals[pc], v->pkeys[pc ^ 1], v->pvals[pc ^ 1],
-                            &sr.stats->pairs_stored, (int)v->pcap, kRadixBits * p, sr.pair_hist + p * kRadix,
+                            &sr.stats->pairs_stored, (int)v->pcap, -1, kRadixBits * p, sr.pair_hist + p * kRadix,
                             sr.pair_status + (size_t)p * psort_tiles * kRadix, sr.tickets + 6 + p, s);
             pc ^= 1;
         }

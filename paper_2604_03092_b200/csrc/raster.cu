@@ -22,6 +22,13 @@
 
 #include "s2d_kernels.h"
 
+#ifndef S2D_FWD_MINB
+#define S2D_FWD_MINB 3
+#endif
+#ifndef S2D_BWD_MINB
+#define S2D_BWD_MINB 3
+#endif
+
 namespace s2d {
 
 namespace {
@@ -167,7 +174,7 @@ __device__ __forceinline__ int warp_cull(const short4 *rect, int nrec, int wx0, 
 }
 
 template <bool kArg, bool kMaxW, bool kNormal>
-__global__ void __launch_bounds__(kRasterThreads, 3) k_raster_fwd(const RasterArgs a) {
+__global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(const RasterArgs a) {
     __shared__ Stage st;
     __shared__ uint8_t s_list[kRasterThreads / 32][kRasterThreads];
     const ViewParams &P = a.P;
@@ -333,7 +340,7 @@ __device__ __forceinline__ float warp_reduce16(float (&v)[16], int lane) {
 __device__ __forceinline__ float sgnf(float x) { return x > 0.f ? 1.f : (x < 0.f ? -1.f : 0.f); }
 
 template <bool kFull>  // kFull: normal / accumulation seeds present (external loss)
-__global__ void __launch_bounds__(kRasterThreads, 3) k_raster_bwd(const RasterArgs a) {
+__global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(const RasterArgs a) {
     __shared__ Stage st;
     __shared__ uint8_t s_list[kRasterThreads / 32][kRasterThreads];
     __shared__ int s_lmax[8];

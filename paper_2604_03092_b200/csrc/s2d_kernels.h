@@ -28,9 +28,9 @@ constexpr int kEmitTile = 256 * kEmitItems;
 struct SyncRegion {
     s2d_view_stats *stats;     // device stats (first, 32 B)
     int *tickets;              // [16]
-    uint32_t *proj_status;     // [ceil(n / kProjThreads)]
-    uint32_t *depth_hist;      // [4 * kRadix]
-    uint32_t *depth_status;    // [4][ceil(n / kSortTile) * kRadix]
+    uint32_t *key_range;       // [2]: ~min, max depth key
+    uint32_t *depth_hist;      // [3 * kRadix]
+    uint32_t *depth_status;    // [3][ceil(n / kSortTile) * kRadix]
     uint32_t *emit_status;     // [ceil(n / kEmitTile)]
     uint32_t *pair_hist;       // [2 * kRadix]
     uint32_t *pair_status;     // [2][ceil(pcap / kSortTile) * kRadix]
@@ -51,15 +51,14 @@ struct ProjectArgs {
     uint32_t *keys;
     uint32_t *vals;
     s2d_view_stats *stats;
-    uint32_t *status;
-    int *ticket;
+    uint32_t *key_range;  // [~min, max] of on-screen depth keys (sync region, zeroed)
 };
 void launch_project(const ProjectArgs &a, cudaStream_t s);
 
-void launch_radix_hist(const uint32_t *keys, const int *d_n, int cap, int passes, uint32_t *hist,
-                       cudaStream_t s);
+void launch_radix_hist(uint32_t *keys, int n, const uint32_t *key_range, uint32_t *hist, cudaStream_t s);
+// n_host >= 0: pass over n_host entries that drops sentinel keys (0xffffffff); else *d_n entries
 void launch_onesweep(const uint32_t *kin, const uint32_t *vin, uint32_t *kout, uint32_t *vout,
-                     const int *d_n, int cap, int shift, const uint32_t *hist_pass,
+                     const int *d_n, int cap, int n_host, int shift, const uint32_t *hist_pass,
                      uint32_t *status, int *ticket, cudaStream_t s);
 void launch_tie_fix(const uint32_t *keys, uint32_t *vals, const double *z64, const int *d_n, int cap,
                     uint32_t *claim, cudaStream_t s);
