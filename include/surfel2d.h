@@ -83,7 +83,7 @@ typedef struct s2d_view_stats {
 /* Introspection of the last forward of a view (device pointers; parity tests). */
 typedef struct s2d_view_debug {
     const uint32_t *order;      /* (V,) input indices in depth order (rasterizer.py:318-320) */
-    const uint32_t *pair_tiles; /* (P,) tile id of each pair, sorted */
+    const uint32_t *pair_tiles; /* (P,) tile id (low 16 bits; bits 16-23: warp-block cull mask), sorted */
     const uint32_t *pair_ids;   /* (P,) surfel index of each pair: per-tile lists in depth order */
     const int32_t *ranges;      /* (ntiles, 2) [start, end) into the pair arrays */
     const int16_t *bbox;        /* (n, 4) x0, x1, y0, y1 (valid where flags & 4) */

@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(256) k_scan_emit(const EmitArgs a) {
             for (int tx = tx0; tx <= tx1; ++tx) {
                 const uint32_t t = (uint32_t)(ty * a.ntx + tx);
                 if (off < a.pcap) {
-                    a.pkeys[off] = t;
+                    a.pkeys[off] = t;  // bits 16-23 receive the warp-block mask in the forward
                     a.pvals[off] = ids[j];
                 }
                 ++off;
@@ -316,9 +316,9 @@ __global__ void __launch_bounds__(256) k_tile_ranges(const uint32_t *__restrict_
     int np = *d_p;
     if ((uint32_t)np > pcap) return;  // overflow: leave all tiles empty
     if (i >= np) return;
-    const uint32_t k = pkeys[i];
-    if (i == 0 || pkeys[i - 1] != k) ranges[k].x = i;
-    if (i == np - 1 || pkeys[i + 1] != k) ranges[k].y = i + 1;
+    const uint32_t k = pkeys[i] & 0xffffu;
+    if (i == 0 || (pkeys[i - 1] & 0xffffu) != k) ranges[k].x = i;
+    if (i == np - 1 || (pkeys[i + 1] & 0xffffu) != k) ranges[k].y = i + 1;
 }
 
 }  // namespace

@@ -389,6 +389,7 @@ int view_forward(s2d_view *v, cudaStream_t s, const float *params, int64_t n, co
     ra.params = params;
     ra.ranges = sr.ranges;
     ra.pair_ids = v->pvals[v->pair_buf];
+    ra.pair_keys = v->pkeys[v->pair_buf];
     ra.rec = v->rec;
     ra.rect = v->rect;
     ra.aux = v->aux;
@@ -573,6 +574,7 @@ int s2d_backward(s2d_view *v, void *stream, const float *params, int64_t n, cons
     ra.params = params;
     ra.ranges = v->sr.ranges;
     ra.pair_ids = v->pvals[v->pair_buf];
+    ra.pair_keys = v->pkeys[v->pair_buf];
     ra.rec = v->rec;
     ra.rect = v->rect;
     ra.aux = v->aux;

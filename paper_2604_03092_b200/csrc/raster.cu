@@ -77,22 +77,28 @@ __device__ __forceinline__ float fast_exp2(float x) {
 
 struct Stage {
     SplatRecord rec[2][kRasterThreads];
-    short4 rect[2][kRasterThreads];
     uint32_t id[2][kRasterThreads];
+    uint8_t mask[2][kRasterThreads];  // warp blocks the splat's ellipse reaches (k_scan_emit)
 };
 
-__device__ __forceinline__ void stage_issue(Stage &st, int buf, int k, uint32_t id, bool valid,
-                                            const SplatRecord *rec, const short4 *rect) {
+// Stage list entry k of a batch: the 64-B record by cp.async, id and cull mask by plain stores
+// (made visible to the other warps by the __syncthreads that precedes their use).
+__device__ __forceinline__ void stage_issue(Stage &st, int buf, int k, uint2 kv, bool valid,
+                                            const SplatRecord *rec) {
     if (valid) {
-        const float4 *g = reinterpret_cast<const float4 *>(rec + id);
+        const float4 *g = reinterpret_cast<const float4 *>(rec + kv.y);
         float4 *d = reinterpret_cast<float4 *>(&st.rec[buf][k]);
         cp_async16(d + 0, g + 0);
         cp_async16(d + 1, g + 1);
         cp_async16(d + 2, g + 2);
         cp_async16(d + 3, g + 3);
-        cp_async8(&st.rect[buf][k], rect + id);
     }
-    st.id[buf][k] = id;
+    st.id[buf][k] = kv.y;
+    st.mask[buf][k] = valid ? (uint8_t)(kv.x >> 16) : (uint8_t)0;
+}
+
+__device__ __forceinline__ uint2 load_pair(const RasterArgs &a, int pos, bool valid) {
+    return valid ? make_uint2(a.pair_keys[pos], a.pair_ids[pos]) : make_uint2(0u, 0u);
 }
 
 // Per-pixel evaluation shared by forward and backward (must take identical decisions).
@@ -106,33 +112,32 @@ struct PairEval {
 };
 
 __device__ __forceinline__ bool eval_pair(const ViewParams &P, const ViewParams *Pg, const float *params,
-                                          const SplatRecord &r, uint32_t id, float lx, float ly, int px, int py,
-                                          PairEval &o, int &guard_hits) {
-    // staged record: q0 = (cx_hi - tile_x0, cy_hi - tile_y0, half2 lo, opacity) — see stage_finish
+                                          const SplatRecord &r, const uint32_t *idp, float pxf, float pyf, int px,
+                                          int py, PairEval &o, int &guard_hits) {
+    // record: q0 = (cx_hi, cy_hi, half2 (cx_lo, cy_lo), opacity)
     const float4 q0 = r.q0;
     const uint32_t lob = __float_as_uint(q0.z);
     const __half2 lo = *reinterpret_cast<const __half2 *>(&lob);
     // explicit round-to-nearest intrinsics: forward and backward must take
     // bit-identical decisions, so nothing here may be contracted differently
-    o.dx = __fsub_rn(__fsub_rn(lx, q0.x), __low2float(lo));
-    o.dy = __fsub_rn(__fsub_rn(ly, q0.y), __high2float(lo));
+    o.dx = __fsub_rn(__fsub_rn(pxf, q0.x), __low2float(lo));
+    o.dy = __fsub_rn(__fsub_rn(pyf, q0.y), __high2float(lo));
     o.u = __fmaf_rn(r.q1.x, o.dx, __fmul_rn(r.q1.y, o.dy));
     o.v = __fmaf_rn(r.q1.z, o.dx, __fmul_rn(r.q1.w, o.dy));
     const float m = __fmaf_rn(o.u, o.u, __fmul_rn(o.v, o.v));
-    const float gbs = r.q3.w;  // guard band, negative when the weight can reach the clamp
-    const float gb = fabsf(gbs);
+    const float gb = r.q3.w;  // guard band of m
     if (m > P.maha_cut_f + gb) return false;
     o.g = fast_exp2(__fmul_rn(m, -0.72134752044448170368f));  // exp(-m/2); m <= sigma^2 + gb keeps it normal
     float w = __fmul_rn(q0.w, o.g);
     bool band = m >= P.maha_cut_f - gb;
     o.clamped = false;
-    if (gbs < 0.0f) {  // opacity close enough to the clamp for the weight to reach it
+    if (q0.w > P.w_clamp_f - 8e-6f) {  // opacity close enough to the clamp for the weight to reach it
         band |= fabsf(w - P.w_clamp_f) <= 4e-6f;
         o.clamped = w > P.w_clamp_f;
     }
     if (band) {
         ++guard_hits;
-        const int rr = guard_resolve(Pg, params, id, px, py);
+        const int rr = guard_resolve(Pg, params, *idp, px, py);
         if (!(rr & 1)) return false;
         o.clamped = (rr & 2) != 0;
     }
@@ -141,30 +146,17 @@ __device__ __forceinline__ bool eval_pair(const ViewParams &P, const ViewParams 
     return w > 0.0f;
 }
 
-// After this thread's cp.async copies of a batch landed: make its staged record's centre
-// tile-relative (cx_hi - tile_x0 is exact: tile_x0 is an integer no larger than the centre's
-// magnitude scale), and flag in the sign of the guard band whether the opacity can reach the
-// weight clamp.  Identical in forward and backward.
-__device__ __forceinline__ void stage_finish(SplatRecord &r, float tx0, float ty0, float clamp_f) {
-    r.q0.x = __fsub_rn(r.q0.x, tx0);
-    r.q0.y = __fsub_rn(r.q0.y, ty0);
-    if (r.q0.w > clamp_f - 8e-6f) r.q3.w = -r.q3.w;
-}
-
-// Ordered list (into s_list) of the staged records whose integer bbox touches the warp's
-// 8x4 pixel block; returns its length.  `limit` excludes list positions > limit (backward).
-__device__ __forceinline__ int warp_cull(const short4 *rect, int nrec, int wx0, int wx1, int wy0, int wy1,
-                                         int lane, uint8_t *list, int base_pos, int limit) {
+// Ordered list (into s_list) of the staged records whose ellipse reaches this warp's 8x4
+// block (bit `warp` of the per-pair mask built at emission); returns its length.  `limit`
+// excludes list positions > limit (backward).
+__device__ __forceinline__ int warp_cull(const uint8_t *mask, int nrec, int warp, int lane, uint8_t *list,
+                                         int base_pos, int limit) {
     const uint32_t lt = lanemask_lt();
     int cnt = 0;
 #pragma unroll
     for (int q = 0; q < kRasterThreads / 32; ++q) {
         const int k = q * 32 + lane;
-        bool hit = false;
-        if (k < nrec && base_pos + k <= limit) {
-            const short4 r = rect[k];
-            hit = (r.x <= wx1) & (r.y >= wx0) & (r.z <= wy1) & (r.w >= wy0);
-        }
+        const bool hit = k < nrec && base_pos + k <= limit && ((mask[k] >> warp) & 1u);
         const uint32_t m = __ballot_sync(kFull, hit);
         if (hit) list[cnt + __popc(m & lt)] = (uint8_t)k;
         cnt += __popc(m);
@@ -185,8 +177,7 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
     const int wx1 = min(wx0 + 7, P.W - 1), wy1 = min(wy0 + 3, P.H - 1);
     const int px = wx0 + (lane & 7), py = wy0 + (lane >> 3);
     const bool inside = px < P.W && py < P.H;
-    const float tx0f = (float)(tx * kTile), ty0f = (float)(ty * kTile);
-    const float lx = (float)(px - tx * kTile), ly = (float)(py - ty * kTile);
+    const float pxf = (float)px, pyf = (float)py;
     const int2 rg = a.ranges[tile];
     const int cnt = rg.y - rg.x;
 
@@ -200,26 +191,34 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
 
     const int nb = (cnt + kRasterThreads - 1) / kRasterThreads;
     if (nb > 0) {
-        uint32_t id_next = tid < cnt ? a.pair_ids[rg.x + tid] : 0u;
-        stage_issue(st, 0, tid, id_next, tid < cnt, a.rec, a.rect);
+        uint2 kv_next = load_pair(a, rg.x + tid, tid < cnt);
+        stage_issue(st, 0, tid, kv_next, tid < cnt, a.rec);
         cp_commit();
-        id_next = (kRasterThreads + tid < cnt) ? a.pair_ids[rg.x + kRasterThreads + tid] : 0u;
+        kv_next = load_pair(a, rg.x + kRasterThreads + tid, kRasterThreads + tid < cnt);
         for (int b = 0; b < nb; ++b) {
             const int buf = b & 1;
             if (b + 1 < nb) {
                 const int k1 = (b + 1) * kRasterThreads + tid;
-                stage_issue(st, buf ^ 1, tid, id_next, k1 < cnt, a.rec, a.rect);
+                stage_issue(st, buf ^ 1, tid, kv_next, k1 < cnt, a.rec);
                 const int k2 = (b + 2) * kRasterThreads + tid;
-                id_next = k2 < cnt ? a.pair_ids[rg.x + k2] : 0u;
+                kv_next = load_pair(a, rg.x + k2, k2 < cnt);
             }
             cp_commit();
             cp_wait<1>();
-            if (b * kRasterThreads + tid < cnt) stage_finish(st.rec[buf][tid], tx0f, ty0f, P.w_clamp_f);
+            {   // this thread's record landed: warp-block cull mask (reused by the backward)
+                const int pos = rg.x + b * kRasterThreads + tid;
+                if (b * kRasterThreads + tid < cnt) {
+                    const uint32_t m = warp_block_mask(tx, ty, a.rect[st.id[buf][tid]], st.rec[buf][tid],
+                                                       P.maha_cut_f);
+                    st.mask[buf][tid] = (uint8_t)m;
+                    a.pair_keys[pos] = (a.pair_keys[pos] & 0xffffu) | (m << 16);
+                }
+            }
             __syncthreads();
             const int base = b * kRasterThreads;
             const int nrec = min(kRasterThreads, cnt - base);
             if (!__all_sync(kFull, done)) {
-                const int nl = warp_cull(st.rect[buf], nrec, wx0, wx1, wy0, wy1, lane, list, 0, nrec);
+                const int nl = warp_cull(st.mask[buf], nrec, warp, lane, list, 0, nrec);
                 for (int j = 0; j < nl; ++j) {
                     const int k = list[j];
                     const uint32_t id = st.id[buf][k];
@@ -227,7 +226,7 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
                     if (!done) {
                         PairEval e;
                         const SplatRecord &r = st.rec[buf][k];
-                        if (eval_pair(P, a.Pg, a.params, r, id, lx, ly, px, py, e, guard)) {
+                        if (eval_pair(P, a.Pg, a.params, r, &st.id[buf][k], pxf, pyf, px, py, e, guard)) {
                             contrib = e.w * T;
                             const float4 q2 = r.q2;
                             c0 = fmaf(contrib, q2.x, c0);
@@ -353,8 +352,7 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
     const int wx1 = min(wx0 + 7, P.W - 1), wy1 = min(wy0 + 3, P.H - 1);
     const int px = wx0 + (lane & 7), py = wy0 + (lane >> 3);
     const bool inside = px < P.W && py < P.H;
-    const float tx0f = (float)(tx * kTile), ty0f = (float)(ty * kTile);
-    const float lx = (float)(px - tx * kTile), ly = (float)(py - ty * kTile);
+    const float pxf = (float)px, pyf = (float)py;
     const int2 rg = a.ranges[tile];
     const int p = py * P.W + px;
 
@@ -452,25 +450,21 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
     {
         int b = nb - 1;
         int k0 = b * kRasterThreads + tid;
-        uint32_t id0 = k0 < cnt ? a.pair_ids[rg.x + k0] : 0u;
-        stage_issue(st, b & 1, tid, id0, k0 < cnt, a.rec, a.rect);
+        stage_issue(st, b & 1, tid, load_pair(a, rg.x + k0, k0 < cnt), k0 < cnt, a.rec);
         cp_commit();
-        int kn = (b - 1) * kRasterThreads + tid;
-        uint32_t id_next = (b >= 1) ? a.pair_ids[rg.x + kn] : 0u;
+        uint2 kv_next = load_pair(a, rg.x + (b - 1) * kRasterThreads + tid, b >= 1);
         for (; b >= 0; --b) {
             const int buf = b & 1;
             if (b >= 1) {
-                stage_issue(st, buf ^ 1, tid, id_next, true, a.rec, a.rect);
-                const int k2 = (b - 2) * kRasterThreads + tid;
-                id_next = (b >= 2) ? a.pair_ids[rg.x + k2] : 0u;
+                stage_issue(st, buf ^ 1, tid, kv_next, true, a.rec);
+                kv_next = load_pair(a, rg.x + (b - 2) * kRasterThreads + tid, b >= 2);
             }
             cp_commit();
             cp_wait<1>();
-            if (b * kRasterThreads + tid < cnt) stage_finish(st.rec[buf][tid], tx0f, ty0f, P.w_clamp_f);
             __syncthreads();
             const int base = b * kRasterThreads;
             const int nrec = min(kRasterThreads, cnt - base);
-            const int nl = warp_cull(st.rect[buf], nrec, wx0, wx1, wy0, wy1, lane, s_list[warp], rg.x + base, wlast);
+            const int nl = warp_cull(st.mask[buf], nrec, warp, lane, s_list[warp], rg.x + base, wlast);
             for (int j = nl - 1; j >= 0; --j) {
                 const int k = s_list[warp][j];
                 const int pos = rg.x + base + k;
@@ -482,7 +476,7 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
                 if (pos <= last) {
                     PairEval e;
                     const SplatRecord &r = st.rec[buf][k];
-                    if (eval_pair(P, a.Pg, a.params, r, id, lx, ly, px, py, e, guard)) {
+                    if (eval_pair(P, a.Pg, a.params, r, &st.id[buf][k], pxf, pyf, px, py, e, guard)) {
                         contrib = true;
                         const float4 q1 = r.q1, q2 = r.q2;
                         float Ti;
@@ -546,6 +540,15 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
 }
 
 }  // namespace
+
+template <auto Kernel>
+static void ensure_smem(int bytes) {
+    static int done = 0;  // one flag per kernel (templated on the kernel itself)
+    if (done < bytes) {
+        cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        done = bytes;
+    }
+}
 
 template <bool kArg, bool kMaxW>
 static void fwd_dispatch(const RasterArgs &a, int tiles, cudaStream_t s) {

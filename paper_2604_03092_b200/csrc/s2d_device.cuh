@@ -212,6 +212,56 @@ __device__ __forceinline__ double exact_maha(const ExactProj &e, int x, int y) {
                 dmul(dmul(e.ic, dy), dy));
 }
 
+// Conservative minimum over the continuous rectangle [x0,x1]x[y0,y1] (pixel coordinates,
+// relative to the splat centre) of m(d) = |Minv d|^2: 0 if the centre is inside, else the
+// smallest of the four edge minima (1-D convex quadratics, minimiser clamped to the edge).
+__device__ __forceinline__ float rect_min_maha(float dx0, float dx1, float dy0, float dy1, float A, float B,
+                                              float C, float D) {
+    if (dx0 <= 0.f && dx1 >= 0.f && dy0 <= 0.f && dy1 >= 0.f) return 0.f;
+    const float ac = A * A + C * C, bd = B * B + D * D, x = A * B + C * D;
+    float best = 3.0e38f;
+    // horizontal edges y = dy0, dy1: minimise over d.x in [dx0, dx1]
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        const float y = e ? dy1 : dy0;
+        const float t = fminf(fmaxf(ac > 0.f ? -x * y / ac : 0.f, dx0), dx1);
+        const float u = A * t + B * y, v = C * t + D * y;
+        best = fminf(best, u * u + v * v);
+    }
+    // vertical edges x = dx0, dx1: minimise over d.y in [dy0, dy1]
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        const float xx = e ? dx1 : dx0;
+        const float t = fminf(fmaxf(bd > 0.f ? -x * xx / bd : 0.f, dy0), dy1);
+        const float u = A * xx + B * t, v = C * xx + D * t;
+        best = fminf(best, u * u + v * v);
+    }
+    return best;
+}
+
+// 8-bit mask of the warp blocks (8x4 pixels; warp w at (w & 1) * 8, (w >> 1) * 4 in the 16x16
+// tile) that the splat can blend into: the block must overlap the integer bbox and come within
+// the 3-sigma ellipse (padded by twice the guard band, so the culling is conservative with
+// respect to the reference's float64 decision).
+__device__ __forceinline__ uint32_t warp_block_mask(int tx, int ty, short4 rc, const SplatRecord &r, float cut) {
+    const uint32_t lob = __float_as_uint(r.q0.z);
+    const __half2 lo = *reinterpret_cast<const __half2 *>(&lob);
+    const float cx = r.q0.x + __low2float(lo), cy = r.q0.y + __high2float(lo);
+    const float thr = cut + 2.f * r.q3.w + 1e-3f;
+    uint32_t m = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+        const int bx0 = tx * kTile + (w & 1) * 8, by0 = ty * kTile + (w >> 1) * 4;
+        const int xa = max(bx0, (int)rc.x), xb = min(bx0 + 7, (int)rc.y);
+        const int ya = max(by0, (int)rc.z), yb = min(by0 + 3, (int)rc.w);
+        if (xa > xb || ya > yb) continue;
+        if (rect_min_maha((float)xa - cx, (float)xb - cx, (float)ya - cy, (float)yb - cy, r.q1.x, r.q1.y, r.q1.z,
+                          r.q1.w) <= thr)
+            m |= 1u << w;
+    }
+    return m;
+}
+
 // ---------------------------------------------------------- small utilities
 __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t m;

@@ -88,6 +88,7 @@ struct RasterArgs {
     const float *params;
     const int2 *ranges;
     const uint32_t *pair_ids;
+    uint32_t *pair_keys;  // tile id | warp-block mask << 16 (mask written by the forward)
     const SplatRecord *rec;
     const short4 *rect;
     int2 *aux;  // per pixel (last list position, float bits of T before it)

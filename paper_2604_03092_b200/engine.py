@@ -216,7 +216,7 @@ class View:
         v, p = st.visible, st.pairs_stored
         out = {
             "order": _wrap(d.order, (v,), "<i4", dev).clone(),
-            "pair_tiles": _wrap(d.pair_tiles, (p,), "<i4", dev).clone(),
+            "pair_tiles": _wrap(d.pair_tiles, (p,), "<i4", dev).clone() & 0xFFFF,  # low 16 bits: tile id
             "pair_ids": _wrap(d.pair_ids, (p,), "<i4", dev).clone(),
             "ranges": _wrap(d.ranges, (d.ntiles, 2), "<i4", dev).clone(),
             "bbox": _wrap(d.bbox, (n, 4), "<i2", dev).clone() if n else torch.zeros((0, 4), dtype=torch.int16),
