@@ -338,18 +338,74 @@ __device__ __forceinline__ float warp_reduce16(float (&v)[16], int lane) {
 
 __device__ __forceinline__ float sgnf(float x) { return x > 0.f ? 1.f : (x < 0.f ? -1.f : 0.f); }
 
-template <bool kFull>  // kFull: normal / accumulation seeds present (external loss)
+// Warp-private candidate ring for the backward: each warp streams ITS OWN culled
+// candidates (mask bit 16+warp of the pair key, written by the forward) from the tile
+// list, so warps never wait on each other at per-batch barriers.
+struct WarpRing {
+    SplatRecord rec[2][32];
+    uint32_t id[2][32];
+    int pos[2][32];
+};
+
+// Cursor over list positions [lo, hi) walked downwards in 32-wide chunks; lane l of the
+// current chunk holds position cb - 1 - l, `nxt` holds the chunk below it.  `pend` = hits of the chunk not yet handed out.
+struct RevCursor {
+    int lo, cb;
+    uint32_t pend;
+    uint32_t kid;  // current chunk's surfel id (this lane)
+    uint2 nxt;     // prefetched next chunk (key, id)
+};
+
+__device__ __forceinline__ uint2 load_chunk(const RasterArgs &a, int cb, int lo, int lane) {
+    const int pos = cb - 1 - lane;
+    return pos >= lo ? make_uint2(__ldcg(a.pair_keys + pos), __ldcg(a.pair_ids + pos)) : make_uint2(0u, 0u);
+}
+
+// Fill ring slot `buf` with up to 32 of this warp's candidates in descending list order
+// (cp.async for the records); returns how many.
+__device__ __forceinline__ int ring_fill(WarpRing &rg, int buf, RevCursor &c, const RasterArgs &a, int warp,
+                                         int lane) {
+    const uint32_t lt = lanemask_lt();
+    int n = 0;
+    while (n < 32) {
+        if (c.pend == 0) {
+            if (c.cb - 32 <= c.lo) break;  // no chunk below the current one
+            const uint2 cur = c.nxt;
+            c.cb -= 32;
+            c.nxt = load_chunk(a, c.cb - 32, c.lo, lane);
+            c.kid = cur.y;
+            c.pend = __ballot_sync(kFull, c.cb - 1 - lane >= c.lo && ((cur.x >> (16 + warp)) & 1u));
+            continue;
+        }
+        const int take = min(__popc(c.pend), 32 - n);
+        const int rank = __popc(c.pend & lt);
+        const bool mine = ((c.pend >> lane) & 1u) && rank < take;
+        if (mine) {
+            const int s = n + rank;
+            const float4 *g = reinterpret_cast<const float4 *>(a.rec + c.kid);
+            float4 *d = reinterpret_cast<float4 *>(&rg.rec[buf][s]);
+            cp_async16(d + 0, g + 0);
+            cp_async16(d + 1, g + 1);
+            cp_async16(d + 2, g + 2);
+            cp_async16(d + 3, g + 3);
+            rg.id[buf][s] = c.kid;
+            rg.pos[buf][s] = c.cb - 1 - lane;
+        }
+        c.pend &= ~__ballot_sync(kFull, mine);
+        n += take;
+    }
+    return n;
+}
+
+template <bool kExt>  // kExt: normal / accumulation seeds present (external loss)
 __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(const RasterArgs a) {
-    __shared__ Stage st;
-    __shared__ uint8_t s_list[kRasterThreads / 32][kRasterThreads];
-    __shared__ int s_lmax[8];
+    __shared__ WarpRing s_ring[kRasterThreads / 32];
     __shared__ float s_loss[8];
     const ViewParams &P = a.P;
     const int tile = blockIdx.x;
     const int tx = tile % P.ntx, ty = tile / P.ntx;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int wx0 = tx * kTile + (warp & 1) * 8, wy0 = ty * kTile + (warp >> 1) * 4;
-    const int wx1 = min(wx0 + 7, P.W - 1), wy1 = min(wy0 + 3, P.H - 1);
     const int px = wx0 + (lane & 7), py = wy0 + (lane >> 3);
     const bool inside = px < P.W && py < P.H;
     const float pxf = (float)px, pyf = (float)py;
@@ -412,127 +468,114 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
             }
         }
     }
-    // block reductions: loss, max(last)
+    // loss: block reduction (the kernel's only barrier); last blended position: warp max
+    int wlast = last;
     {
         float l = lpx;
-        int lm = last;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             l += __shfl_xor_sync(kFull, l, o);
-            lm = max(lm, __shfl_xor_sync(kFull, lm, o));
+            wlast = max(wlast, __shfl_xor_sync(kFull, wlast, o));
         }
-        if (lane == 0) {
-            s_loss[warp] = l;
-            s_lmax[warp] = lm;
-        }
+        if (lane == 0) s_loss[warp] = l;
     }
     __syncthreads();
-    int lmax = -1;
-    int wlast = s_lmax[warp];
     if (tid == 0 && a.loss_accum) {
         float l = 0.f;
         for (int w = 0; w < 8; ++w) l += s_loss[w];
         if (l != 0.f) atomicAdd(a.loss_accum, (double)l);
     }
-#pragma unroll
-    for (int w = 0; w < 8; ++w) lmax = max(lmax, s_lmax[w]);
-    if (lmax < rg.x) return;  // nothing blended in this tile (uniform)
+    if (wlast < rg.x) return;  // nothing blended in this warp's block (warp-uniform)
 
-    // ---- reverse traversal ----
+    // ---- reverse traversal of this warp's candidates ----
     float Tn = Tlast;          // transmittance before the later contributor
     bool first = true;
     float R = 1.f;             // prod_{j later} (1 - w_j)
     float S0 = 0.f, S1 = 0.f, S2 = 0.f, Sd = 0.f, Sn0 = 0.f, Sn1 = 0.f, Sn2 = 0.f;
     int guard = 0;
-    const int cnt = lmax + 1 - rg.x;   // list prefix that matters
-    const int nb = (cnt + kRasterThreads - 1) / kRasterThreads;
-    // batch b covers list positions [rg.x + b*256, ...); traverse b = nb-1 .. 0
-    {
-        int b = nb - 1;
-        int k0 = b * kRasterThreads + tid;
-        stage_issue(st, b & 1, tid, load_pair(a, rg.x + k0, k0 < cnt), k0 < cnt, a.rec);
+    WarpRing &ring = s_ring[warp];
+    RevCursor cur;
+    cur.lo = rg.x;
+    cur.cb = wlast + 1 + 32;  // virtual chunk above the range; the first advance lands on wlast
+    cur.pend = 0;
+    cur.kid = 0;
+    cur.nxt = load_chunk(a, wlast + 1, cur.lo, lane);
+    int buf = 0;
+    int n = ring_fill(ring, 0, cur, a, warp, lane);
+    cp_commit();
+    while (n > 0) {
+        const int nn = ring_fill(ring, buf ^ 1, cur, a, warp, lane);
         cp_commit();
-        uint2 kv_next = load_pair(a, rg.x + (b - 1) * kRasterThreads + tid, b >= 1);
-        for (; b >= 0; --b) {
-            const int buf = b & 1;
-            if (b >= 1) {
-                stage_issue(st, buf ^ 1, tid, kv_next, true, a.rec);
-                kv_next = load_pair(a, rg.x + (b - 2) * kRasterThreads + tid, b >= 2);
-            }
-            cp_commit();
-            cp_wait<1>();
-            __syncthreads();
-            const int base = b * kRasterThreads;
-            const int nrec = min(kRasterThreads, cnt - base);
-            const int nl = warp_cull(st.mask[buf], nrec, warp, lane, s_list[warp], rg.x + base, wlast);
-            for (int j = nl - 1; j >= 0; --j) {
-                const int k = s_list[warp][j];
-                const int pos = rg.x + base + k;
-                const uint32_t id = st.id[buf][k];
-                float v[16];
+        cp_wait<1>();
+        __syncwarp();
+        for (int s = 0; s < n; ++s) {
+            const int pos = ring.pos[buf][s];
+            float v[16];
 #pragma unroll
-                for (int t = 0; t < 16; ++t) v[t] = 0.f;
-                bool contrib = false;
-                if (pos <= last) {
-                    PairEval e;
-                    const SplatRecord &r = st.rec[buf][k];
-                    if (eval_pair(P, a.Pg, a.params, r, &st.id[buf][k], pxf, pyf, px, py, e, guard)) {
-                        contrib = true;
-                        const float4 q1 = r.q1, q2 = r.q2;
-                        float Ti;
-                        if (first) {
-                            Ti = Tlast;
-                            first = false;
-                        } else {
-                            Ti = Tn / (1.0f - e.w);
-                        }
-                        Tn = Ti;
-                        const float alpha = e.w * Ti;
-                        v[1] = gc0 * alpha;
-                        v[2] = gc1 * alpha;
-                        v[3] = gc2 * alpha;
-                        v[4] = gd * alpha;
-                        // dL/dw = T_i [ G.(c - S) + gd (z - Sd) + Gn.(n - Sn) ] + ga T_i R
-                        float dLdw = gc0 * (q2.x - S0) + gc1 * (q2.y - S1) + gc2 * (q2.z - S2) + gd * (q2.w - Sd);
-                        const float omw = 1.0f - e.w;
-                        if (kFull) {
-                            const float4 q3 = r.q3;
-                            v[11] = gn0 * alpha;
-                            v[12] = gn1 * alpha;
-                            v[13] = gn2 * alpha;
-                            dLdw += gn0 * (q3.x - Sn0) + gn1 * (q3.y - Sn1) + gn2 * (q3.z - Sn2) + ga * R;
-                            Sn0 = e.w * q3.x + omw * Sn0;
-                            Sn1 = e.w * q3.y + omw * Sn1;
-                            Sn2 = e.w * q3.z + omw * Sn2;
-                            R *= omw;
-                        }
-                        dLdw *= Ti;
-                        if (!e.clamped) {
-                            v[0] = dLdw * e.g;
-                            const float gm = -0.5f * e.w * dLdw;  // dL/dm
-                            const float gu = 2.f * gm * e.u, gv = 2.f * gm * e.v;
-                            v[5] = gu * e.dx;
-                            v[6] = gu * e.dy;
-                            v[7] = gv * e.dx;
-                            v[8] = gv * e.dy;
-                            v[9] = -(gu * q1.x + gv * q1.z);
-                            v[10] = -(gu * q1.y + gv * q1.w);
-                        }
-                        S0 = e.w * q2.x + omw * S0;
-                        S1 = e.w * q2.y + omw * S1;
-                        S2 = e.w * q2.z + omw * S2;
-                        Sd = e.w * q2.w + omw * Sd;
+            for (int t = 0; t < 16; ++t) v[t] = 0.f;
+            bool contrib = false;
+            if (pos <= last) {
+                PairEval e;
+                const SplatRecord &r = ring.rec[buf][s];
+                if (eval_pair(P, a.Pg, a.params, r, &ring.id[buf][s], pxf, pyf, px, py, e, guard)) {
+                    contrib = true;
+                    const float4 q1 = r.q1, q2 = r.q2;
+                    float Ti;
+                    if (first) {
+                        Ti = Tlast;
+                        first = false;
+                    } else {
+                        Ti = Tn * __frcp_rn(1.0f - e.w);  // w <= clamp < 1 here
                     }
-                }
-                if (__any_sync(0xffffffffu, contrib)) {
-                    const float sum = warp_reduce16(v, lane);
-                    if (!(lane & 1) && lane < 28 && sum != 0.f) atomicAdd(a.grad2d + (size_t)id * 16 + (lane >> 1), sum);
+                    Tn = Ti;
+                    const float alpha = e.w * Ti;
+                    v[1] = gc0 * alpha;
+                    v[2] = gc1 * alpha;
+                    v[3] = gc2 * alpha;
+                    v[4] = gd * alpha;
+                    // dL/dw = T_i [ G.(c - S) + gd (z - Sd) + Gn.(n - Sn) ] + ga T_i R
+                    float dLdw = gc0 * (q2.x - S0) + gc1 * (q2.y - S1) + gc2 * (q2.z - S2) + gd * (q2.w - Sd);
+                    const float omw = 1.0f - e.w;
+                    if (kExt) {
+                        const float4 q3 = r.q3;
+                        v[11] = gn0 * alpha;
+                        v[12] = gn1 * alpha;
+                        v[13] = gn2 * alpha;
+                        dLdw += gn0 * (q3.x - Sn0) + gn1 * (q3.y - Sn1) + gn2 * (q3.z - Sn2) + ga * R;
+                        Sn0 = e.w * q3.x + omw * Sn0;
+                        Sn1 = e.w * q3.y + omw * Sn1;
+                        Sn2 = e.w * q3.z + omw * Sn2;
+                        R *= omw;
+                    }
+                    dLdw *= Ti;
+                    if (!e.clamped) {
+                        v[0] = dLdw * e.g;
+                        const float gm = -0.5f * e.w * dLdw;  // dL/dm
+                        const float gu = 2.f * gm * e.u, gv = 2.f * gm * e.v;
+                        v[5] = gu * e.dx;
+                        v[6] = gu * e.dy;
+                        v[7] = gv * e.dx;
+                        v[8] = gv * e.dy;
+                        v[9] = -(gu * q1.x + gv * q1.z);
+                        v[10] = -(gu * q1.y + gv * q1.w);
+                    }
+                    S0 = e.w * q2.x + omw * S0;
+                    S1 = e.w * q2.y + omw * S1;
+                    S2 = e.w * q2.z + omw * S2;
+                    Sd = e.w * q2.w + omw * Sd;
                 }
             }
-            __syncthreads();
+            if (__any_sync(kFull, contrib)) {
+                const float sum = warp_reduce16(v, lane);
+                const uint32_t id = ring.id[buf][s];
+                if (!(lane & 1) && lane < 28 && sum != 0.f) atomicAdd(a.grad2d + (size_t)id * 16 + (lane >> 1), sum);
+            }
         }
-        cp_wait<0>();
+        __syncwarp();  // slot `buf` is refilled by the next ring_fill
+        buf ^= 1;
+        n = nn;
     }
+    cp_wait<0>();
     int gsum = guard;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) gsum += __shfl_xor_sync(kFull, gsum, o);
