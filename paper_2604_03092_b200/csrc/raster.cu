@@ -75,6 +75,12 @@ __device__ __forceinline__ float fast_exp2(float x) {
     return y;
 }
 
+__device__ __forceinline__ float fast_rcp(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 struct Stage {
     SplatRecord rec[2][kRasterThreads];
     uint32_t id[2][kRasterThreads];
@@ -525,7 +531,7 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
                         Ti = Tlast;
                         first = false;
                     } else {
-                        Ti = Tn * __frcp_rn(1.0f - e.w);  // w <= clamp < 1 here
+                        Ti = Tn * fast_rcp(1.0f - e.w);  // w <= clamp < 1 here
                     }
                     Tn = Ti;
                     const float alpha = e.w * Ti;

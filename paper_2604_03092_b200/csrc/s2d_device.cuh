@@ -219,12 +219,15 @@ __device__ __forceinline__ float rect_min_maha(float dx0, float dx1, float dy0, 
                                               float C, float D) {
     if (dx0 <= 0.f && dx1 >= 0.f && dy0 <= 0.f && dy1 >= 0.f) return 0.f;
     const float ac = A * A + C * C, bd = B * B + D * D, x = A * B + C * D;
+    // approximate reciprocals are fine: the edge minimiser only needs to be close (the value
+    // at a nearby t exceeds the minimum by O(dt^2), far inside the 1e-3 culling slack)
+    const float iac = ac > 0.f ? __frcp_rn(ac) : 0.f, ibd = bd > 0.f ? __frcp_rn(bd) : 0.f;
     float best = 3.0e38f;
     // horizontal edges y = dy0, dy1: minimise over d.x in [dx0, dx1]
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
         const float y = e ? dy1 : dy0;
-        const float t = fminf(fmaxf(ac > 0.f ? -x * y / ac : 0.f, dx0), dx1);
+        const float t = fminf(fmaxf(-x * y * iac, dx0), dx1);
         const float u = A * t + B * y, v = C * t + D * y;
         best = fminf(best, u * u + v * v);
     }
@@ -232,7 +235,7 @@ __device__ __forceinline__ float rect_min_maha(float dx0, float dx1, float dy0, 
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
         const float xx = e ? dx1 : dx0;
-        const float t = fminf(fmaxf(bd > 0.f ? -x * xx / bd : 0.f, dy0), dy1);
+        const float t = fminf(fmaxf(-x * xx * ibd, dy0), dy1);
         const float u = A * xx + B * t, v = C * xx + D * t;
         best = fminf(best, u * u + v * v);
     }
