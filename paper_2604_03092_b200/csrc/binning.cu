@@ -292,17 +292,29 @@ __global__ void __launch_bounds__(256) k_scan_emit(const EmitArgs a) {
     for (int j = 0; j < kEmitItems; ++j) {
         if (!(rc[j].x <= rc[j].y && rc[j].z <= rc[j].w)) continue;
         const int tx0 = rc[j].x >> 4, tx1 = rc[j].y >> 4, ty0 = rc[j].z >> 4, ty1 = rc[j].w >> 4;
-        for (int ty = ty0; ty <= ty1; ++ty)
+        for (int ty = ty0; ty <= ty1; ++ty) {
+            // rows of 4-pixel warp blocks the integer bbox overlaps (4 bits -> pairs of mask bits)
+            const int by = ty * kTile;
+            uint32_t rows = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (rc[j].z <= by + 4 * q + 3 && rc[j].w >= by + 4 * q) rows |= 3u << (2 * q);
             for (int tx = tx0; tx <= tx1; ++tx) {
+                const int bx = tx * kTile;
+                const uint32_t cols = (rc[j].x <= bx + 7 && rc[j].y >= bx ? 0x55u : 0u) |
+                                      (rc[j].x <= bx + 15 && rc[j].y >= bx + 8 ? 0xAAu : 0u);
                 const uint32_t t = (uint32_t)(ty * a.ntx + tx);
                 if (off < a.pcap) {
-                    a.pkeys[off] = t;  // bits 16-23 receive the warp-block mask in the forward
+                    // key: tile | bbox-vs-warp-block mask << 16; the forward ORs the ellipse
+                    // mask into bits 24-31 (raster.cu)
+                    a.pkeys[off] = t | ((rows & cols) << 16);
                     a.pvals[off] = ids[j];
                 }
                 ++off;
                 atomicAdd(&s_hist[t & (kRadix - 1)], 1u);
                 if (a.pair_passes > 1) atomicAdd(&s_hist[kRadix + ((t >> kRadixBits) & (kRadix - 1))], 1u);
             }
+        }
     }
     __syncthreads();
     for (int k = tid; k < a.pair_passes * kRadix; k += 256)

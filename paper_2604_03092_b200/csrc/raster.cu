@@ -41,9 +41,6 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p) {
 __device__ __forceinline__ void cp_async16(void *smem, const void *g) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(g) : "memory");
 }
-__device__ __forceinline__ void cp_async8(void *smem, const void *g) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem)), "l"(g) : "memory");
-}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() {
@@ -79,32 +76,6 @@ __device__ __forceinline__ float fast_rcp(float x) {
     float y;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
-}
-
-struct Stage {
-    SplatRecord rec[2][kRasterThreads];
-    uint32_t id[2][kRasterThreads];
-    uint8_t mask[2][kRasterThreads];  // warp blocks the splat's ellipse reaches (k_scan_emit)
-};
-
-// Stage list entry k of a batch: the 64-B record by cp.async, id and cull mask by plain stores
-// (made visible to the other warps by the __syncthreads that precedes their use).
-__device__ __forceinline__ void stage_issue(Stage &st, int buf, int k, uint2 kv, bool valid,
-                                            const SplatRecord *rec) {
-    if (valid) {
-        const float4 *g = reinterpret_cast<const float4 *>(rec + kv.y);
-        float4 *d = reinterpret_cast<float4 *>(&st.rec[buf][k]);
-        cp_async16(d + 0, g + 0);
-        cp_async16(d + 1, g + 1);
-        cp_async16(d + 2, g + 2);
-        cp_async16(d + 3, g + 3);
-    }
-    st.id[buf][k] = kv.y;
-    st.mask[buf][k] = valid ? (uint8_t)(kv.x >> 16) : (uint8_t)0;
-}
-
-__device__ __forceinline__ uint2 load_pair(const RasterArgs &a, int pos, bool valid) {
-    return valid ? make_uint2(a.pair_keys[pos], a.pair_ids[pos]) : make_uint2(0u, 0u);
 }
 
 // Per-pixel evaluation shared by forward and backward (must take identical decisions).
@@ -152,40 +123,99 @@ __device__ __forceinline__ bool eval_pair(const ViewParams &P, const ViewParams 
     return w > 0.0f;
 }
 
-// Ordered list (into s_list) of the staged records whose ellipse reaches this warp's 8x4
-// block (bit `warp` of the per-pair mask built at emission); returns its length.  `limit`
-// excludes list positions > limit (backward).
-__device__ __forceinline__ int warp_cull(const uint8_t *mask, int nrec, int warp, int lane, uint8_t *list,
-                                         int base_pos, int limit) {
+// Warp-private candidate ring.  Each warp streams ITS OWN candidates from the tile's list:
+// list entries are read 32 at a time (key + surfel id), the warp keeps those whose mask bit
+// for its 8x4 block is set, and copies their 64-B records into a 2-deep ring of 32 slots with
+// cp.async.  Warps never wait on each other, so a warp with a short candidate list (or whose
+// pixels all terminated) does not hold the others back at per-batch barriers.
+struct WarpRing {
+    SplatRecord rec[2][32];
+    uint32_t id[2][32];
+    int pos[2][32];
+};
+
+// Cursor over list positions [lo, hi).  The current 32-wide chunk starts at `cb`; lane l
+// holds position cb + l (forward) or cb - 1 - l (backward, cb = chunk end); `pend` = the
+// chunk's hits not yet handed out, `nxt` = the prefetched next chunk (key, id).
+struct ListCursor {
+    int lo, hi, cb;
+    uint32_t pend;
+    uint32_t kid;
+    uint2 nxt;
+};
+
+template <bool kRev>
+__device__ __forceinline__ int chunk_pos(int cb, int lane) {
+    return kRev ? cb - 1 - lane : cb + lane;
+}
+
+template <bool kRev>
+__device__ __forceinline__ uint2 load_chunk(const RasterArgs &a, int cb, const ListCursor &c, int lane) {
+    const int pos = chunk_pos<kRev>(cb, lane);
+    return pos >= c.lo && pos < c.hi ? make_uint2(__ldcg(a.pair_keys + pos), __ldcg(a.pair_ids + pos))
+                                     : make_uint2(0u, 0u);
+}
+
+template <bool kRev>
+__device__ __forceinline__ void cursor_init(ListCursor &c, const RasterArgs &a, int lo, int hi, int lane) {
+    c.lo = lo;
+    c.hi = hi;
+    c.cb = kRev ? hi + 32 : lo - 32;  // virtual chunk outside the range; the first advance lands on it
+    c.pend = 0;
+    c.kid = 0;
+    c.nxt = load_chunk<kRev>(a, kRev ? hi : lo, c, lane);
+}
+
+// Fill ring slot `buf` with up to 32 candidates in traversal order (records by cp.async);
+// `bit` selects the key's mask bit for this warp.  Returns how many.
+template <bool kRev>
+__device__ __forceinline__ int ring_fill(WarpRing &rg, int buf, ListCursor &c, const RasterArgs &a, int bit,
+                                         int lane) {
     const uint32_t lt = lanemask_lt();
-    int cnt = 0;
-#pragma unroll
-    for (int q = 0; q < kRasterThreads / 32; ++q) {
-        const int k = q * 32 + lane;
-        const bool hit = k < nrec && base_pos + k <= limit && ((mask[k] >> warp) & 1u);
-        const uint32_t m = __ballot_sync(kFull, hit);
-        if (hit) list[cnt + __popc(m & lt)] = (uint8_t)k;
-        cnt += __popc(m);
+    int n = 0;
+    while (n < 32) {
+        if (c.pend == 0) {
+            if (kRev ? c.cb - 32 <= c.lo : c.cb + 32 >= c.hi) break;  // no chunk beyond the current one
+            const uint2 cur = c.nxt;
+            c.cb += kRev ? -32 : 32;
+            c.nxt = load_chunk<kRev>(a, c.cb + (kRev ? -32 : 32), c, lane);
+            c.kid = cur.y;
+            const int pos = chunk_pos<kRev>(c.cb, lane);
+            c.pend = __ballot_sync(kFull, pos >= c.lo && pos < c.hi && ((cur.x >> bit) & 1u));
+            continue;
+        }
+        const int take = min(__popc(c.pend), 32 - n);
+        const int rank = __popc(c.pend & lt);
+        const bool mine = ((c.pend >> lane) & 1u) && rank < take;
+        if (mine) {
+            const int s = n + rank;
+            const float4 *g = reinterpret_cast<const float4 *>(a.rec + c.kid);
+            float4 *d = reinterpret_cast<float4 *>(&rg.rec[buf][s]);
+            cp_async16(d + 0, g + 0);
+            cp_async16(d + 1, g + 1);
+            cp_async16(d + 2, g + 2);
+            cp_async16(d + 3, g + 3);
+            rg.id[buf][s] = c.kid;
+            rg.pos[buf][s] = chunk_pos<kRev>(c.cb, lane);
+        }
+        c.pend &= ~__ballot_sync(kFull, mine);
+        n += take;
     }
-    __syncwarp();
-    return cnt;
+    return n;
 }
 
 template <bool kArg, bool kMaxW, bool kNormal>
 __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(const RasterArgs a) {
-    __shared__ Stage st;
-    __shared__ uint8_t s_list[kRasterThreads / 32][kRasterThreads];
+    __shared__ WarpRing s_ring[kRasterThreads / 32];
     const ViewParams &P = a.P;
     const int tile = blockIdx.x;
     const int tx = tile % P.ntx, ty = tile / P.ntx;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int wx0 = tx * kTile + (warp & 1) * 8, wy0 = ty * kTile + (warp >> 1) * 4;
-    const int wx1 = min(wx0 + 7, P.W - 1), wy1 = min(wy0 + 3, P.H - 1);
     const int px = wx0 + (lane & 7), py = wy0 + (lane >> 3);
     const bool inside = px < P.W && py < P.H;
     const float pxf = (float)px, pyf = (float)py;
     const int2 rg = a.ranges[tile];
-    const int cnt = rg.y - rg.x;
 
     float T = 1.0f, Tpre = 1.0f;
     float c0 = 0.f, c1 = 0.f, c2 = 0.f, dep = 0.f, n0 = 0.f, n1 = 0.f, n2 = 0.f;
@@ -193,88 +223,77 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
     int argw = -1, last = -1, guard = 0;
     bool done = !inside;
     const float term_t = P.term_t_f;
-    uint8_t *list = s_list[warp];
+    WarpRing &ring = s_ring[warp];
 
-    const int nb = (cnt + kRasterThreads - 1) / kRasterThreads;
-    if (nb > 0) {
-        uint2 kv_next = load_pair(a, rg.x + tid, tid < cnt);
-        stage_issue(st, 0, tid, kv_next, tid < cnt, a.rec);
+    if (rg.y > rg.x && !__all_sync(kFull, done)) {
+        ListCursor cur;
+        cursor_init<false>(cur, a, rg.x, rg.y, lane);
+        int buf = 0;
+        int n = ring_fill<false>(ring, 0, cur, a, 16 + warp, lane);  // bbox bit (k_scan_emit)
         cp_commit();
-        kv_next = load_pair(a, rg.x + kRasterThreads + tid, kRasterThreads + tid < cnt);
-        for (int b = 0; b < nb; ++b) {
-            const int buf = b & 1;
-            if (b + 1 < nb) {
-                const int k1 = (b + 1) * kRasterThreads + tid;
-                stage_issue(st, buf ^ 1, tid, kv_next, k1 < cnt, a.rec);
-                const int k2 = (b + 2) * kRasterThreads + tid;
-                kv_next = load_pair(a, rg.x + k2, k2 < cnt);
-            }
+        while (n > 0) {
+            const int nn = ring_fill<false>(ring, buf ^ 1, cur, a, 16 + warp, lane);
             cp_commit();
             cp_wait<1>();
-            {   // this thread's record landed: warp-block cull mask (reused by the backward)
-                const int pos = rg.x + b * kRasterThreads + tid;
-                if (b * kRasterThreads + tid < cnt) {
-                    const uint32_t m = warp_block_mask(tx, ty, a.rect[st.id[buf][tid]], st.rec[buf][tid],
-                                                       P.maha_cut_f);
-                    st.mask[buf][tid] = (uint8_t)m;
-                    a.pair_keys[pos] = (a.pair_keys[pos] & 0xffffu) | (m << 16);
-                }
-            }
-            __syncthreads();
-            const int base = b * kRasterThreads;
-            const int nrec = min(kRasterThreads, cnt - base);
-            if (!__all_sync(kFull, done)) {
-                const int nl = warp_cull(st.mask[buf], nrec, warp, lane, list, 0, nrec);
-                for (int j = 0; j < nl; ++j) {
-                    const int k = list[j];
-                    const uint32_t id = st.id[buf][k];
-                    float contrib = 0.f;
-                    if (!done) {
-                        PairEval e;
-                        const SplatRecord &r = st.rec[buf][k];
-                        if (eval_pair(P, a.Pg, a.params, r, &st.id[buf][k], pxf, pyf, px, py, e, guard)) {
-                            contrib = e.w * T;
-                            const float4 q2 = r.q2;
-                            c0 = fmaf(contrib, q2.x, c0);
-                            c1 = fmaf(contrib, q2.y, c1);
-                            c2 = fmaf(contrib, q2.z, c2);
-                            dep = fmaf(contrib, q2.w, dep);
-                            if (kNormal) {
-                                const float4 q3 = r.q3;
-                                n0 = fmaf(contrib, q3.x, n0);
-                                n1 = fmaf(contrib, q3.y, n1);
-                                n2 = fmaf(contrib, q3.z, n2);
-                            }
-                            if (kArg && contrib > maxw) {
-                                maxw = contrib;
-                                argw = (int)id;
-                            }
-                            Tpre = T;
-                            T = T * (1.0f - e.w);
-                            last = rg.x + base + k;
-                            done = T < term_t;
+            __syncwarp();
+            // lane-parallel ellipse cull of the staged candidates; the survivors' bit 24+warp
+            // marks the pair for the backward
+            const bool reach = lane < n && block_reach(wx0, wy0, ring.rec[buf][lane], P.maha_cut_f);
+            uint32_t hm = __ballot_sync(kFull, reach);
+            if (reach) atomicOr(a.pair_keys + ring.pos[buf][lane], 1u << (24 + warp));
+            while (hm) {
+                const int k = __ffs(hm) - 1;
+                hm &= hm - 1;
+                const uint32_t id = ring.id[buf][k];
+                float contrib = 0.f;
+                if (!done) {
+                    PairEval e;
+                    const SplatRecord &r = ring.rec[buf][k];
+                    if (eval_pair(P, a.Pg, a.params, r, &ring.id[buf][k], pxf, pyf, px, py, e, guard)) {
+                        contrib = e.w * T;
+                        const float4 q2 = r.q2;
+                        c0 = fmaf(contrib, q2.x, c0);
+                        c1 = fmaf(contrib, q2.y, c1);
+                        c2 = fmaf(contrib, q2.z, c2);
+                        dep = fmaf(contrib, q2.w, dep);
+                        if (kNormal) {
+                            const float4 q3 = r.q3;
+                            n0 = fmaf(contrib, q3.x, n0);
+                            n1 = fmaf(contrib, q3.y, n1);
+                            n2 = fmaf(contrib, q3.z, n2);
                         }
+                        if (kArg && contrib > maxw) {
+                            maxw = contrib;
+                            argw = (int)id;
+                        }
+                        Tpre = T;
+                        T = T * (1.0f - e.w);
+                        last = ring.pos[buf][k];
+                        done = T < term_t;
                     }
-                    if (kMaxW) {
-                        float mx = contrib;
-                        float mm = (a.mask != nullptr && inside && a.mask[py * P.W + px]) ? contrib : 0.f;
+                }
+                if (kMaxW) {
+                    float mx = contrib;
+                    float mm = (a.mask != nullptr && inside && a.mask[py * P.W + px]) ? contrib : 0.f;
 #pragma unroll
-                        for (int o = 16; o > 0; o >>= 1) {
-                            mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
-                            mm = fmaxf(mm, __shfl_xor_sync(kFull, mm, o));
-                        }
-                        if (lane == 0) {
-                            if (mx > 0.f) atomicMax(reinterpret_cast<int *>(a.max_all + id), __float_as_int(mx));
-                            if (mm > 0.f && a.max_marked)
-                                atomicMax(reinterpret_cast<int *>(a.max_marked + id), __float_as_int(mm));
-                        }
+                    for (int o = 16; o > 0; o >>= 1) {
+                        mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
+                        mm = fmaxf(mm, __shfl_xor_sync(kFull, mm, o));
                     }
-                    if (__all_sync(kFull, done)) break;
+                    if (lane == 0) {
+                        if (mx > 0.f) atomicMax(reinterpret_cast<int *>(a.max_all + id), __float_as_int(mx));
+                        if (mm > 0.f && a.max_marked)
+                            atomicMax(reinterpret_cast<int *>(a.max_marked + id), __float_as_int(mm));
+                    }
                 }
+                if (__all_sync(kFull, done)) break;
             }
-            if (__syncthreads_and(done)) break;
+            if (__all_sync(kFull, done)) break;
+            __syncwarp();  // slot `buf` is refilled by the next ring_fill
+            buf ^= 1;
+            n = nn;
         }
-    cp_wait<0>();
+        cp_wait<0>();
     }
     if (inside) {
         const int p = py * P.W + px;
@@ -296,12 +315,12 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
         }
         a.aux[p] = make_int2(last, __float_as_int(Tpre));
     }
-    const int nm = __syncthreads_count(inside && (1.0f - T) > 0.5f);
+    const int nm = __popc(__ballot_sync(kFull, inside && (1.0f - T) > 0.5f));
     int gsum = guard;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) gsum += __shfl_xor_sync(kFull, gsum, o);
     if (lane == 0 && gsum) atomicAdd(&a.stats->guard_hits, gsum);
-    if (tid == 0 && nm) atomicAdd(&a.stats->n_mask, nm);
+    if (lane == 0 && nm) atomicAdd(&a.stats->n_mask, nm);
 }
 
 // 16 values per lane -> lane l (l even or odd) holds the warp sum of value (l >> 1).
@@ -343,65 +362,6 @@ __device__ __forceinline__ float warp_reduce16(float (&v)[16], int lane) {
 }
 
 __device__ __forceinline__ float sgnf(float x) { return x > 0.f ? 1.f : (x < 0.f ? -1.f : 0.f); }
-
-// Warp-private candidate ring for the backward: each warp streams ITS OWN culled
-// candidates (mask bit 16+warp of the pair key, written by the forward) from the tile
-// list, so warps never wait on each other at per-batch barriers.
-struct WarpRing {
-    SplatRecord rec[2][32];
-    uint32_t id[2][32];
-    int pos[2][32];
-};
-
-// Cursor over list positions [lo, hi) walked downwards in 32-wide chunks; lane l of the
-// current chunk holds position cb - 1 - l, `nxt` holds the chunk below it.  `pend` = hits of the chunk not yet handed out.
-struct RevCursor {
-    int lo, cb;
-    uint32_t pend;
-    uint32_t kid;  // current chunk's surfel id (this lane)
-    uint2 nxt;     // prefetched next chunk (key, id)
-};
-
-__device__ __forceinline__ uint2 load_chunk(const RasterArgs &a, int cb, int lo, int lane) {
-    const int pos = cb - 1 - lane;
-    return pos >= lo ? make_uint2(__ldcg(a.pair_keys + pos), __ldcg(a.pair_ids + pos)) : make_uint2(0u, 0u);
-}
-
-// Fill ring slot `buf` with up to 32 of this warp's candidates in descending list order
-// (cp.async for the records); returns how many.
-__device__ __forceinline__ int ring_fill(WarpRing &rg, int buf, RevCursor &c, const RasterArgs &a, int warp,
-                                         int lane) {
-    const uint32_t lt = lanemask_lt();
-    int n = 0;
-    while (n < 32) {
-        if (c.pend == 0) {
-            if (c.cb - 32 <= c.lo) break;  // no chunk below the current one
-            const uint2 cur = c.nxt;
-            c.cb -= 32;
-            c.nxt = load_chunk(a, c.cb - 32, c.lo, lane);
-            c.kid = cur.y;
-            c.pend = __ballot_sync(kFull, c.cb - 1 - lane >= c.lo && ((cur.x >> (16 + warp)) & 1u));
-            continue;
-        }
-        const int take = min(__popc(c.pend), 32 - n);
-        const int rank = __popc(c.pend & lt);
-        const bool mine = ((c.pend >> lane) & 1u) && rank < take;
-        if (mine) {
-            const int s = n + rank;
-            const float4 *g = reinterpret_cast<const float4 *>(a.rec + c.kid);
-            float4 *d = reinterpret_cast<float4 *>(&rg.rec[buf][s]);
-            cp_async16(d + 0, g + 0);
-            cp_async16(d + 1, g + 1);
-            cp_async16(d + 2, g + 2);
-            cp_async16(d + 3, g + 3);
-            rg.id[buf][s] = c.kid;
-            rg.pos[buf][s] = c.cb - 1 - lane;
-        }
-        c.pend &= ~__ballot_sync(kFull, mine);
-        n += take;
-    }
-    return n;
-}
 
 template <bool kExt>  // kExt: normal / accumulation seeds present (external loss)
 __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(const RasterArgs a) {
@@ -500,17 +460,13 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
     float S0 = 0.f, S1 = 0.f, S2 = 0.f, Sd = 0.f, Sn0 = 0.f, Sn1 = 0.f, Sn2 = 0.f;
     int guard = 0;
     WarpRing &ring = s_ring[warp];
-    RevCursor cur;
-    cur.lo = rg.x;
-    cur.cb = wlast + 1 + 32;  // virtual chunk above the range; the first advance lands on wlast
-    cur.pend = 0;
-    cur.kid = 0;
-    cur.nxt = load_chunk(a, wlast + 1, cur.lo, lane);
+    ListCursor cur;
+    cursor_init<true>(cur, a, rg.x, wlast + 1, lane);
     int buf = 0;
-    int n = ring_fill(ring, 0, cur, a, warp, lane);
+    int n = ring_fill<true>(ring, 0, cur, a, 24 + warp, lane);  // ellipse bit (forward)
     cp_commit();
     while (n > 0) {
-        const int nn = ring_fill(ring, buf ^ 1, cur, a, warp, lane);
+        const int nn = ring_fill<true>(ring, buf ^ 1, cur, a, 24 + warp, lane);
         cp_commit();
         cp_wait<1>();
         __syncwarp();

@@ -242,27 +242,17 @@ __device__ __forceinline__ float rect_min_maha(float dx0, float dx1, float dy0, 
     return best;
 }
 
-// 8-bit mask of the warp blocks (8x4 pixels; warp w at (w & 1) * 8, (w >> 1) * 4 in the 16x16
-// tile) that the splat can blend into: the block must overlap the integer bbox and come within
-// the 3-sigma ellipse (padded by twice the guard band, so the culling is conservative with
-// respect to the reference's float64 decision).
-__device__ __forceinline__ uint32_t warp_block_mask(int tx, int ty, short4 rc, const SplatRecord &r, float cut) {
+// Whether the splat's 3-sigma ellipse can reach the 8x4 warp block with top-left pixel
+// (bx0, by0): the continuous minimum of m over the block's pixel-centre rectangle against the
+// cut padded by twice the guard band (+1e-3), so the cull is conservative with respect to the
+// reference's float64 decision (the pixel test itself re-checks m exactly).
+__device__ __forceinline__ bool block_reach(int bx0, int by0, const SplatRecord &r, float cut) {
     const uint32_t lob = __float_as_uint(r.q0.z);
     const __half2 lo = *reinterpret_cast<const __half2 *>(&lob);
     const float cx = r.q0.x + __low2float(lo), cy = r.q0.y + __high2float(lo);
     const float thr = cut + 2.f * r.q3.w + 1e-3f;
-    uint32_t m = 0;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) {
-        const int bx0 = tx * kTile + (w & 1) * 8, by0 = ty * kTile + (w >> 1) * 4;
-        const int xa = max(bx0, (int)rc.x), xb = min(bx0 + 7, (int)rc.y);
-        const int ya = max(by0, (int)rc.z), yb = min(by0 + 3, (int)rc.w);
-        if (xa > xb || ya > yb) continue;
-        if (rect_min_maha((float)xa - cx, (float)xb - cx, (float)ya - cy, (float)yb - cy, r.q1.x, r.q1.y, r.q1.z,
-                          r.q1.w) <= thr)
-            m |= 1u << w;
-    }
-    return m;
+    return rect_min_maha((float)bx0 - cx, (float)(bx0 + 7) - cx, (float)by0 - cy, (float)(by0 + 3) - cy, r.q1.x,
+                         r.q1.y, r.q1.z, r.q1.w) <= thr;
 }
 
 // ---------------------------------------------------------- small utilities

@@ -88,7 +88,7 @@ struct RasterArgs {
     const float *params;
     const int2 *ranges;
     const uint32_t *pair_ids;
-    uint32_t *pair_keys;  // tile id | warp-block mask << 16 (mask written by the forward)
+    uint32_t *pair_keys;  // tile | bbox warp-block mask << 16 | ellipse warp-block mask << 24 (forward)
     const SplatRecord *rec;
     const short4 *rect;
     int2 *aux;  // per pixel (last list position, float bits of T before it)
