@@ -182,13 +182,15 @@ struct s2d_view {
     // capacities (elements)
     int64_t cap_rec = 0, cap_rect = 0, cap_z = 0, cap_flags = 0, cap_keys[2] = {0, 0},
             cap_vals[2] = {0, 0}, cap_grad = 0, cap_aux = 0, cap_pk[2] = {0, 0}, cap_pv[2] = {0, 0},
-            cap_sync = 0;
+            cap_bs = 0, cap_bc = 0, cap_sync = 0;
     SplatRecord *rec = nullptr;
     short4 *rect = nullptr;
     double *z64 = nullptr;
     uint8_t *flags = nullptr;
     uint32_t *keys[2] = {nullptr, nullptr}, *vals[2] = {nullptr, nullptr};
     uint32_t *pkeys[2] = {nullptr, nullptr}, *pvals[2] = {nullptr, nullptr};
+    uint2 *bstream = nullptr;  // [8 pcap] per-warp (surfel, lane mask) streams of blended pairs
+    int *bcount = nullptr;     // [ntiles * 8] stream lengths
     float *grad2d = nullptr;
     int2 *aux = nullptr;
     uint8_t *sync = nullptr;
@@ -287,6 +289,8 @@ int ensure_capacity(s2d_view *v, int64_t n, int64_t npx, int ntiles) {
         if ((rc = grow(v->pkeys[b], v->cap_pk[b], v->pcap))) return rc;
         if ((rc = grow(v->pvals[b], v->cap_pv[b], v->pcap))) return rc;
     }
+    if ((rc = grow(v->bstream, v->cap_bs, 8 * v->pcap))) return rc;
+    if ((rc = grow(v->bcount, v->cap_bc, 8 * (int64_t)ntiles))) return rc;
     return layout_sync(v, nn, v->pcap, ntiles);
 }
 
@@ -390,6 +394,8 @@ int view_forward(s2d_view *v, cudaStream_t s, const float *params, int64_t n, co
     ra.ranges = sr.ranges;
     ra.pair_ids = v->pvals[v->pair_buf];
     ra.pair_keys = v->pkeys[v->pair_buf];
+    ra.bstream = v->bstream;
+    ra.bcount = v->bcount;
     ra.rec = v->rec;
     ra.rect = v->rect;
     ra.aux = v->aux;
@@ -450,7 +456,7 @@ int s2d_view_create(s2d_ctx *ctx, s2d_view **out) {
 int s2d_view_destroy(s2d_view *v) {
     if (!v) return S2D_OK;
     void *ptrs[] = {v->rec, v->rect, v->z64, v->flags, v->keys[0], v->keys[1], v->vals[0], v->vals[1],
-                    v->pkeys[0], v->pkeys[1], v->pvals[0], v->pvals[1], v->grad2d, v->aux, v->sync,
+                    v->pkeys[0], v->pkeys[1], v->pvals[0], v->pvals[1], v->bstream, v->bcount, v->grad2d, v->aux, v->sync,
                     v->h_params_dev, v->h_img_dev};
     for (void *p : ptrs)
         if (p) cudaFree(p);
@@ -575,6 +581,8 @@ int s2d_backward(s2d_view *v, void *stream, const float *params, int64_t n, cons
     ra.ranges = v->sr.ranges;
     ra.pair_ids = v->pvals[v->pair_buf];
     ra.pair_keys = v->pkeys[v->pair_buf];
+    ra.bstream = v->bstream;
+    ra.bcount = v->bcount;
     ra.rec = v->rec;
     ra.rect = v->rect;
     ra.aux = v->aux;

@@ -1,7 +1,7 @@
 // optim.cu — projection backward (N2) and the fused Adam step (N4).
 //
 // k_project_bwd: per on-screen surfel, chains the per-view 2D gradients
-//   [dL/d opacity, dL/d rgb(3), dL/dz, dL/d Minv(4), dL/d centre(2), dL/d normal(3)]
+//   [dL/d opacity, dL/d rgb(3), dL/dz, K = sum dL/dm w w^T (3), e = sum dL/dm w (2), dL/d normal(3)]
 // through Minv = (J(p) Bc)^-1, centre(p), z, normal = R_cw R(q)[:,2] back to
 // the parameters (means, raw quats, scales, opacity, colours), in float64, and
 // ACCUMULATES into the packed gradient block with atomic reductions (views sum with no
@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(128) k_project_bwd(const ProjectBwdArgs a) {
     const int64_t n = P.n;
     const float4 *__restrict__ g4 = reinterpret_cast<const float4 *>(a.grad2d + (size_t)i * 16);
     const float4 G0 = g4[0], G1 = g4[1], G2 = g4[2];
-    const float G3x = a.grad2d[(size_t)i * 16 + 12], G3y = a.grad2d[(size_t)i * 16 + 13];
+    const float G3 = a.grad2d[(size_t)i * 16 + 12];
     float *gmeans = a.grads, *gquats = a.grads + 3 * n;
     float *gscales = a.grads + 7 * n, *gopac = a.grads + 9 * n;
     float *gcol = a.grads + 10 * n;
@@ -92,8 +92,18 @@ __global__ void __launch_bounds__(128) k_project_bwd(const ProjectBwdArgs a) {
     const double M11 = e.J[1][1] * e.Bc[1][1] + e.J[1][2] * e.Bc[2][1];
     const double id = 1.0 / (M00 * M11 - M01 * M10);
     const double N[2][2] = {{M11 * id, -M01 * id}, {-M10 * id, M00 * id}};
-    // 2D gradient record: [opacity, rgb(3), z, Minv A,B,C,D, centre x,y, normal(3), -, -]
-    const double GN[2][2] = {{G1.y, G1.z}, {G1.w, G2.x}};
+    // 2D gradient record (k_raster_bwd): [opacity, rgb(3), z, K(uu, uv, vv), e(u, v), normal(3)]
+    // with K = sum dL/dm w w^T and e = sum dL/dm w over the pixels, w = N d the whitened
+    // offset (d = pixel - centre, m = |w|^2):   dL/dN = 2 K M^T,   dL/dcentre = -2 N^T e
+    const double K[2][2] = {{G1.y, G1.z}, {G1.z, G1.w}};
+    const double Mm[2][2] = {{M00, M01}, {M10, M11}};
+    double GN[2][2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) GN[r][c] = 2.0 * (K[r][0] * Mm[c][0] + K[r][1] * Mm[c][1]);
+    const double gcx = -2.0 * (N[0][0] * G2.x + N[1][0] * G2.y);
+    const double gcy = -2.0 * (N[0][1] * G2.x + N[1][1] * G2.y);
     // dL/dM = -N^T GN N^T
     double T[2][2], GM[2][2];
 #pragma unroll
@@ -138,7 +148,7 @@ __global__ void __launch_bounds__(128) k_project_bwd(const ProjectBwdArgs a) {
         for (int k = 0; k < 3; ++k)
             nn[k] = P.r_cw[3 * k] * e.R[2] + P.r_cw[3 * k + 1] * e.R[5] + P.r_cw[3 * k + 2] * e.R[8];
         const double sg = (nn[0] * e.p[0] + nn[1] * e.p[1] + nn[2] * e.p[2]) > 0.0 ? -1.0 : 1.0;
-        const double gn[3] = {G2.w, G3x, G3y};
+        const double gn[3] = {G2.z, G2.w, G3};
 #pragma unroll
         for (int b = 0; b < 3; ++b)
             gR[3 * b + 2] = sg * (P.r_cw[b] * gn[0] + P.r_cw[3 + b] * gn[1] + P.r_cw[6 + b] * gn[2]);
@@ -156,10 +166,10 @@ __global__ void __launch_bounds__(128) k_project_bwd(const ProjectBwdArgs a) {
     gp2 += gJ[0][0] * (-fx * iz2) + gJ[0][2] * (2.0 * fx * x * iz3);
     gp1 += gJ[1][2] * (-fy * iz2);
     gp2 += gJ[1][1] * (-fy * iz2) + gJ[1][2] * (2.0 * fy * y * iz3);
-    gp0 += (double)G2.y * (fx * iz);
-    gp2 += (double)G2.y * (-fx * x * iz2);
-    gp1 += (double)G2.z * (fy * iz);
-    gp2 += (double)G2.z * (-fy * y * iz2);
+    gp0 += gcx * (fx * iz);
+    gp2 += gcx * (-fx * x * iz2);
+    gp1 += gcy * (fy * iz);
+    gp2 += gcy * (-fy * y * iz2);
     // p = s_inv R(q_inv) mu + t_inv.  Accumulation is atomic (fire-and-forget reductions), so
     // views running concurrently on different streams may share one gradient block.
 #pragma unroll

@@ -123,20 +123,20 @@ __device__ __forceinline__ bool eval_pair(const ViewParams &P, const ViewParams 
     return w > 0.0f;
 }
 
-// Warp-private candidate ring.  Each warp streams ITS OWN candidates from the tile's list:
-// list entries are read 32 at a time (key + surfel id), the warp keeps those whose mask bit
-// for its 8x4 block is set, and copies their 64-B records into a 2-deep ring of 32 slots with
-// cp.async.  Warps never wait on each other, so a warp with a short candidate list (or whose
-// pixels all terminated) does not hold the others back at per-batch barriers.
+// Warp-private candidate ring (forward).  Each warp streams ITS OWN candidates from the tile's
+// list: list entries are read 32 at a time (key + surfel id), the warp keeps those whose bbox
+// bit for its 8x4 block is set, and copies their 64-B records into a 2-deep ring of 32 slots
+// with cp.async.  Warps never wait on each other, so a warp with a short candidate list (or
+// whose pixels all terminated) does not hold the others back at per-batch barriers.
 struct WarpRing {
     SplatRecord rec[2][32];
     uint32_t id[2][32];
-    int pos[2][32];
+    uint32_t aux[2][32];  // forward: list position; backward: lane mask
 };
 
-// Cursor over list positions [lo, hi).  The current 32-wide chunk starts at `cb`; lane l
-// holds position cb + l (forward) or cb - 1 - l (backward, cb = chunk end); `pend` = the
-// chunk's hits not yet handed out, `nxt` = the prefetched next chunk (key, id).
+// Cursor over list positions [lo, hi).  The current 32-wide chunk starts at `cb` (lane l holds
+// position cb + l); `pend` = the chunk's hits not yet handed out, `nxt` = the prefetched next
+// chunk (key, id).
 struct ListCursor {
     int lo, hi, cb;
     uint32_t pend;
@@ -144,44 +144,36 @@ struct ListCursor {
     uint2 nxt;
 };
 
-template <bool kRev>
-__device__ __forceinline__ int chunk_pos(int cb, int lane) {
-    return kRev ? cb - 1 - lane : cb + lane;
-}
-
-template <bool kRev>
 __device__ __forceinline__ uint2 load_chunk(const RasterArgs &a, int cb, const ListCursor &c, int lane) {
-    const int pos = chunk_pos<kRev>(cb, lane);
+    const int pos = cb + lane;
     return pos >= c.lo && pos < c.hi ? make_uint2(__ldcg(a.pair_keys + pos), __ldcg(a.pair_ids + pos))
                                      : make_uint2(0u, 0u);
 }
 
-template <bool kRev>
 __device__ __forceinline__ void cursor_init(ListCursor &c, const RasterArgs &a, int lo, int hi, int lane) {
     c.lo = lo;
     c.hi = hi;
-    c.cb = kRev ? hi + 32 : lo - 32;  // virtual chunk outside the range; the first advance lands on it
+    c.cb = lo - 32;  // virtual chunk before the range; the first advance lands on lo
     c.pend = 0;
     c.kid = 0;
-    c.nxt = load_chunk<kRev>(a, kRev ? hi : lo, c, lane);
+    c.nxt = load_chunk(a, lo, c, lane);
 }
 
-// Fill ring slot `buf` with up to 32 candidates in traversal order (records by cp.async);
-// `bit` selects the key's mask bit for this warp.  Returns how many.
-template <bool kRev>
-__device__ __forceinline__ int ring_fill(WarpRing &rg, int buf, ListCursor &c, const RasterArgs &a, int bit,
+// Fill ring slot `buf` with up to 32 candidates in list order (records by cp.async): the
+// entries whose bbox bit for this warp's block is set.  Returns how many.
+__device__ __forceinline__ int ring_fill(WarpRing &rg, int buf, ListCursor &c, const RasterArgs &a, int warp,
                                          int lane) {
     const uint32_t lt = lanemask_lt();
     int n = 0;
     while (n < 32) {
         if (c.pend == 0) {
-            if (kRev ? c.cb - 32 <= c.lo : c.cb + 32 >= c.hi) break;  // no chunk beyond the current one
+            if (c.cb + 32 >= c.hi) break;  // no chunk beyond the current one
             const uint2 cur = c.nxt;
-            c.cb += kRev ? -32 : 32;
-            c.nxt = load_chunk<kRev>(a, c.cb + (kRev ? -32 : 32), c, lane);
+            c.cb += 32;
+            c.nxt = load_chunk(a, c.cb + 32, c, lane);
             c.kid = cur.y;
-            const int pos = chunk_pos<kRev>(c.cb, lane);
-            c.pend = __ballot_sync(kFull, pos >= c.lo && pos < c.hi && ((cur.x >> bit) & 1u));
+            const int pos = c.cb + lane;
+            c.pend = __ballot_sync(kFull, pos < c.hi && ((cur.x >> (16 + warp)) & 1u));
             continue;
         }
         const int take = min(__popc(c.pend), 32 - n);
@@ -196,10 +188,29 @@ __device__ __forceinline__ int ring_fill(WarpRing &rg, int buf, ListCursor &c, c
             cp_async16(d + 2, g + 2);
             cp_async16(d + 3, g + 3);
             rg.id[buf][s] = c.kid;
-            rg.pos[buf][s] = chunk_pos<kRev>(c.cb, lane);
+            rg.aux[buf][s] = (uint32_t)(c.cb + lane);
         }
         c.pend &= ~__ballot_sync(kFull, mine);
         n += take;
+    }
+    return n;
+}
+
+// Backward ring fill: entries [e0, e1) of the warp's blend stream, newest first (slot s holds
+// entry e1 - 1 - s).  Every entry is work, so this is one coalesced 8-B load per lane.
+__device__ __forceinline__ int stream_fill(WarpRing &rg, int buf, const uint2 *ws, int e0, int e1,
+                                           const SplatRecord *rec, int lane) {
+    const int n = min(32, e1 - e0);
+    if (lane < n) {
+        const uint2 en = __ldcg(ws + (e1 - 1 - lane));
+        const float4 *g = reinterpret_cast<const float4 *>(rec + en.x);
+        float4 *d = reinterpret_cast<float4 *>(&rg.rec[buf][lane]);
+        cp_async16(d + 0, g + 0);
+        cp_async16(d + 1, g + 1);
+        cp_async16(d + 2, g + 2);
+        cp_async16(d + 3, g + 3);
+        rg.id[buf][lane] = en.x;
+        rg.aux[buf][lane] = en.y;
     }
     return n;
 }
@@ -225,31 +236,36 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
     const float term_t = P.term_t_f;
     WarpRing &ring = s_ring[warp];
 
+    // this warp's blend stream (one entry per pair its pixels blended, for the backward);
+    // entries are gathered in registers, lane (count % 32) holding the newest, and written
+    // 32 at a time
+    uint2 *ws = a.bstream + 8 * (size_t)rg.x + (size_t)warp * (size_t)max(rg.y - rg.x, 0);
+    int wc = 0;
+    uint2 went = make_uint2(0u, 0u);
     if (rg.y > rg.x && !__all_sync(kFull, done)) {
         ListCursor cur;
-        cursor_init<false>(cur, a, rg.x, rg.y, lane);
+        cursor_init(cur, a, rg.x, rg.y, lane);
         int buf = 0;
-        int n = ring_fill<false>(ring, 0, cur, a, 16 + warp, lane);  // bbox bit (k_scan_emit)
+        int n = ring_fill(ring, 0, cur, a, warp, lane);  // bbox bit (k_scan_emit)
         cp_commit();
         while (n > 0) {
-            const int nn = ring_fill<false>(ring, buf ^ 1, cur, a, 16 + warp, lane);
+            const int nn = ring_fill(ring, buf ^ 1, cur, a, warp, lane);
             cp_commit();
             cp_wait<1>();
             __syncwarp();
-            // lane-parallel ellipse cull of the staged candidates; the survivors' bit 24+warp
-            // marks the pair for the backward
-            const bool reach = lane < n && block_reach(wx0, wy0, ring.rec[buf][lane], P.maha_cut_f);
-            uint32_t hm = __ballot_sync(kFull, reach);
-            if (reach) atomicOr(a.pair_keys + ring.pos[buf][lane], 1u << (24 + warp));
+            // lane-parallel ellipse cull of the staged candidates
+            uint32_t hm = __ballot_sync(kFull, lane < n && block_reach(wx0, wy0, ring.rec[buf][lane], P.maha_cut_f));
             while (hm) {
                 const int k = __ffs(hm) - 1;
                 hm &= hm - 1;
                 const uint32_t id = ring.id[buf][k];
                 float contrib = 0.f;
+                bool blended = false;
                 if (!done) {
                     PairEval e;
                     const SplatRecord &r = ring.rec[buf][k];
                     if (eval_pair(P, a.Pg, a.params, r, &ring.id[buf][k], pxf, pyf, px, py, e, guard)) {
+                        blended = true;
                         contrib = e.w * T;
                         const float4 q2 = r.q2;
                         c0 = fmaf(contrib, q2.x, c0);
@@ -268,9 +284,16 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
                         }
                         Tpre = T;
                         T = T * (1.0f - e.w);
-                        last = ring.pos[buf][k];
+                        last = (int)ring.aux[buf][k];
                         done = T < term_t;
                     }
+                }
+                // the exact set of this block's pixels that blended the pair
+                const uint32_t bm = __ballot_sync(kFull, blended);
+                if (bm) {
+                    if (lane == (wc & 31)) went = make_uint2(id, bm);
+                    if ((wc & 31) == 31) ws[wc - 31 + lane] = went;
+                    ++wc;
                 }
                 if (kMaxW) {
                     float mx = contrib;
@@ -295,6 +318,8 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
         }
         cp_wait<0>();
     }
+    if (lane < (wc & 31)) ws[(wc & ~31) + lane] = went;
+    if (lane == 0) a.bcount[8 * tile + warp] = wc;
     if (inside) {
         const int p = py * P.W + px;
         if (a.color) {
@@ -323,42 +348,65 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
     if (lane == 0 && nm) atomicAdd(&a.stats->n_mask, nm);
 }
 
-// 16 values per lane -> lane l (l even or odd) holds the warp sum of value (l >> 1).
-__device__ __forceinline__ float warp_reduce16(float (&v)[16], int lane) {
-    {
-        const bool up = lane & 16;
+// Transposed warp reduction of C per-lane values (C <= 16): at each butterfly stage the
+// lanes exchange half of their values, so the whole reduction costs about C shuffles
+// instead of 5 C.  Afterwards every lane's v[0] is the warp sum of one value; red_map
+// (run once per kernel) says which value (vi) and whether this lane owns it (each value
+// is owned by exactly one lane).
+template <int C, int O>
+__device__ __forceinline__ void red_stage(float (&v)[16], int lane) {
+    constexpr int H = (C + 1) / 2, F = C / 2;
+    const bool up = lane & O;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const float send = up ? v[j] : v[j + 8];
-            const float keep = up ? v[j + 8] : v[j];
-            v[j] = keep + __shfl_xor_sync(kFull, send, 16);
-        }
+    for (int j = 0; j < F; ++j) {
+        const float send = up ? v[j] : v[j + H];
+        const float keep = up ? v[j + H] : v[j];
+        v[j] = keep + __shfl_xor_sync(kFull, send, O);
     }
-    {
-        const bool up = lane & 8;
+    if constexpr (H > F) v[F] += __shfl_xor_sync(kFull, v[F], O);
+    if constexpr (O > 1) red_stage<H, O / 2>(v, lane);
+}
+
+template <int C, int O>
+__device__ __forceinline__ void map_stage(int (&ix)[16], bool (&own)[16], int lane) {
+    constexpr int H = (C + 1) / 2, F = C / 2;
+    const bool up = lane & O;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const float send = up ? v[j] : v[j + 4];
-            const float keep = up ? v[j + 4] : v[j];
-            v[j] = keep + __shfl_xor_sync(kFull, send, 8);
-        }
+    for (int j = 0; j < F; ++j) {
+        const bool send = up ? own[j] : own[j + H];
+        const bool psend = __shfl_xor_sync(kFull, (int)send, O) != 0;
+        ix[j] = up ? ix[j + H] : ix[j];
+        own[j] = (up ? own[j + H] : own[j]) && psend;
     }
-    {
-        const bool up = lane & 4;
+    if constexpr (H > F) {
+        const bool pown = __shfl_xor_sync(kFull, (int)own[F], O) != 0;  // every lane shuffles
+        own[F] = own[F] && pown && !up;
+    }
+    if constexpr (O > 1) map_stage<H, O / 2>(ix, own, lane);
+}
+
+template <int C>
+__device__ __forceinline__ void red_map(int lane, int &vi, bool &own) {
+    int ix[16];
+    bool ow[16];
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            const float send = up ? v[j] : v[j + 2];
-            const float keep = up ? v[j + 2] : v[j];
-            v[j] = keep + __shfl_xor_sync(kFull, send, 4);
-        }
+    for (int j = 0; j < 16; ++j) {
+        ix[j] = j;
+        ow[j] = true;
     }
-    {
-        const bool up = lane & 2;
-        const float send = up ? v[0] : v[1];
-        const float keep = up ? v[1] : v[0];
-        v[0] = keep + __shfl_xor_sync(kFull, send, 2);
-    }
-    return v[0] + __shfl_xor_sync(kFull, v[0], 1);
+    map_stage<C, 16>(ix, ow, lane);
+    vi = ix[0];
+    own = ow[0];
+}
+
+// Rare path of the backward: the weight-clamp decision for a pair whose opacity is within
+// 8e-6 of the clamp, taken exactly as eval_pair takes it in the forward.
+__device__ __noinline__ bool clamp_decision(const ViewParams *__restrict__ Pg, const float *params, uint32_t id,
+                                            float m, float w, float gb, int x, int y) {
+    const ViewParams &P = *Pg;
+    const bool band = m >= P.maha_cut_f - gb || fabsf(w - P.w_clamp_f) <= 4e-6f;
+    if (!band) return w > P.w_clamp_f;
+    return (guard_resolve(Pg, params, id, x, y) & 2) != 0;
 }
 
 __device__ __forceinline__ float sgnf(float x) { return x > 0.f ? 1.f : (x < 0.f ? -1.f : 0.f); }
@@ -381,11 +429,9 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
     // ---- loss seeds (rasterizer.py:375-380 for MSE; L1; external) ----
     float gc0 = 0.f, gc1 = 0.f, gc2 = 0.f, gd = 0.f, gn0 = 0.f, gn1 = 0.f, gn2 = 0.f, ga = 0.f;
     float lpx = 0.f;
-    int last = -1;
     float Tlast = 1.f;
     if (inside) {
         const int2 ax = a.aux[p];
-        last = ax.x;
         Tlast = __int_as_float(ax.y);
         const double npx = (double)P.W * (double)P.H;
         if (a.loss_kind == S2D_LOSS_EXTERNAL) {
@@ -434,15 +480,11 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
             }
         }
     }
-    // loss: block reduction (the kernel's only barrier); last blended position: warp max
-    int wlast = last;
+    // loss: block reduction (the kernel's only barrier)
     {
         float l = lpx;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            l += __shfl_xor_sync(kFull, l, o);
-            wlast = max(wlast, __shfl_xor_sync(kFull, wlast, o));
-        }
+        for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(kFull, l, o);
         if (lane == 0) s_loss[warp] = l;
     }
     __syncthreads();
@@ -451,97 +493,103 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
         for (int w = 0; w < 8; ++w) l += s_loss[w];
         if (l != 0.f) atomicAdd(a.loss_accum, (double)l);
     }
-    if (wlast < rg.x) return;  // nothing blended in this warp's block (warp-uniform)
+    const int cnt = a.bcount[8 * tile + warp];
+    if (cnt == 0) return;  // no pixel of this warp's block blended anything (warp-uniform)
 
-    // ---- reverse traversal of this warp's candidates ----
-    float Tn = Tlast;          // transmittance before the later contributor
+    // ---- reverse traversal of the pairs this warp's pixels blended ----
+    // Per pair, only the lanes in the forward's lane mask work (no cut / guard-band tests);
+    // their 2D gradients are warp-reduced (NV values) and added with one atomic per value:
+    //   [0] dL/d opacity, [1..3] dL/d rgb, [4] dL/dz,
+    //   [5..7] K = sum dL/dm w w^T (uu, uv, vv), [8..9] e = sum dL/dm w, [10..12] dL/d normal
+    // with w = (u, v) = Minv d the whitened pixel offset (dL/dMinv = 2 K M^T and
+    // dL/dcentre = -2 Minv^T e are formed in k_project_bwd).
+    constexpr int NV = kExt ? 13 : 10;
+    int vi;
+    bool own;
+    red_map<NV>(lane, vi, own);
+    float Tn = Tlast;  // transmittance before the later contributor
     bool first = true;
-    float R = 1.f;             // prod_{j later} (1 - w_j)
+    float R = 1.f;     // prod_{j later} (1 - w_j)
     float S0 = 0.f, S1 = 0.f, S2 = 0.f, Sd = 0.f, Sn0 = 0.f, Sn1 = 0.f, Sn2 = 0.f;
-    int guard = 0;
     WarpRing &ring = s_ring[warp];
-    ListCursor cur;
-    cursor_init<true>(cur, a, rg.x, wlast + 1, lane);
+    const uint2 *ws = a.bstream + 8 * (size_t)rg.x + (size_t)warp * (size_t)(rg.y - rg.x);
+    int e1 = cnt;
     int buf = 0;
-    int n = ring_fill<true>(ring, 0, cur, a, 24 + warp, lane);  // ellipse bit (forward)
+    int n = stream_fill(ring, 0, ws, max(e1 - 32, 0), e1, a.rec, lane);
+    e1 -= n;
     cp_commit();
     while (n > 0) {
-        const int nn = ring_fill<true>(ring, buf ^ 1, cur, a, 24 + warp, lane);
+        const int nn = stream_fill(ring, buf ^ 1, ws, max(e1 - 32, 0), e1, a.rec, lane);
+        e1 -= nn;
         cp_commit();
         cp_wait<1>();
         __syncwarp();
         for (int s = 0; s < n; ++s) {
-            const int pos = ring.pos[buf][s];
             float v[16];
 #pragma unroll
             for (int t = 0; t < 16; ++t) v[t] = 0.f;
-            bool contrib = false;
-            if (pos <= last) {
-                PairEval e;
+            if ((ring.aux[buf][s] >> lane) & 1u) {
+                // the forward's arithmetic (eval_pair), minus the decisions it already took
                 const SplatRecord &r = ring.rec[buf][s];
-                if (eval_pair(P, a.Pg, a.params, r, &ring.id[buf][s], pxf, pyf, px, py, e, guard)) {
-                    contrib = true;
-                    const float4 q1 = r.q1, q2 = r.q2;
-                    float Ti;
-                    if (first) {
-                        Ti = Tlast;
-                        first = false;
-                    } else {
-                        Ti = Tn * fast_rcp(1.0f - e.w);  // w <= clamp < 1 here
-                    }
-                    Tn = Ti;
-                    const float alpha = e.w * Ti;
-                    v[1] = gc0 * alpha;
-                    v[2] = gc1 * alpha;
-                    v[3] = gc2 * alpha;
-                    v[4] = gd * alpha;
-                    // dL/dw = T_i [ G.(c - S) + gd (z - Sd) + Gn.(n - Sn) ] + ga T_i R
-                    float dLdw = gc0 * (q2.x - S0) + gc1 * (q2.y - S1) + gc2 * (q2.z - S2) + gd * (q2.w - Sd);
-                    const float omw = 1.0f - e.w;
-                    if (kExt) {
-                        const float4 q3 = r.q3;
-                        v[11] = gn0 * alpha;
-                        v[12] = gn1 * alpha;
-                        v[13] = gn2 * alpha;
-                        dLdw += gn0 * (q3.x - Sn0) + gn1 * (q3.y - Sn1) + gn2 * (q3.z - Sn2) + ga * R;
-                        Sn0 = e.w * q3.x + omw * Sn0;
-                        Sn1 = e.w * q3.y + omw * Sn1;
-                        Sn2 = e.w * q3.z + omw * Sn2;
-                        R *= omw;
-                    }
-                    dLdw *= Ti;
-                    if (!e.clamped) {
-                        v[0] = dLdw * e.g;
-                        const float gm = -0.5f * e.w * dLdw;  // dL/dm
-                        const float gu = 2.f * gm * e.u, gv = 2.f * gm * e.v;
-                        v[5] = gu * e.dx;
-                        v[6] = gu * e.dy;
-                        v[7] = gv * e.dx;
-                        v[8] = gv * e.dy;
-                        v[9] = -(gu * q1.x + gv * q1.z);
-                        v[10] = -(gu * q1.y + gv * q1.w);
-                    }
-                    S0 = e.w * q2.x + omw * S0;
-                    S1 = e.w * q2.y + omw * S1;
-                    S2 = e.w * q2.z + omw * S2;
-                    Sd = e.w * q2.w + omw * Sd;
+                const float4 q0 = r.q0, q1 = r.q1, q2 = r.q2;
+                const uint32_t lob = __float_as_uint(q0.z);
+                const __half2 lo = *reinterpret_cast<const __half2 *>(&lob);
+                const float dx = __fsub_rn(__fsub_rn(pxf, q0.x), __low2float(lo));
+                const float dy = __fsub_rn(__fsub_rn(pyf, q0.y), __high2float(lo));
+                const float u = __fmaf_rn(q1.x, dx, __fmul_rn(q1.y, dy));
+                const float vv = __fmaf_rn(q1.z, dx, __fmul_rn(q1.w, dy));
+                const float m = __fmaf_rn(u, u, __fmul_rn(vv, vv));
+                const float g = fast_exp2(__fmul_rn(m, -0.72134752044448170368f));
+                float w = __fmul_rn(q0.w, g);
+                bool clamped = false;
+                if (q0.w > P.w_clamp_f - 8e-6f)
+                    clamped = clamp_decision(a.Pg, a.params, ring.id[buf][s], m, w, r.q3.w, px, py);
+                if (clamped) w = P.w_clamp_f;
+                const float Ti = first ? Tlast : Tn * fast_rcp(1.0f - w);  // w <= clamp < 1
+                first = false;
+                Tn = Ti;
+                const float alpha = w * Ti;
+                v[1] = gc0 * alpha;
+                v[2] = gc1 * alpha;
+                v[3] = gc2 * alpha;
+                v[4] = gd * alpha;
+                // dL/dw = T_i [ G.(c - S) + gd (z - Sd) + Gn.(n - Sn) ] + ga T_i R
+                float dLdw = gc0 * (q2.x - S0) + gc1 * (q2.y - S1) + gc2 * (q2.z - S2) + gd * (q2.w - Sd);
+                const float omw = 1.0f - w;
+                if (kExt) {
+                    const float4 q3 = r.q3;
+                    v[10] = gn0 * alpha;
+                    v[11] = gn1 * alpha;
+                    v[12] = gn2 * alpha;
+                    dLdw += gn0 * (q3.x - Sn0) + gn1 * (q3.y - Sn1) + gn2 * (q3.z - Sn2) + ga * R;
+                    Sn0 = w * q3.x + omw * Sn0;
+                    Sn1 = w * q3.y + omw * Sn1;
+                    Sn2 = w * q3.z + omw * Sn2;
+                    R *= omw;
                 }
+                dLdw *= Ti;
+                if (!clamped) {
+                    v[0] = dLdw * g;
+                    const float gm = -0.5f * w * dLdw;  // dL/dm
+                    v[8] = gm * u;  // whitened offset w = (u, v)
+                    v[9] = gm * vv;
+                    v[5] = v[8] * u;
+                    v[6] = v[8] * vv;
+                    v[7] = v[9] * vv;
+                }
+                S0 = w * q2.x + omw * S0;
+                S1 = w * q2.y + omw * S1;
+                S2 = w * q2.z + omw * S2;
+                Sd = w * q2.w + omw * Sd;
             }
-            if (__any_sync(kFull, contrib)) {
-                const float sum = warp_reduce16(v, lane);
-                const uint32_t id = ring.id[buf][s];
-                if (!(lane & 1) && lane < 28 && sum != 0.f) atomicAdd(a.grad2d + (size_t)id * 16 + (lane >> 1), sum);
-            }
+            red_stage<NV, 16>(v, lane);
+            if (own && v[0] != 0.f) atomicAdd(a.grad2d + (size_t)ring.id[buf][s] * 16 + vi, v[0]);
         }
         __syncwarp();  // slot `buf` is refilled by the next ring_fill
         buf ^= 1;
         n = nn;
     }
     cp_wait<0>();
-    int gsum = guard;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) gsum += __shfl_xor_sync(kFull, gsum, o);
-    if (lane == 0 && gsum) atomicAdd(&a.stats->guard_hits, gsum);
 }
 
 }  // namespace

@@ -88,7 +88,12 @@ struct RasterArgs {
     const float *params;
     const int2 *ranges;
     const uint32_t *pair_ids;
-    uint32_t *pair_keys;  // tile | bbox warp-block mask << 16 | ellipse warp-block mask << 24 (forward)
+    uint32_t *pair_keys;  // tile | bbox warp-block mask << 16
+    // Forward -> backward work lists: warp w of tile t appends, in list order, one (surfel id,
+    // lane mask of the block's pixels that blended it) entry per pair its pixels blended, at
+    // bstream[8 ranges[t].x + w (ranges[t].y - ranges[t].x) ...]; bcount[8 t + w] = entries.
+    uint2 *bstream;
+    int *bcount;
     const SplatRecord *rec;
     const short4 *rect;
     int2 *aux;  // per pixel (last list position, float bits of T before it)
@@ -103,7 +108,7 @@ struct RasterArgs {
     double w_rgb, w_depth;
     const float *target_rgb, *target_depth;
     const float *d_color, *d_depth, *d_normal, *d_accum;
-    float *grad2d;  // [n][16]
+    float *grad2d;  // [n][16] per-view 2D gradients (layout in raster.cu, k_raster_bwd)
     double *loss_accum;
 };
 void launch_raster_forward(const RasterArgs &a, cudaStream_t s);
