@@ -90,7 +90,7 @@ typedef struct s2d_view_debug {
     const double *z;            /* (n,) float64 camera depth (valid where flags & 4) */
     const uint8_t *flags;       /* (n,) bit0 in_front, bit1 valid, bit2 on_screen */
     const float *records;       /* (n, 16) splat records */
-    const int32_t *pixel_state; /* (H*W, 2) last blended list position, float bits of T before it */
+    const int32_t *pixel_state; /* (H*W, 2) number of blended pairs, float bits of the final T */
     int32_t ntiles, tiles_x;
     int64_t pair_capacity;
 } s2d_view_debug;

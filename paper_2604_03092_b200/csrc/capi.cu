@@ -189,7 +189,7 @@ struct s2d_view {
     uint8_t *flags = nullptr;
     uint32_t *keys[2] = {nullptr, nullptr}, *vals[2] = {nullptr, nullptr};
     uint32_t *pkeys[2] = {nullptr, nullptr}, *pvals[2] = {nullptr, nullptr};
-    uint2 *bstream = nullptr;  // [8 pcap] per-warp (surfel, lane mask) streams of blended pairs
+    uint4 *bstream = nullptr;  // [8 pcap] per-warp (surfel, blend mask, clamp mask) streams of blended pairs
     int *bcount = nullptr;     // [ntiles * 8] stream lengths
     float *grad2d = nullptr;
     int2 *aux = nullptr;

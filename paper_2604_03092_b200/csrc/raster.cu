@@ -53,7 +53,15 @@ __device__ __forceinline__ void cp_wait() {
 // m <= sigma^2, _raster_kernels.py:32-41); bit1: the weight clamps (w > weight_clamp, :43-44).
 // Takes the view constants from GLOBAL memory: passing the by-value kernel parameter by
 // reference to an out-of-line function would force a copy of it to local memory in every thread.
-__device__ __noinline__ int guard_resolve(const ViewParams *__restrict__ Pg, const float *params, uint32_t id,
+#ifndef S2D_GUARD_INLINE
+#define S2D_GUARD_INLINE 0
+#endif
+#if S2D_GUARD_INLINE
+__device__ __forceinline__
+#else
+__device__ __noinline__
+#endif
+int guard_resolve(const ViewParams *__restrict__ Pg, const float *params, uint32_t id,
                                           int x, int y) {
     const ViewParams &P = *Pg;
     const ParamView pv(params, P.n);
@@ -78,49 +86,41 @@ __device__ __forceinline__ float fast_rcp(float x) {
     return y;
 }
 
-// Per-pixel evaluation shared by forward and backward (must take identical decisions).
-// Fast path: m = |Minv d|^2 in float32.  m < cut - gb implies the reference's float64 m is
-// below the cut, hence the pixel lies inside the reference bbox (the bbox is the ellipse's
-// exact extent), so no bbox test is needed; m > cut + gb rejects.  Inside the band, or when
-// the weight is within 4e-6 of the clamp, guard_resolve decides in float64.
-struct PairEval {
-    float dx, dy, u, v, g, w;
-    bool clamped;
-};
-
-__device__ __forceinline__ bool eval_pair(const ViewParams &P, const ViewParams *Pg, const float *params,
-                                          const SplatRecord &r, const uint32_t *idp, float pxf, float pyf, int px,
-                                          int py, PairEval &o, int &guard_hits) {
-    // record: q0 = (cx_hi, cy_hi, half2 (cx_lo, cy_lo), opacity)
-    const float4 q0 = r.q0;
+// Forward weight of pair (record r, pixel), fwd_weight: 0 if the pair does not blend, else the weight the reference blends with.  Fast path: m = |Minv d|^2 in float32.  m < cut - gb implies the
+// reference's float64 m is below the cut, hence the pixel lies inside the reference bbox (the
+// bbox is the ellipse's exact extent), so no bbox test is needed; m > cut + gb rejects.  Inside
+// the band, or when the weight is within 4e-6 of the clamp, guard_resolve decides in float64.
+// The backward recomputes w with the same float32 operations and takes the clamp decision from
+// the forward's blend stream, so both passes see bit-identical weights.
+__device__ __forceinline__ float pair_maha(const SplatRecord &r, float pxf, float pyf) {
+    const float4 q0 = r.q0, q1 = r.q1;
     const uint32_t lob = __float_as_uint(q0.z);
     const __half2 lo = *reinterpret_cast<const __half2 *>(&lob);
-    // explicit round-to-nearest intrinsics: forward and backward must take
-    // bit-identical decisions, so nothing here may be contracted differently
-    o.dx = __fsub_rn(__fsub_rn(pxf, q0.x), __low2float(lo));
-    o.dy = __fsub_rn(__fsub_rn(pyf, q0.y), __high2float(lo));
-    o.u = __fmaf_rn(r.q1.x, o.dx, __fmul_rn(r.q1.y, o.dy));
-    o.v = __fmaf_rn(r.q1.z, o.dx, __fmul_rn(r.q1.w, o.dy));
-    const float m = __fmaf_rn(o.u, o.u, __fmul_rn(o.v, o.v));
-    const float gb = r.q3.w;  // guard band of m
-    if (m > P.maha_cut_f + gb) return false;
-    o.g = fast_exp2(__fmul_rn(m, -0.72134752044448170368f));  // exp(-m/2); m <= sigma^2 + gb keeps it normal
-    float w = __fmul_rn(q0.w, o.g);
-    bool band = m >= P.maha_cut_f - gb;
-    o.clamped = false;
-    if (q0.w > P.w_clamp_f - 8e-6f) {  // opacity close enough to the clamp for the weight to reach it
-        band |= fabsf(w - P.w_clamp_f) <= 4e-6f;
-        o.clamped = w > P.w_clamp_f;
-    }
-    if (band) {
+    const float dx = __fsub_rn(__fsub_rn(pxf, q0.x), __low2float(lo));
+    const float dy = __fsub_rn(__fsub_rn(pyf, q0.y), __high2float(lo));
+    const float u = __fmaf_rn(q1.x, dx, __fmul_rn(q1.y, dy));
+    const float v = __fmaf_rn(q1.z, dx, __fmul_rn(q1.w, dy));
+    return __fmaf_rn(u, u, __fmul_rn(v, v));
+}
+
+__device__ __forceinline__ float fwd_weight(const ViewParams &P, const ViewParams *Pg, const float *params,
+                                            const SplatRecord &r, uint32_t id, float pxf, float pyf, int px,
+                                            int py, bool &clamped, int &guard_hits) {
+    const float m = pair_maha(r, pxf, pyf);
+    const float op = r.q0.w, gb = r.q3.w;
+    clamped = false;
+    if (m > P.maha_cut_f + gb) return 0.f;
+    const float w = __fmul_rn(op, fast_exp2(__fmul_rn(m, -0.72134752044448170368f)));
+    const bool nearclamp = op > P.w_clamp_f - 8e-6f;
+    if (m >= P.maha_cut_f - gb || (nearclamp && fabsf(w - P.w_clamp_f) <= 4e-6f)) {
         ++guard_hits;
-        const int rr = guard_resolve(Pg, params, *idp, px, py);
-        if (!(rr & 1)) return false;
-        o.clamped = (rr & 2) != 0;
+        const int rr = guard_resolve(Pg, params, id, px, py);
+        if (!(rr & 1)) return 0.f;
+        clamped = (rr & 2) != 0;
+    } else {
+        clamped = nearclamp && w > P.w_clamp_f;
     }
-    if (o.clamped) w = P.w_clamp_f;
-    o.w = w;
-    return w > 0.0f;
+    return clamped ? P.w_clamp_f : fmaxf(w, 0.f);
 }
 
 // Warp-private candidate ring (forward).  Each warp streams ITS OWN candidates from the tile's
@@ -131,7 +131,8 @@ __device__ __forceinline__ bool eval_pair(const ViewParams &P, const ViewParams 
 struct WarpRing {
     SplatRecord rec[2][32];
     uint32_t id[2][32];
-    uint32_t aux[2][32];  // forward: list position; backward: lane mask
+    uint32_t lm[2][32];  // backward: lane mask of the pixels that blended the pair
+    uint32_t cm[2][32];  // backward: ... of the pixels whose weight was clamped
 };
 
 // Cursor over list positions [lo, hi).  The current 32-wide chunk starts at `cb` (lane l holds
@@ -188,7 +189,6 @@ __device__ __forceinline__ int ring_fill(WarpRing &rg, int buf, ListCursor &c, c
             cp_async16(d + 2, g + 2);
             cp_async16(d + 3, g + 3);
             rg.id[buf][s] = c.kid;
-            rg.aux[buf][s] = (uint32_t)(c.cb + lane);
         }
         c.pend &= ~__ballot_sync(kFull, mine);
         n += take;
@@ -198,11 +198,11 @@ __device__ __forceinline__ int ring_fill(WarpRing &rg, int buf, ListCursor &c, c
 
 // Backward ring fill: entries [e0, e1) of the warp's blend stream, newest first (slot s holds
 // entry e1 - 1 - s).  Every entry is work, so this is one coalesced 8-B load per lane.
-__device__ __forceinline__ int stream_fill(WarpRing &rg, int buf, const uint2 *ws, int e0, int e1,
+__device__ __forceinline__ int stream_fill(WarpRing &rg, int buf, const uint4 *ws, int e0, int e1,
                                            const SplatRecord *rec, int lane) {
     const int n = min(32, e1 - e0);
     if (lane < n) {
-        const uint2 en = __ldcg(ws + (e1 - 1 - lane));
+        const uint4 en = __ldcg(ws + (e1 - 1 - lane));
         const float4 *g = reinterpret_cast<const float4 *>(rec + en.x);
         float4 *d = reinterpret_cast<float4 *>(&rg.rec[buf][lane]);
         cp_async16(d + 0, g + 0);
@@ -210,7 +210,8 @@ __device__ __forceinline__ int stream_fill(WarpRing &rg, int buf, const uint2 *w
         cp_async16(d + 2, g + 2);
         cp_async16(d + 3, g + 3);
         rg.id[buf][lane] = en.x;
-        rg.aux[buf][lane] = en.y;
+        rg.lm[buf][lane] = en.y;
+        rg.cm[buf][lane] = en.z;
     }
     return n;
 }
@@ -228,20 +229,18 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
     const float pxf = (float)px, pyf = (float)py;
     const int2 rg = a.ranges[tile];
 
-    float T = 1.0f, Tpre = 1.0f;
+    float T = 1.0f;
     float c0 = 0.f, c1 = 0.f, c2 = 0.f, dep = 0.f, n0 = 0.f, n1 = 0.f, n2 = 0.f;
     float maxw = 0.f;
-    int argw = -1, last = -1, guard = 0;
+    int argw = -1, nblend = 0, guard = 0;
     bool done = !inside;
     const float term_t = P.term_t_f;
     WarpRing &ring = s_ring[warp];
 
-    // this warp's blend stream (one entry per pair its pixels blended, for the backward);
-    // entries are gathered in registers, lane (count % 32) holding the newest, and written
-    // 32 at a time
-    uint2 *ws = a.bstream + 8 * (size_t)rg.x + (size_t)warp * (size_t)max(rg.y - rg.x, 0);
+    // this warp's blend stream: one (surfel, lane mask) entry per pair its pixels blended, in
+    // list order (the backward's work list)
+    uint4 *ws = a.bstream + 8 * (size_t)rg.x + (size_t)warp * (size_t)max(rg.y - rg.x, 0);
     int wc = 0;
-    uint2 went = make_uint2(0u, 0u);
     if (rg.y > rg.x && !__all_sync(kFull, done)) {
         ListCursor cur;
         cursor_init(cur, a, rg.x, rg.y, lane);
@@ -258,15 +257,14 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
             while (hm) {
                 const int k = __ffs(hm) - 1;
                 hm &= hm - 1;
-                const uint32_t id = ring.id[buf][k];
+                const SplatRecord &r = ring.rec[buf][k];
                 float contrib = 0.f;
-                bool blended = false;
+                bool bl = false, clamped = false;
                 if (!done) {
-                    PairEval e;
-                    const SplatRecord &r = ring.rec[buf][k];
-                    if (eval_pair(P, a.Pg, a.params, r, &ring.id[buf][k], pxf, pyf, px, py, e, guard)) {
-                        blended = true;
-                        contrib = e.w * T;
+                    const float w = fwd_weight(P, a.Pg, a.params, r, ring.id[buf][k], pxf, pyf, px, py, clamped, guard);
+                    if (w > 0.f) {  // blend (blend_forward, _raster_kernels.py:47-55)
+                        bl = true;
+                        contrib = w * T;
                         const float4 q2 = r.q2;
                         c0 = fmaf(contrib, q2.x, c0);
                         c1 = fmaf(contrib, q2.y, c1);
@@ -280,22 +278,17 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
                         }
                         if (kArg && contrib > maxw) {
                             maxw = contrib;
-                            argw = (int)id;
+                            argw = (int)ring.id[buf][k];
                         }
-                        Tpre = T;
-                        T = T * (1.0f - e.w);
-                        last = (int)ring.aux[buf][k];
+                        T = T * (1.0f - w);
+                        ++nblend;
                         done = T < term_t;
                     }
                 }
-                // the exact set of this block's pixels that blended the pair
-                const uint32_t bm = __ballot_sync(kFull, blended);
-                if (bm) {
-                    if (lane == (wc & 31)) went = make_uint2(id, bm);
-                    if ((wc & 31) == 31) ws[wc - 31 + lane] = went;
-                    ++wc;
-                }
+                // the exact set of this block's pixels that blended the pair -> blend stream
+                const uint32_t bm = __ballot_sync(kFull, bl);
                 if (kMaxW) {
+                    const uint32_t id = ring.id[buf][k];
                     float mx = contrib;
                     float mm = (a.mask != nullptr && inside && a.mask[py * P.W + px]) ? contrib : 0.f;
 #pragma unroll
@@ -309,7 +302,12 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
                             atomicMax(reinterpret_cast<int *>(a.max_marked + id), __float_as_int(mm));
                     }
                 }
-                if (__all_sync(kFull, done)) break;
+                if (bm) {
+                    const uint32_t cm = __ballot_sync(kFull, bl && clamped);
+                    if (lane == 0) ws[wc] = make_uint4(ring.id[buf][k], bm, cm, 0u);
+                    ++wc;
+                    if (__all_sync(kFull, done)) break;
+                }
             }
             if (__all_sync(kFull, done)) break;
             __syncwarp();  // slot `buf` is refilled by the next ring_fill
@@ -318,7 +316,6 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
         }
         cp_wait<0>();
     }
-    if (lane < (wc & 31)) ws[(wc & ~31) + lane] = went;
     if (lane == 0) a.bcount[8 * tile + warp] = wc;
     if (inside) {
         const int p = py * P.W + px;
@@ -338,7 +335,7 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
             if (a.max_w) a.max_w[p] = maxw;
             if (a.arg_w) a.arg_w[p] = argw;
         }
-        a.aux[p] = make_int2(last, __float_as_int(Tpre));
+        a.aux[p] = make_int2(nblend, __float_as_int(T));
     }
     const int nm = __popc(__ballot_sync(kFull, inside && (1.0f - T) > 0.5f));
     int gsum = guard;
@@ -399,16 +396,6 @@ __device__ __forceinline__ void red_map(int lane, int &vi, bool &own) {
     own = ow[0];
 }
 
-// Rare path of the backward: the weight-clamp decision for a pair whose opacity is within
-// 8e-6 of the clamp, taken exactly as eval_pair takes it in the forward.
-__device__ __noinline__ bool clamp_decision(const ViewParams *__restrict__ Pg, const float *params, uint32_t id,
-                                            float m, float w, float gb, int x, int y) {
-    const ViewParams &P = *Pg;
-    const bool band = m >= P.maha_cut_f - gb || fabsf(w - P.w_clamp_f) <= 4e-6f;
-    if (!band) return w > P.w_clamp_f;
-    return (guard_resolve(Pg, params, id, x, y) & 2) != 0;
-}
-
 __device__ __forceinline__ float sgnf(float x) { return x > 0.f ? 1.f : (x < 0.f ? -1.f : 0.f); }
 
 template <bool kExt>  // kExt: normal / accumulation seeds present (external loss)
@@ -429,10 +416,10 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
     // ---- loss seeds (rasterizer.py:375-380 for MSE; L1; external) ----
     float gc0 = 0.f, gc1 = 0.f, gc2 = 0.f, gd = 0.f, gn0 = 0.f, gn1 = 0.f, gn2 = 0.f, ga = 0.f;
     float lpx = 0.f;
-    float Tlast = 1.f;
+    float Tn = 1.f;  // transmittance after the contributors processed so far (forward: final T)
     if (inside) {
         const int2 ax = a.aux[p];
-        Tlast = __int_as_float(ax.y);
+        Tn = __int_as_float(ax.y);
         const double npx = (double)P.W * (double)P.H;
         if (a.loss_kind == S2D_LOSS_EXTERNAL) {
             if (a.d_color) {
@@ -507,12 +494,10 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
     int vi;
     bool own;
     red_map<NV>(lane, vi, own);
-    float Tn = Tlast;  // transmittance before the later contributor
-    bool first = true;
     float R = 1.f;     // prod_{j later} (1 - w_j)
     float S0 = 0.f, S1 = 0.f, S2 = 0.f, Sd = 0.f, Sn0 = 0.f, Sn1 = 0.f, Sn2 = 0.f;
     WarpRing &ring = s_ring[warp];
-    const uint2 *ws = a.bstream + 8 * (size_t)rg.x + (size_t)warp * (size_t)(rg.y - rg.x);
+    const uint4 *ws = a.bstream + 8 * (size_t)rg.x + (size_t)warp * (size_t)(rg.y - rg.x);
     int e1 = cnt;
     int buf = 0;
     int n = stream_fill(ring, 0, ws, max(e1 - 32, 0), e1, a.rec, lane);
@@ -528,8 +513,8 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
             float v[16];
 #pragma unroll
             for (int t = 0; t < 16; ++t) v[t] = 0.f;
-            if ((ring.aux[buf][s] >> lane) & 1u) {
-                // the forward's arithmetic (eval_pair), minus the decisions it already took
+            if ((ring.lm[buf][s] >> lane) & 1u) {
+                // the forward's arithmetic (fwd_weight), minus the decisions it already took
                 const SplatRecord &r = ring.rec[buf][s];
                 const float4 q0 = r.q0, q1 = r.q1, q2 = r.q2;
                 const uint32_t lob = __float_as_uint(q0.z);
@@ -540,13 +525,9 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
                 const float vv = __fmaf_rn(q1.z, dx, __fmul_rn(q1.w, dy));
                 const float m = __fmaf_rn(u, u, __fmul_rn(vv, vv));
                 const float g = fast_exp2(__fmul_rn(m, -0.72134752044448170368f));
-                float w = __fmul_rn(q0.w, g);
-                bool clamped = false;
-                if (q0.w > P.w_clamp_f - 8e-6f)
-                    clamped = clamp_decision(a.Pg, a.params, ring.id[buf][s], m, w, r.q3.w, px, py);
-                if (clamped) w = P.w_clamp_f;
-                const float Ti = first ? Tlast : Tn * fast_rcp(1.0f - w);  // w <= clamp < 1
-                first = false;
+                const bool clamped = (ring.cm[buf][s] >> lane) & 1u;
+                const float w = clamped ? P.w_clamp_f : __fmul_rn(q0.w, g);
+                const float Ti = Tn * fast_rcp(1.0f - w);  // T before this contributor; w <= clamp < 1
                 Tn = Ti;
                 const float alpha = w * Ti;
                 v[1] = gc0 * alpha;

@@ -90,9 +90,10 @@ struct RasterArgs {
     const uint32_t *pair_ids;
     uint32_t *pair_keys;  // tile | bbox warp-block mask << 16
     // Forward -> backward work lists: warp w of tile t appends, in list order, one (surfel id,
-    // lane mask of the block's pixels that blended it) entry per pair its pixels blended, at
+    // lane mask of the block's pixels that blended it, lane mask of those whose weight was
+    // clamped, 0) entry per pair its pixels blended, at
     // bstream[8 ranges[t].x + w (ranges[t].y - ranges[t].x) ...]; bcount[8 t + w] = entries.
-    uint2 *bstream;
+    uint4 *bstream;
     int *bcount;
     const SplatRecord *rec;
     const short4 *rect;
