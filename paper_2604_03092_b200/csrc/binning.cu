@@ -56,7 +56,6 @@ __device__ __forceinline__ uint32_t block_exclusive_scan_256(uint32_t v, uint32_
 __global__ void __launch_bounds__(kProjThreads) k_project(const ProjectArgs a) {
     const int64_t i = (int64_t)blockIdx.x * kProjThreads + threadIdx.x;
     const ViewParams &P = a.P;
-    if (blockIdx.x == 0 && threadIdx.x == 0) *a.P_out = a.P;
     bool on = false, degen = false;
     uint32_t key = 0xffffffffu;
     if (i < P.n) {
@@ -93,6 +92,13 @@ __global__ void __launch_bounds__(kProjThreads) k_project(const ProjectArgs a) {
             const double gb = 4e-5 * kappa + 1e-5 / sqrt(e.lmin) + 4e-6;
             r.q3 = make_float4((float)(sg * nn[0]), (float)(sg * nn[1]), (float)(sg * nn[2]), (float)gb);
             a.rec[i] = r;
+            ExactRec x;
+            x.cx = e.cx;
+            x.cy = e.cy;
+            x.ia = e.ia;
+            x.ib = e.ib;
+            x.ic = e.ic;
+            a.exact[i] = x;
             a.rect[i] = make_short4((short)e.x0, (short)e.x1, (short)e.y0, (short)e.y1);
             a.z64[i] = e.p[2];
             key = (uint32_t)((uint64_t)__double_as_longlong(e.p[2]) >> 32);  // z > 0: monotone

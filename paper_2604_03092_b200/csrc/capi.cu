@@ -182,8 +182,9 @@ struct s2d_view {
     // capacities (elements)
     int64_t cap_rec = 0, cap_rect = 0, cap_z = 0, cap_flags = 0, cap_keys[2] = {0, 0},
             cap_vals[2] = {0, 0}, cap_grad = 0, cap_aux = 0, cap_pk[2] = {0, 0}, cap_pv[2] = {0, 0},
-            cap_bs = 0, cap_bc = 0, cap_sync = 0;
+            cap_bs = 0, cap_bc = 0, cap_ex = 0, cap_sync = 0;
     SplatRecord *rec = nullptr;
+    ExactRec *exact = nullptr;  // float64 centre + inv_abc per on-screen surfel (guard-band path)
     short4 *rect = nullptr;
     double *z64 = nullptr;
     uint8_t *flags = nullptr;
@@ -251,7 +252,6 @@ int layout_sync(s2d_view *v, int64_t n, int64_t pcap, int ntiles) {
     const size_t o_pstat = take((size_t)2 * psort_tiles * kRadix * 4);
     const size_t o_claim = take((size_t)(n + 1) * 4);
     const size_t o_ranges = take((size_t)ntiles * sizeof(int2));
-    const size_t o_params = take(sizeof(ViewParams));
     int64_t need = (int64_t)off;
     int rc = grow(v->sync, v->cap_sync, need);
     if (rc) return rc;
@@ -266,7 +266,6 @@ int layout_sync(s2d_view *v, int64_t n, int64_t pcap, int ntiles) {
     v->sr.pair_status = reinterpret_cast<uint32_t *>(b + o_pstat);
     v->sr.tie_claim = reinterpret_cast<uint32_t *>(b + o_claim);
     v->sr.ranges = reinterpret_cast<int2 *>(b + o_ranges);
-    v->sr.params = reinterpret_cast<ViewParams *>(b + o_params);
     v->sr.bytes = off;
     return S2D_OK;
 }
@@ -275,6 +274,7 @@ int ensure_capacity(s2d_view *v, int64_t n, int64_t npx, int ntiles) {
     int rc;
     const int64_t nn = n < 1 ? 1 : n;
     if ((rc = grow(v->rec, v->cap_rec, nn))) return rc;
+    if ((rc = grow(v->exact, v->cap_ex, nn))) return rc;
     if ((rc = grow(v->rect, v->cap_rect, nn))) return rc;
     if ((rc = grow(v->z64, v->cap_z, nn))) return rc;
     if ((rc = grow(v->flags, v->cap_flags, nn))) return rc;
@@ -326,9 +326,9 @@ int view_forward(s2d_view *v, cudaStream_t s, const float *params, int64_t n, co
     if (n > 0) {
         ProjectArgs pa;
         pa.P = P;
-        pa.P_out = sr.params;
         pa.params = params;
         pa.rec = v->rec;
+        pa.exact = v->exact;
         pa.rect = v->rect;
         pa.z64 = v->z64;
         pa.flags = v->flags;
@@ -389,7 +389,6 @@ int view_forward(s2d_view *v, cudaStream_t s, const float *params, int64_t n, co
     RasterArgs ra;
     memset(&ra, 0, sizeof(ra));
     ra.P = P;
-    ra.Pg = sr.params;
     ra.params = params;
     ra.ranges = sr.ranges;
     ra.pair_ids = v->pvals[v->pair_buf];
@@ -397,6 +396,7 @@ int view_forward(s2d_view *v, cudaStream_t s, const float *params, int64_t n, co
     ra.bstream = v->bstream;
     ra.bcount = v->bcount;
     ra.rec = v->rec;
+    ra.exact = v->exact;
     ra.rect = v->rect;
     ra.aux = v->aux;
     ra.color = out->color;
@@ -455,7 +455,7 @@ int s2d_view_create(s2d_ctx *ctx, s2d_view **out) {
 
 int s2d_view_destroy(s2d_view *v) {
     if (!v) return S2D_OK;
-    void *ptrs[] = {v->rec, v->rect, v->z64, v->flags, v->keys[0], v->keys[1], v->vals[0], v->vals[1],
+    void *ptrs[] = {v->rec, v->exact, v->rect, v->z64, v->flags, v->keys[0], v->keys[1], v->vals[0], v->vals[1],
                     v->pkeys[0], v->pkeys[1], v->pvals[0], v->pvals[1], v->bstream, v->bcount, v->grad2d, v->aux, v->sync,
                     v->h_params_dev, v->h_img_dev};
     for (void *p : ptrs)
@@ -576,7 +576,6 @@ int s2d_backward(s2d_view *v, void *stream, const float *params, int64_t n, cons
     RasterArgs ra;
     memset(&ra, 0, sizeof(ra));
     ra.P = v->P;
-    ra.Pg = v->sr.params;
     ra.params = params;
     ra.ranges = v->sr.ranges;
     ra.pair_ids = v->pvals[v->pair_buf];
@@ -584,6 +583,7 @@ int s2d_backward(s2d_view *v, void *stream, const float *params, int64_t n, cons
     ra.bstream = v->bstream;
     ra.bcount = v->bcount;
     ra.rec = v->rec;
+    ra.exact = v->exact;
     ra.rect = v->rect;
     ra.aux = v->aux;
     ra.color = image->color;

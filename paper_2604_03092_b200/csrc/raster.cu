@@ -23,7 +23,7 @@
 #include "s2d_kernels.h"
 
 #ifndef S2D_FWD_MINB
-#define S2D_FWD_MINB 3
+#define S2D_FWD_MINB 4
 #endif
 #ifndef S2D_BWD_MINB
 #define S2D_BWD_MINB 3
@@ -47,30 +47,18 @@ __device__ __forceinline__ void cp_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// Guard-band resolution (rare path, kept out of line so the hot loop stays lean):
-// re-takes the reference's decisions for pixel (x, y) and surfel `id` in float64 with the
-// reference's own formulas.  bit0: the pair blends (pixel inside the reference bbox and
-// m <= sigma^2, _raster_kernels.py:32-41); bit1: the weight clamps (w > weight_clamp, :43-44).
-// Takes the view constants from GLOBAL memory: passing the by-value kernel parameter by
-// reference to an out-of-line function would force a copy of it to local memory in every thread.
-#ifndef S2D_GUARD_INLINE
-#define S2D_GUARD_INLINE 0
-#endif
-#if S2D_GUARD_INLINE
-__device__ __forceinline__
-#else
-__device__ __noinline__
-#endif
-int guard_resolve(const ViewParams *__restrict__ Pg, const float *params, uint32_t id,
-                                          int x, int y) {
-    const ViewParams &P = *Pg;
-    const ParamView pv(params, P.n);
-    ExactProj e;
-    project_exact(P, pv, id, e);
-    if (x < e.x0 || x > e.x1 || y < e.y0 || y > e.y1) return 0;
-    const double m64 = exact_maha(e, x, y);
+// Guard-band resolution (rare path): re-takes the reference's decisions for pixel (x, y) and
+// surfel `id` in float64 from the projection's exact record.  bit0: the pair blends (pixel
+// inside the reference bbox and m <= sigma^2, _raster_kernels.py:32-41); bit1: the weight
+// clamps (w > weight_clamp, :43-44).
+__device__ __forceinline__ int guard_resolve(const ViewParams &P, const RasterArgs &a, uint32_t id, float op, int x,
+                                             int y) {
+    const short4 b = a.rect[id];
+    if (x < b.x || x > b.y || y < b.z || y > b.w) return 0;
+    const ExactRec &e = a.exact[id];
+    const double m64 = exact_maha(e.cx, e.cy, e.ia, e.ib, e.ic, x, y);
     if (m64 > P.maha_cut) return 0;
-    const double w64 = (double)pv.opac[id] * exp(-0.5 * m64);
+    const double w64 = (double)op * exp(-0.5 * m64);
     return 1 | (w64 > P.w_clamp ? 2 : 0);
 }
 
@@ -103,9 +91,9 @@ __device__ __forceinline__ float pair_maha(const SplatRecord &r, float pxf, floa
     return __fmaf_rn(u, u, __fmul_rn(v, v));
 }
 
-__device__ __forceinline__ float fwd_weight(const ViewParams &P, const ViewParams *Pg, const float *params,
-                                            const SplatRecord &r, uint32_t id, float pxf, float pyf, int px,
-                                            int py, bool &clamped, int &guard_hits) {
+__device__ __forceinline__ float fwd_weight(const ViewParams &P, const RasterArgs &a, const SplatRecord &r,
+                                            uint32_t id, float pxf, float pyf, int px, int py, bool &clamped,
+                                            int &guard_hits) {
     const float m = pair_maha(r, pxf, pyf);
     const float op = r.q0.w, gb = r.q3.w;
     clamped = false;
@@ -114,7 +102,7 @@ __device__ __forceinline__ float fwd_weight(const ViewParams &P, const ViewParam
     const bool nearclamp = op > P.w_clamp_f - 8e-6f;
     if (m >= P.maha_cut_f - gb || (nearclamp && fabsf(w - P.w_clamp_f) <= 4e-6f)) {
         ++guard_hits;
-        const int rr = guard_resolve(Pg, params, id, px, py);
+        const int rr = guard_resolve(P, a, id, op, px, py);
         if (!(rr & 1)) return 0.f;
         clamped = (rr & 2) != 0;
     } else {
@@ -261,7 +249,7 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
                 float contrib = 0.f;
                 bool bl = false, clamped = false;
                 if (!done) {
-                    const float w = fwd_weight(P, a.Pg, a.params, r, ring.id[buf][k], pxf, pyf, px, py, clamped, guard);
+                    const float w = fwd_weight(P, a, r, ring.id[buf][k], pxf, pyf, px, py, clamped, guard);
                     if (w > 0.f) {  // blend (blend_forward, _raster_kernels.py:47-55)
                         bl = true;
                         contrib = w * T;

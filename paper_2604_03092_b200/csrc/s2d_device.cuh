@@ -203,13 +203,18 @@ __device__ __forceinline__ void project_exact(const ViewParams &P, const ParamVi
                   (dadd(o.cy, o.ry) >= 0.0) && (dsub(o.cy, o.ry) <= P.hm1);
 }
 
+// The float64 quantities the per-pixel decisions depend on (reference centre and inv_abc),
+// written per on-screen surfel by k_project for the raster guard-band re-checks.
+struct ExactRec {
+    double cx, cy, ia, ib, ic;
+};
+
 // Reference Mahalanobis distance at integer pixel (x, y), float64 with the
 // reference's association (_raster_kernels.py:38-39), for guard-band re-checks.
-__device__ __forceinline__ double exact_maha(const ExactProj &e, int x, int y) {
-    const double dx = dsub((double)x, e.cx);
-    const double dy = dsub((double)y, e.cy);
-    return dadd(dadd(dmul(dmul(e.ia, dx), dx), dmul(dmul(dmul(2.0, e.ib), dx), dy)),
-                dmul(dmul(e.ic, dy), dy));
+__device__ __forceinline__ double exact_maha(double cx, double cy, double ia, double ib, double ic, int x, int y) {
+    const double dx = dsub((double)x, cx);
+    const double dy = dsub((double)y, cy);
+    return dadd(dadd(dmul(dmul(ia, dx), dx), dmul(dmul(dmul(2.0, ib), dx), dy)), dmul(dmul(ic, dy), dy));
 }
 
 // Conservative minimum over the continuous rectangle [x0,x1]x[y0,y1] (pixel coordinates,

@@ -36,15 +36,14 @@ struct SyncRegion {
     uint32_t *pair_status;     // [2][ceil(pcap / kSortTile) * kRadix]
     uint32_t *tie_claim;       // [n]
     int2 *ranges;              // [ntiles]
-    ViewParams *params;        // device copy of the view constants (guard-band path)
     size_t bytes;
 };
 
 struct ProjectArgs {
     ViewParams P;
-    ViewParams *P_out;  // device copy written by block 0 (read by the raster guard path)
     const float *params;
     SplatRecord *rec;
+    ExactRec *exact;
     short4 *rect;
     double *z64;
     uint8_t *flags;
@@ -84,7 +83,6 @@ void launch_tile_ranges(const uint32_t *pkeys, const int *d_p, uint32_t pcap, in
 
 struct RasterArgs {
     ViewParams P;
-    const ViewParams *Pg;  // the same constants in global memory (rare float64 path)
     const float *params;
     const int2 *ranges;
     const uint32_t *pair_ids;
@@ -96,6 +94,7 @@ struct RasterArgs {
     uint4 *bstream;
     int *bcount;
     const SplatRecord *rec;
+    const ExactRec *exact;
     const short4 *rect;
     int2 *aux;  // per pixel (last list position, float bits of T before it)
     // forward outputs (forward writes, backward reads)
