@@ -128,6 +128,33 @@ def test_config_gradients(name, sc, pose, kind):
         assert ok, (f, mx, l2)
 
 
+@pytest.mark.parametrize("kind", ["mse", "l1"])
+def test_saturated_opacity_gradients(kind):
+    """Opacities at 1 (where Adam's clip leaves them) and just around the weight clamp: the
+    forward's clamp decisions travel to the backward in the blend stream; all five parameter
+    groups vs the float64 oracle."""
+    sc = scenes.config2(3)
+    s = sc.surfels
+    rng = np.random.default_rng(5)
+    op = np.asarray(s.opacities, dtype=np.float64).copy()
+    pick = rng.random(len(op))
+    op[pick < 0.4] = 1.0
+    band = (pick >= 0.4) & (pick < 0.5)
+    op[band] = np.float32(0.999) + rng.integers(-40, 40, band.sum()) * 1e-6
+    s = SurfelArrays(s.means, s.quats, s.scales, op.astype(np.float32).astype(np.float64), s.colors)
+    pose = sc.poses[0]
+    run = Run(s, pose, sc.intr, normal=True, argmax=False)
+    ref = O.render(s, pose, sc.intr)
+    trgb, tdep = far_targets(ref.color, ref.depth, np.random.default_rng(19))
+    mask = kind == "mse"
+    g, loss = run.backward(kind, trgb, tdep, 1.0, 0.1, mask)
+    oloss, og, _ = O.loss_and_grads(s, pose, sc.intr, trgb, tdep, kind, 1.0, 0.1, mask_depth=mask)
+    assert abs(loss - oloss) <= 1e-5 * abs(oloss)
+    for f in ("colors", "opacities", "means", "quats", "scales"):
+        ok, mx, l2 = gate(g[f], getattr(og, f))
+        assert ok, (f, mx, l2)
+
+
 def test_external_seeds_normal_and_accumulation_grads():
     """Upstream gradients on all four outputs (normal and accumulation included)."""
     sc = scenes.config2(1)
