@@ -53,13 +53,46 @@ __device__ __forceinline__ uint32_t block_exclusive_scan_256(uint32_t v, uint32_
 
 // ------------------------------------------------------------------ projection
 
+// Conservative early rejection: true only when the surfel certainly fails the reference's
+// in-front gates (rasterizer.py:206-210, 231-236), judged in float32 with a wide margin.
+// Such surfels have in_front = valid = on_screen = false exactly, so the float64 projection
+// (divisions, square roots) is skipped for them; everything near a gate boundary takes the
+// exact path.
+__device__ __forceinline__ bool clearly_out(const ViewParams &P, const ParamView &pv, int64_t i) {
+    const float mx = pv.means[3 * i], my = pv.means[3 * i + 1], mz = pv.means[3 * i + 2];
+    float p[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+        p[r] = (float)P.m_cw[3 * r] * mx + (float)P.m_cw[3 * r + 1] * my + (float)P.m_cw[3 * r + 2] * mz +
+               (float)P.inv[1 + r];
+    // float32 p carries an absolute error of about 1e-6 |m_cw||mu| + |t|; keep a generous slack
+    const float slack = 1e-4f * (fabsf(mx) + fabsf(my) + fabsf(mz) + fabsf((float)P.inv[1]) +
+                                 fabsf((float)P.inv[2]) + fabsf((float)P.inv[3]) + 1.f);
+    const float z = p[2];
+    if (z + slack <= (float)P.near_plane) return true;  // certainly z <= near
+    if (z - slack <= 0.f) return false;                 // too close to call: exact path
+    const float zl = z - slack, zh = z + slack;
+    // centre x range over the z / x uncertainty (fx > 0)
+    const float xl = p[0] - slack, xh = p[0] + slack, yl = p[1] - slack, yh = p[1] + slack;
+    const float fx = (float)P.fx, fy = (float)P.fy;
+    const float cxl = fx * fminf(xl / zl, xl / zh) + (float)P.cx, cxh = fx * fmaxf(xh / zl, xh / zh) + (float)P.cx;
+    const float cyl = fy * fminf(yl / zl, yl / zh) + (float)P.cy, cyh = fy * fmaxf(yh / zl, yh / zh) + (float)P.cy;
+    const float tol = 1e-3f * (fabsf(cxl) + fabsf(cxh) + fabsf(cyl) + fabsf(cyh) + 1.f);
+    return cxh + tol < -(float)P.mx || cxl - tol > (float)P.wmax || cyh + tol < -(float)P.my ||
+           cyl - tol > (float)P.hmax;
+}
+
 __global__ void __launch_bounds__(kProjThreads) k_project(const ProjectArgs a) {
     const int64_t i = (int64_t)blockIdx.x * kProjThreads + threadIdx.x;
     const ViewParams &P = a.P;
     bool on = false, degen = false;
     uint32_t key = 0xffffffffu;
-    if (i < P.n) {
-        const ParamView pv(a.params, P.n);
+    const ParamView pv(a.params, P.n);
+    if (i < P.n && clearly_out(P, pv, i)) {
+        a.flags[i] = 0;
+        a.keys[i] = key;
+        a.vals[i] = (uint32_t)i;
+    } else if (i < P.n) {
         ExactProj e;
         project_exact(P, pv, i, e);
         on = e.on_screen;
