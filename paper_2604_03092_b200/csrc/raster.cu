@@ -1,23 +1,28 @@
 // raster.cu — per-tile front-to-back compositing and its reverse-order backward
 // (SURVEY.md §8(a) A7-A9, N1-N3).
 //
-// One 256-thread CTA per 16x16 tile.  Warp w owns an 8x4 pixel block
-// (2 columns x 4 rows of warps); lane l owns pixel (l & 7, l >> 3) of it.
-// The tile's depth-ordered list is staged 256 records at a time into shared
-// memory with cp.async (double buffered, ids prefetched two batches ahead).
-// Each warp then ballots which staged records' integer bboxes touch its 8x4
-// block and walks only those, in list order, so per-pixel work is spent on
-// in-bbox pairs instead of the whole tile list.  A warp stops when every lane's
-// transmittance is below the termination threshold (ballot), the CTA when all
-// warps have (barrier count).
+// One 256-thread CTA per 16x16 tile.  Warp w owns an 8x4 pixel block (2 columns x 4 rows
+// of warps); lane l owns pixel (l & 7, l >> 3) of it.
 //
-// Semantics follow blend_forward (_raster_kernels.py:22-55) exactly: the
-// termination test precedes blending, pixel (row y, col x) samples (x, y),
-// the Mahalanobis cut is `m > sigma^2` on the integer bbox, weights clamp at
-// weight_clamp, `w <= 0` skips.  m and the weight clamp are evaluated in
-// float32; inside a per-surfel guard band around the cut and around the clamp
-// the decision is re-taken in float64 with the reference's formula, so the
-// set of blended pairs equals the reference's.
+// Forward (k_raster_fwd): each warp streams its own candidates from the tile's depth-ordered
+// list (entries whose bbox bit for its block is set, k_scan_emit) into a warp-private
+// double-buffered ring of 64-B records (cp.async), culls them lane-parallel against the
+// block with the exact ellipse test, and blends the survivors in list order, one pixel per
+// lane.  A warp stops when every lane's transmittance is below the termination threshold.
+// For every pair its pixels blended the warp appends (surfel, lane mask of the pixels that
+// blended it, lane mask of those whose weight clamped) to its blend stream.
+//
+// Backward (k_raster_bwd): each warp walks its blend stream newest first and runs the
+// reverse recurrence (transmittance recovered by division, normalised suffix
+// S <- w c + (1 - w) S) on exactly the forward's blended set; the per-entry 2D gradients are
+// reduced over the warp (transposed butterfly) and added with one atomic per value.
+//
+// Semantics follow blend_forward (_raster_kernels.py:22-55) exactly: the termination test
+// precedes blending, pixel (row y, col x) samples (x, y), the Mahalanobis cut is
+// `m > sigma^2` on the integer bbox, weights clamp at weight_clamp, `w <= 0` skips.  m and
+// the weight clamp are evaluated in float32; inside a per-surfel guard band around the cut
+// and around the clamp the decision is re-taken in float64 with the reference's formula, so
+// the set of blended pairs equals the reference's.
 #include <cuda_fp16.h>
 
 #include "s2d_kernels.h"
