@@ -203,6 +203,39 @@ int s2d_render_host(s2d_view *view, const double *means, const double *quats, co
                     double *color, double *depth, double *accumulation, double *normal,
                     int32_t *degenerate_skipped);
 
+/* ---- map maintenance around the render path ---- */
+
+/*
+ * transform_surfels (mapper.py:184-197): params_out = Sim(3) `pose` applied to the packed
+ * block params_in (n surfels, device; may not alias): means by pk_act (geometry.py:198-199),
+ * rotations left-composed and canonicalised (geometry.py:39-50, 71-84), scales times the
+ * pose scale, opacity/colour copied.  float64 arithmetic in the reference's order, rounded
+ * to float32 once.
+ */
+int s2d_transform_surfels(void *stream, const double pose[8], const float *params_in, int64_t n,
+                          float *params_out);
+
+/*
+ * fuse's accumulation gate (mapper.py:212-224): keep[i] = 1 when candidate i (camera-frame
+ * packed block, device) falls outside the image or its own pixel round(f x / z + c) of the
+ * map's rendered accumulation (H, W) is below accum_threshold.
+ */
+int s2d_fuse_gate(void *stream, const float *accumulation, const s2d_camera *cam, const float *params,
+                  int64_t n, double accum_threshold, uint8_t *keep);
+
+/*
+ * prune's error mask (mapper.py:246-253) over npx pixels: marked = accumulation > 0.5 and
+ * (max_c |color - observed_rgb| > rgb_error or (observed_depth > 0 and
+ * |depth / max(accumulation, 1e-12) - observed_depth| > depth_error_frac * observed_depth)).
+ */
+int s2d_prune_mark(void *stream, const float *color, const float *depth, const float *accumulation,
+                   const float *observed_rgb, const float *observed_depth, int64_t npx, double rgb_error,
+                   double depth_error_frac, uint8_t *marked);
+
+/* prune's victim test (mapper.py:255-256): keep[i] = !(max_marked[i] > contribution_floor). */
+int s2d_prune_keep(void *stream, const float *max_marked, int64_t n, double contribution_floor,
+                   uint8_t *keep);
+
 #ifdef __cplusplus
 }
 #endif

@@ -23,7 +23,8 @@ _lib = None
 __all__ = [
     "build_oracle", "load", "pose_inverse", "project", "depth_order", "tile_lists",
     "render", "loss_seeds", "backward", "loss_and_grads", "max_blend_weights",
-    "adam_step", "DEFAULTS",
+    "adam_step", "DEFAULTS", "quat_mul", "quat_canonicalize", "transform_surfels", "fuse_gate", "fuse",
+    "prune_mark", "prune",
 ]
 
 DEFAULTS = SimpleNamespace(weight_clamp=0.999, termination_transmittance=1e-4, footprint_sigma=3.0,
@@ -310,3 +311,80 @@ def adam_step(params, grads, m1, m2, step, lr_means=1e-3, lr_rest=5e-3, b1=0.9, 
     L.o_adam_step(ctypes.c_int64(n), _p(params), _p(grads), _p(m1), _p(m2), ctypes.c_int64(step),
                   ctypes.c_double(lr_means), ctypes.c_double(lr_rest), ctypes.c_double(b1),
                   ctypes.c_double(b2), ctypes.c_double(eps), ctypes.c_double(scale_min), _p(mk))
+
+
+# ---------------------------------------------------------------- map maintenance (§8(f) 2-3)
+# numpy float64 restatements; each elementwise expression keeps the reference's association.
+
+def quat_mul(q1, q2):
+    """geometry.py:39-50"""
+    w1, x1, y1, z1 = q1[..., 0], q1[..., 1], q1[..., 2], q1[..., 3]
+    w2, x2, y2, z2 = q2[..., 0], q2[..., 1], q2[..., 2], q2[..., 3]
+    return np.stack([w1 * w2 - x1 * x2 - y1 * y2 - z1 * z2,
+                     w1 * x2 + x1 * w2 + y1 * z2 - z1 * y2,
+                     w1 * y2 - x1 * z2 + y1 * w2 + z1 * x2,
+                     w1 * z2 + x1 * y2 - y1 * x2 + z1 * w2], axis=-1)
+
+
+def quat_canonicalize(q):
+    """geometry.py:71-84: w >= 0, ties on the first non-zero vector component, no -0.0."""
+    q = np.asarray(q, dtype=float)
+    w, x, y, z = q[..., 0], q[..., 1], q[..., 2], q[..., 3]
+    flip = (w < 0) | ((w == 0) & ((x < 0) | ((x == 0) & ((y < 0) | ((y == 0) & (z < 0))))))
+    return np.where(flip[..., None], -q, q) + 0.0
+
+
+def transform_surfels(means, quats, scales, pose):
+    """mapper.py:184-197 on the geometric fields -> (means, quats, scales); pose packed Sim(3)."""
+    a = _packed(pose)
+    m = a[0] * _qrot(np.broadcast_to(a[4:8], (len(means), 4)), np.asarray(means, float)) + a[1:4]
+    q = quat_canonicalize(quat_mul(a[4:8][None, :], np.asarray(quats, float)))
+    return m, q, a[0] * np.asarray(scales, float)
+
+
+def fuse_gate(accumulation, cand_means, intr, accum_threshold=0.5):
+    """mapper.py:215-224: keep flags of camera-frame candidates (map non-empty)."""
+    cm = np.asarray(cand_means, float)
+    z = cm[:, 2]
+    with np.errstate(divide="ignore", invalid="ignore"):
+        px = np.round(intr.fx * cm[:, 0] / z + intr.cx).astype(int)
+        py = np.round(intr.fy * cm[:, 1] / z + intr.cy).astype(int)
+    inside = (px >= 0) & (px < intr.width) & (py >= 0) & (py < intr.height) & (z > 0)
+    acc = np.zeros(len(cm))
+    acc[inside] = np.asarray(accumulation)[py[inside], px[inside]]
+    return acc < accum_threshold
+
+
+def fuse(map_surfels, cand, pose, intr, accum_threshold=0.5, cfg=None):
+    """mapper.py:200-230 -> (keep flags, world means, quats, scales of the kept candidates)."""
+    n_map = len(np.asarray(map_surfels.means).reshape(-1, 3))
+    if n_map == 0:
+        keep = np.ones(len(cand.means), bool)
+    else:
+        buf = render(map_surfels, pose, intr, cfg, with_normal=False)
+        keep = fuse_gate(buf.accumulation, cand.means, intr, accum_threshold)
+    m, q, s = transform_surfels(np.asarray(cand.means)[keep], np.asarray(cand.quats)[keep],
+                                np.asarray(cand.scales)[keep], pose)
+    return keep, m, q, s
+
+
+def prune_mark(color, depth, accumulation, observed_rgb, observed_depth, rgb_error=0.2, depth_error_frac=0.10):
+    """mapper.py:246-253"""
+    covered = accumulation > 0.5
+    rgb_err = np.max(np.abs(color - observed_rgb), axis=2) > rgb_error
+    depth_norm = depth / np.maximum(accumulation, 1e-12)
+    obs = np.asarray(observed_depth, dtype=float)
+    depth_err = (obs > 0) & (np.abs(depth_norm - obs) > depth_error_frac * obs)
+    return covered & (rgb_err | depth_err)
+
+
+def prune(map_surfels, pose, intr, observed_rgb, observed_depth, rgb_error=0.2, depth_error_frac=0.10,
+          contribution_floor=0.1, cfg=None):
+    """mapper.py:238-260 -> (victim indices, marked pixel mask)."""
+    buf = render(map_surfels, pose, intr, cfg, with_normal=False)
+    marked = prune_mark(buf.color, buf.depth, buf.accumulation, observed_rgb, observed_depth, rgb_error,
+                        depth_error_frac)
+    if not marked.any():
+        return np.zeros(0, np.int64), marked
+    _, max_marked = max_blend_weights(map_surfels, pose, intr, marked, cfg)
+    return np.flatnonzero(max_marked > contribution_floor), marked

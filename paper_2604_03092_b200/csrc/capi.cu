@@ -714,4 +714,56 @@ int s2d_render_host(s2d_view *v, const double *means, const double *quats, const
     return S2D_OK;
 }
 
+int s2d_transform_surfels(void *stream, const double pose[8], const float *params_in, int64_t n,
+                          float *params_out) {
+    if (!pose) return fail(S2D_ERR_INVALID, "pose is NULL");
+    if (n < 0) return fail(S2D_ERR_INVALID, "negative n");
+    if (!(pose[0] > 0) || !std::isfinite(pose[0])) return fail(S2D_ERR_INVALID, "pose scale must be positive");
+    if (n == 0) return S2D_OK;
+    if (!params_in || !params_out) return fail(S2D_ERR_INVALID, "NULL buffer");
+    if (params_in == params_out) return fail(S2D_ERR_INVALID, "params_in and params_out must not alias");
+    launch_transform(params_in, params_out, n, pose, (cudaStream_t)stream);
+    S2D_CHECK_LAUNCH();
+    return S2D_OK;
+}
+
+int s2d_fuse_gate(void *stream, const float *accumulation, const s2d_camera *cam, const float *params, int64_t n,
+                  double accum_threshold, uint8_t *keep) {
+    int rc = validate_camera(cam);
+    if (rc) return rc;
+    if (n < 0) return fail(S2D_ERR_INVALID, "negative n");
+    if (!(accum_threshold > 0.0 && accum_threshold < 1.0))
+        return fail(S2D_ERR_INVALID, "accum_threshold must be in (0, 1)");  // FusionConfig (mapper.py:57-58)
+    if (n == 0) return S2D_OK;
+    if (!accumulation || !params || !keep) return fail(S2D_ERR_INVALID, "NULL buffer");
+    launch_fuse_gate(accumulation, *cam, params, n, accum_threshold, keep, (cudaStream_t)stream);
+    S2D_CHECK_LAUNCH();
+    return S2D_OK;
+}
+
+int s2d_prune_mark(void *stream, const float *color, const float *depth, const float *accumulation,
+                   const float *observed_rgb, const float *observed_depth, int64_t npx, double rgb_error,
+                   double depth_error_frac, uint8_t *marked) {
+    if (npx < 0) return fail(S2D_ERR_INVALID, "negative pixel count");
+    if (!(rgb_error > 0.0) || !(depth_error_frac > 0.0))
+        return fail(S2D_ERR_INVALID, "prune thresholds must be positive");  // FusionConfig (mapper.py:59-61)
+    if (npx == 0) return S2D_OK;
+    if (!color || !depth || !accumulation || !observed_rgb || !observed_depth || !marked)
+        return fail(S2D_ERR_INVALID, "NULL buffer");
+    launch_prune_mark(color, depth, accumulation, observed_rgb, observed_depth, npx, rgb_error, depth_error_frac,
+                      marked, (cudaStream_t)stream);
+    S2D_CHECK_LAUNCH();
+    return S2D_OK;
+}
+
+int s2d_prune_keep(void *stream, const float *max_marked, int64_t n, double contribution_floor, uint8_t *keep) {
+    if (n < 0) return fail(S2D_ERR_INVALID, "negative n");
+    if (!(contribution_floor > 0.0)) return fail(S2D_ERR_INVALID, "prune thresholds must be positive");
+    if (n == 0) return S2D_OK;
+    if (!max_marked || !keep) return fail(S2D_ERR_INVALID, "NULL buffer");
+    launch_prune_keep(max_marked, n, contribution_floor, keep, (cudaStream_t)stream);
+    S2D_CHECK_LAUNCH();
+    return S2D_OK;
+}
+
 }  // extern "C"

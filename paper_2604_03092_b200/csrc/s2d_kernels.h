@@ -126,6 +126,15 @@ void launch_project_backward(const ProjectBwdArgs &a, cudaStream_t s);
 void launch_adam(float *params, const float *grads, float *m1, float *m2, int64_t n, int64_t step,
                  const s2d_adam_config &cfg, const uint8_t *mask, cudaStream_t s);
 
+// map maintenance (map.cu)
+void launch_transform(const float *in, float *out, int64_t n, const double pose[8], cudaStream_t s);
+void launch_fuse_gate(const float *acc, const s2d_camera &cam, const float *params, int64_t n, double thr,
+                      uint8_t *keep, cudaStream_t s);
+void launch_prune_mark(const float *color, const float *depth, const float *acc, const float *orgb,
+                       const float *odep, int64_t npx, double rgb_err, double depth_frac, uint8_t *marked,
+                       cudaStream_t s);
+void launch_prune_keep(const float *max_marked, int64_t n, double floor_, uint8_t *keep, cudaStream_t s);
+
 // number of 8-bit digit passes needed for keys < 2^bits
 inline int passes_for_bits(int bits) { return bits <= 0 ? 1 : (bits + kRadixBits - 1) / kRadixBits; }
 

@@ -6,6 +6,9 @@
   warm-started step; the summed loss never increases.  The map stays resident
   on the device for the whole call; every trial is V x (forward + backward)
   through the fused kernels.
+* :func:`transform_surfels`, :func:`fuse`, :func:`prune` — drop-ins for the map
+  maintenance around refinement (mapper.py:184-260): the map is rendered on the GPU
+  and the per-candidate / per-pixel / per-surfel decisions run in the map.cu kernels.
 * :class:`AdamRefiner` — the multi-view refinement of BASELINE configs 4-5:
   every iteration renders this rank's views forward+backward (L1 RGB + depth),
   all-reduces the packed 13N gradient block over NCCL, and applies the fused
@@ -14,6 +17,7 @@
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass, field
 
@@ -28,8 +32,8 @@ from .geometry import as_packed_pose
 from .rasterizer import (DEFAULT_RASTER_CONFIG, CameraIntrinsics, LossWeights, RasterConfig, SurfelArrays,
                          loss_struct)
 
-__all__ = ["RefinementConfig", "RefinementReport", "GlobalSurfelMap", "refine", "psnr", "AdamConfig",
-           "ViewLoss", "AdamRefiner"]
+__all__ = ["FusionConfig", "RefinementConfig", "RefinementReport", "GlobalSurfelMap", "transform_surfels",
+           "fuse", "prune", "refine", "psnr", "AdamConfig", "ViewLoss", "AdamRefiner"]
 
 PSNR_EXACT = float("inf")
 
@@ -44,6 +48,22 @@ def psnr(rendered, target) -> float:
     if mse == 0.0:
         return PSNR_EXACT
     return 10.0 * math.log10(1.0 / mse)
+
+
+@dataclass(frozen=True)
+class FusionConfig:
+    """mapper.py:53-62"""
+
+    accum_threshold: float = 0.5
+    prune_rgb_error: float = 0.2
+    prune_depth_error_frac: float = 0.10
+    prune_contribution_floor: float = 0.1
+
+    def __post_init__(self):
+        if not 0 < self.accum_threshold < 1:
+            raise ValueError("accum_threshold must be in (0, 1)")
+        if min(self.prune_rgb_error, self.prune_depth_error_frac, self.prune_contribution_floor) <= 0:
+            raise ValueError("prune thresholds must be positive")
 
 
 @dataclass(frozen=True)
@@ -76,6 +96,128 @@ class GlobalSurfelMap:
 
     def __len__(self):
         return len(self.surfels)
+
+    @property
+    def keyframe_index(self):
+        """keyframe_id -> surfel indices; covers every surfel exactly once."""
+        out = {}
+        for i, kf in enumerate(np.asarray(self.surfels.keyframe_ids)):
+            out.setdefault(int(kf), []).append(i)
+        return out
+
+    def insert(self, new: SurfelArrays):
+        unknown = set(np.unique(np.asarray(new.keyframe_ids)).tolist()) - set(self.keyframe_poses)
+        if unknown:
+            raise KeyError(f"surfels bound to unregistered keyframes {sorted(unknown)}")
+        self.surfels = SurfelArrays.concatenate([self.surfels, new])
+
+    def remove(self, indices):
+        keep = np.ones(len(self.surfels), dtype=bool)
+        keep[np.asarray(indices, dtype=int)] = False
+        self.surfels = self.surfels.select(keep)
+
+    def copy(self) -> "GlobalSurfelMap":
+        return GlobalSurfelMap(self.surfels.copy(), dict(self.keyframe_poses))
+
+
+# --------------------------------------------------------------------------- map maintenance
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _host_block(t: torch.Tensor, n: int) -> dict:
+    return {k: v.double().cpu().numpy() for k, v in unpack_params(t, n).items()}
+
+
+def transform_surfels(surfels: SurfelArrays, t) -> SurfelArrays:
+    """Camera->world per the node pose (mapper.py:184-197): means by the Sim(3) action,
+    rotations left-composed and canonicalised, tangent scales times the pose scale.
+    Computed by k_transform (float64 in the reference's order, float32 result)."""
+    arrays = SurfelArrays.from_surfels(surfels)
+    n = len(arrays)
+    if n == 0:
+        return arrays.copy()
+    ctx = DeviceContext.get()
+    pin = pack_params(arrays, ctx.device)
+    out = torch.empty_like(pin)
+    N.check(N.lib().s2d_transform_surfels(_stream(), N.as_doubles(as_packed_pose(t)), N.dptr(pin), n,
+                                          N.dptr(out)), "s2d_transform_surfels")
+    P = _host_block(out, n)
+    return SurfelArrays(P["means"], P["quats"], P["scales"], P["opacities"], P["colors"],
+                        np.array(arrays.confidences, copy=True), np.array(arrays.keyframe_ids, copy=True),
+                        np.array(arrays.submap_ids, copy=True))
+
+
+def fuse(map_: GlobalSurfelMap, new_surfels: SurfelArrays, keyframe_id: int, pose, intr: CameraIntrinsics,
+         cfg: FusionConfig = FusionConfig(), raster_cfg: RasterConfig = DEFAULT_RASTER_CONFIG,
+         submap_id: int = -1) -> dict:
+    """Insert camera-frame surfels where the map's accumulation is still low (mapper.py:200-230).
+
+    The map's accumulation is rendered on the GPU from the keyframe pose; k_fuse_gate looks
+    up each candidate's own pixel; the kept candidates are warped to the world frame by
+    k_transform and appended."""
+    if keyframe_id not in map_.keyframe_poses:
+        map_.keyframe_poses[keyframe_id] = pose
+    cand = SurfelArrays.from_surfels(new_surfels)
+    n_cand = len(cand)
+    if n_cand == 0:
+        return {"candidates": 0, "inserted": 0}
+    ctx = DeviceContext.get()
+    dev = ctx.device
+    cp = pack_params(cand, dev)
+    if len(map_) == 0:
+        keep = np.ones(n_cand, dtype=bool)
+    else:
+        from .rasterizer import _device_render
+        _, _, img, _, _, _ = _device_render(map_.surfels, pose, intr, raster_cfg, normal=False)
+        keep_t = torch.empty(n_cand, dtype=torch.uint8, device=dev)
+        N.check(N.lib().s2d_fuse_gate(_stream(), N.dptr(img.accumulation), ctypes.byref(camera_struct(intr)),
+                                      N.dptr(cp), n_cand, float(cfg.accum_threshold), N.dptr(keep_t)),
+                "s2d_fuse_gate")
+        keep = keep_t.cpu().numpy().astype(bool)
+    world = transform_surfels(cand.select(keep), pose)
+    world.keyframe_ids = np.full(len(world), keyframe_id, np.int64)
+    world.submap_ids = np.full(len(world), submap_id, np.int64)
+    map_.insert(world)
+    return {"candidates": n_cand, "inserted": int(keep.sum())}
+
+
+def prune(map_: GlobalSurfelMap, keyframe_id: int, observed_rgb, observed_depth, intr: CameraIntrinsics,
+          cfg: FusionConfig = FusionConfig(), raster_cfg: RasterConfig = DEFAULT_RASTER_CONFIG) -> int:
+    """Remove surfels that contribute to pixels with large reconstruction error (mapper.py:238-260).
+
+    Render (GPU), k_prune_mark over the pixels, the forward's per-surfel max weight over
+    the marked pixels, k_prune_keep; the victims are removed from the map."""
+    if len(map_) == 0:
+        return 0
+    pose = map_.keyframe_poses[keyframe_id]
+    from .rasterizer import _device_render
+    arrays, params, img, _, view, _ = _device_render(map_.surfels, pose, intr, raster_cfg, normal=False)
+    dev = params.device
+    n = len(arrays)
+    orgb = torch.from_numpy(np.ascontiguousarray(np.asarray(observed_rgb, dtype=np.float32))).to(dev)
+    odep = torch.from_numpy(np.ascontiguousarray(np.asarray(observed_depth, dtype=np.float32))).to(dev)
+    if orgb.shape != (intr.height, intr.width, 3) or odep.shape != (intr.height, intr.width):
+        raise ValueError("observation dimensions do not match the camera")
+    npx = intr.width * intr.height
+    marked = torch.empty((intr.height, intr.width), dtype=torch.uint8, device=dev)
+    N.check(N.lib().s2d_prune_mark(_stream(), N.dptr(img.color), N.dptr(img.depth), N.dptr(img.accumulation),
+                                   N.dptr(orgb), N.dptr(odep), npx, float(cfg.prune_rgb_error),
+                                   float(cfg.prune_depth_error_frac), N.dptr(marked)), "s2d_prune_mark")
+    if not bool(marked.any()):
+        return 0
+    max_all = torch.zeros(n, device=dev)
+    max_marked = torch.zeros(n, device=dev)
+    forward_checked(view, params, n, as_packed_pose(pose), camera_struct(intr), config_struct(raster_cfg), img,
+                    max_all, max_marked, marked)
+    keep = torch.empty(n, dtype=torch.uint8, device=dev)
+    N.check(N.lib().s2d_prune_keep(_stream(), N.dptr(max_marked), n, float(cfg.prune_contribution_floor),
+                                   N.dptr(keep)), "s2d_prune_keep")
+    victims = np.flatnonzero(keep.cpu().numpy() == 0)
+    if len(victims):
+        map_.remove(victims)
+    return int(len(victims))
 
 
 class _ViewSet:

@@ -126,7 +126,94 @@ def kat_scenes():
     return intr, {"kat_two": two, "kat_edge": edge, "kat_occluder": occl, "kat_random40": rnd}
 
 
+def capture_map_ops():
+    """transform_surfels / fuse / prune (mapper.py:184-260) and the surfel PLY writer (io.py:118-150)
+    of the reference on seeded inputs (float32-representable, so the GPU sees the same values)."""
+    from surfelslam import mapper as M
+    from surfelslam import io as RIO
+    f = scenes.f32
+    rng = np.random.default_rng(31)
+    out = {}
+    # transform_surfels on random surfels; a Sim(3) with scale, rotation and translation
+    s = scenes.random_surfels(rng, 500)
+    arr = ref_arrays(s)
+    t = Sim3Transform(1.3, UnitQuaternion.from_axis_angle([0.2, -1.0, 0.4], 0.9), np.array([0.5, -0.25, 1.5]))
+    w = M.transform_surfels(arr, t)
+    out.update(tr_means=arr.means, tr_quats=arr.quats, tr_scales=arr.scales, tr_pose=t.packed(),
+               tr_out_means=w.means, tr_out_quats=w.quats, tr_out_scales=w.scales)
+    # fuse: a map (config-1 cloud bound to keyframe 0 at pose p0) and camera-frame candidates from
+    # keyframe 1 at pose p1
+    c1 = scenes.config1(0)
+    intr = ref_intr(c1.intr)
+    p0 = Sim3Transform(1.0, UnitQuaternion.from_axis_angle([0, 1, 0], 0.05), np.array([0.05, 0.0, 0.0]))
+    p1 = Sim3Transform(1.0, UnitQuaternion.from_axis_angle([1, 0, 0.3], 0.08), np.array([-0.1, 0.05, 0.1]))
+    m = M.GlobalSurfelMap()
+    map_arr = ref_arrays(c1.surfels)
+    M.fuse(m, map_arr, 0, p0, intr)                       # empty map: everything inserted
+    # round the world map to float32 so both sides render the very same map
+    for fld in ("means", "quats", "scales", "opacities", "colors"):
+        setattr(m.surfels, fld, f(getattr(m.surfels, fld)))
+    cand = ref_arrays(scenes.random_surfels(np.random.default_rng(32), 1500))
+    m_before = m.surfels.copy()
+    stats = M.fuse(m, cand, 1, p1, intr)
+    n0 = len(m_before.means)
+    out.update(fu_intr=np.array([intr.fx, intr.fy, intr.cx, intr.cy, intr.width, intr.height], float),
+               fu_map_means=m_before.means, fu_map_quats=m_before.quats, fu_map_scales=m_before.scales,
+               fu_map_opacities=m_before.opacities, fu_map_colors=m_before.colors,
+               fu_p1=p1.packed(), fu_cand_means=cand.means, fu_cand_quats=cand.quats, fu_cand_scales=cand.scales,
+               fu_cand_opacities=cand.opacities, fu_cand_colors=cand.colors,
+               fu_inserted=np.int64(stats["inserted"]), fu_new_means=m.surfels.means[n0:],
+               fu_new_quats=m.surfels.quats[n0:], fu_new_scales=m.surfels.scales[n0:],
+               fu_new_kf=m.surfels.keyframe_ids[n0:],
+               fu_acc=R.render(m_before, p1, intr).accumulation)
+    # prune: observations = the map's own render at keyframe 0 with a corrupted block
+    for fld in ("means", "quats", "scales", "opacities", "colors"):
+        setattr(m.surfels, fld, f(getattr(m.surfels, fld)))
+    buf = R.render(m.surfels, m.keyframe_poses[0], intr)
+    orgb = f(buf.color.copy())
+    odep = f(buf.depth / np.maximum(buf.accumulation, 1e-12))
+    orgb[30:60, 40:90] = f(np.clip(1.0 - orgb[30:60, 40:90], 0, 1))
+    odep[10:25, 10:50] *= np.float32(1.5)
+    m_pr = m.copy()
+    victims_n = M.prune(m_pr, 0, orgb, odep, intr)
+    keep = np.ones(len(m.surfels.means), bool)
+    # victims as indices: the surfels missing from the pruned map (prune keeps order)
+    cfg = M.FusionConfig()
+    covered = buf.accumulation > 0.5
+    rgb_err = np.max(np.abs(buf.color - orgb), axis=2) > cfg.prune_rgb_error
+    dn = buf.depth / np.maximum(buf.accumulation, 1e-12)
+    depth_err = (odep > 0) & (np.abs(dn - odep) > cfg.prune_depth_error_frac * odep)
+    marked = covered & (rgb_err | depth_err)
+    _, mm = R.per_surfel_max_weight(m.surfels, m.keyframe_poses[0], intr, marked)
+    victims = np.flatnonzero(mm > cfg.prune_contribution_floor)
+    keep[victims] = False
+    assert victims_n == len(victims) and np.array_equal(m_pr.surfels.means, m.surfels.means[keep])
+    out.update(pr_map_means=m.surfels.means, pr_map_quats=m.surfels.quats, pr_map_scales=m.surfels.scales,
+               pr_map_opacities=m.surfels.opacities, pr_map_colors=m.surfels.colors, pr_p0=p0.packed(),
+               pr_obs_rgb=orgb, pr_obs_depth=odep, pr_marked=marked, pr_victims=victims, pr_max_marked=mm)
+    # surfel PLY bytes written by the reference
+    import tempfile
+    small = m.surfels.select(np.arange(20))
+    small.confidences = np.linspace(0.1, 1.0, 20)
+    small.submap_ids = np.arange(20, dtype=np.int64) % 3
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "s.ply")
+        RIO.write_surfel_ply(path, small)
+        with open(path, "rb") as fh:
+            ply = np.frombuffer(fh.read(), np.uint8)
+    out.update(ply_bytes=ply, ply_means=small.means, ply_quats=small.quats, ply_scales=small.scales,
+               ply_opacities=small.opacities, ply_colors=small.colors, ply_conf=small.confidences,
+               ply_kf=small.keyframe_ids, ply_submap=small.submap_ids)
+    path = os.path.join(HERE, "map_ops.npz")
+    np.savez_compressed(path, **out)
+    print(f"map_ops: inserted {stats['inserted']}/{len(cand.means)}, victims {len(victims)}, "
+          f"marked px {int(marked.sum())} -> {os.path.getsize(path) / 1e3:.0f} kB")
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "map_ops":
+        capture_map_ops()
+        return
     exact = R.RasterConfig(weight_clamp=1.0)
     intr, kats = kat_scenes()
     ident = SE3Pose.identity()
@@ -143,6 +230,7 @@ def main():
     # config 2: binning pins at scale, images stored float32
     c2 = scenes.config2(0)
     capture("c2", c2.surfels, ident, c2.intr, images_f32=True, grads=False)
+    capture_map_ops()
 
 
 if __name__ == "__main__":
