@@ -124,16 +124,31 @@ def render_targets(sc, device):
     return rgbs, deps
 
 
-# algorithmic bytes per launch of each phase
-def phase_bytes(n, v, p, x):
+# algorithmic bytes per launch of each phase (DESIGN.md "Kernels, their bound and algorithmic
+# bytes"): every logical tensor access counted once.  n surfels, v visible, p (tile, surfel)
+# pairs, e blend-stream entries ((pair, 8x4 block) with >= 1 blended pixel), x pixels.
+def phase_bytes(n, v, p, x, e):
     return {
-        "project": 52 * n + n + 88 * v,                       # params in; flags, record 64, rect 8, z64 8, key/val 8
-        "depth_sort": 4 * v + 4 * 16 * v + 12 * v,            # hist read + 4 passes x (r+w keys+vals) + tie fix
-        "tile_bin": 12 * v + 8 * p + 2 * 16 * p + 4 * p,      # order+rect in, pairs out, 2 sort passes, ranges
-        "raster_fwd": 4 * p + 72 * p + 28 * x,                # ids + (record, rect) per pair; rgb, depth, acc, aux out
-        "raster_bwd": 4 * p + 72 * p + 44 * x + 64 * v,       # ids + records; pixel outputs/aux/targets; 2D grads
-        "project_bwd": n + 64 * v + 52 * v + 104 * v + 64 * v,  # flags; 2D grads in; params in; grads r+w; zero
+        "project": 52 * n + n + 8 * n + 120 * v,   # params in; flags, keys/vals out; record 64, exact 40, rect 8, z64 8
+        "depth_sort": 12 * n + 52 * v,              # hist over n keys, 3 stable passes (first one compacts), tie fix
+        "tile_bin": 12 * v + 44 * p,                # order+rect in; pairs out; 2 stable passes; tile ranges
+        "raster_fwd": 72 * p + 16 * e + 28 * x,     # key+id+record per pair; blend stream out; rgb, depth, acc, aux out
+        "raster_bwd": 16 * e + 64 * p + 40 * x + 40 * v,  # stream + records; aux, render, targets; 2D gradients
+        "project_bwd": n + 260 * v,                 # flags; 2D grads in + zeroed; params in; gradients r+w
     }
+
+
+def load_traffic():
+    """Per-launch DRAM bytes of each kernel from the committed ncu --set full capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+KERNEL_OF_PHASE = {"raster_fwd": "k_raster_fwd", "raster_bwd": "k_raster_bwd", "project": "k_project",
+                   "project_bwd": "k_project_bwd"}
 
 
 def run_cpu_port(sc, targets, views, threads):
@@ -260,8 +275,8 @@ def main():
     st = ref.view.stats()
     nfw = max(ph["n_forward"], 1)
     per_launch_ms = {k: ph[k] / nfw for k in ref.view.PHASES}
-    nvis, npairs = st.visible, st.pairs
-    pb = phase_bytes(ref.n, nvis, npairs, px)
+    nvis, npairs, nblend = st.visible, st.pairs, st.blended
+    pb = phase_bytes(ref.n, nvis, npairs, px, nblend)
     peaks = {}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -272,7 +287,15 @@ def main():
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
     dom = max(per_launch_ms, key=per_launch_ms.get)
     achieved = pb[dom] / (per_launch_ms[dom] * 1e-3) / 1e9
-    view_bytes = 104 * ref.n + 312 * nvis + 180 * npairs + 88 * px
+    traffic_src = load_traffic()
+    traffic = None
+    issue = None
+    if traffic_src and KERNEL_OF_PHASE.get(dom) in traffic_src.get("per_launch", {}):
+        kt = traffic_src["per_launch"][KERNEL_OF_PHASE[dom]]
+        traffic = kt.get("dram_bytes")
+        issue = {"issue_active_pct": kt.get("issue_active_pct"), "warp_instructions": kt.get("warp_instructions"),
+                 "source": traffic_src.get("source")}
+    view_bytes = 104 * ref.n + 312 * nvis + 180 * npairs + 88 * px  # SURVEY.md §8(d) model
     view_ms = sum(per_launch_ms.values())
     phases = {k: {"ms": round(per_launch_ms[k], 4), "gbs": round(pb[k] / (per_launch_ms[k] * 1e-3) / 1e9, 1)
                   if per_launch_ms[k] > 0 else None} for k in per_launch_ms}
@@ -323,15 +346,15 @@ def main():
                        "views": n_views, "image": [sc.intr.width, sc.intr.height],
                        "parallelism": f"view-sharded dp{world}",
                        "l2": "working set per step > L2 (params+grads+moments 208 MB, targets 157 MB)",
-                       "visible_last_view": nvis, "pairs_last_view": npairs},
+                       "visible_last_view": nvis, "pairs_last_view": npairs, "blend_entries_last_view": nblend},
             "refine_iters_per_s": round(1000.0 / ms_step, 3),
             "fwd_bwd_mpix_per_s_per_view": round(px / (view_ms * 1e-3) / 1e6, 2) if view_ms > 0 else None,
             "views_in_flight": inflight,
             "loss_first_last": [losses[0], losses[-1]],
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm,
-                         "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": None,
+                         "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": traffic,
                          "peak_source": peak_src, "algorithmic_bytes_per_launch": pb[dom],
-                         "launch_ms": round(per_launch_ms[dom], 4)},
+                         "launch_ms": round(per_launch_ms[dom], 4), "sm_issue": issue},
             "roofline_view": {"bytes": view_bytes, "ms": round(view_ms, 4),
                               "achieved_gbs": round(view_bytes / (view_ms * 1e-3) / 1e9, 1) if view_ms > 0 else None,
                               "frac": round(view_bytes / (view_ms * 1e-3) / 1e9 / hbm, 4) if view_ms > 0 else None},

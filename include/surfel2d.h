@@ -77,7 +77,7 @@ typedef struct s2d_view_stats {
     int32_t overflow;    /* pair capacity exceeded (view must be re-run; handled internally) */
     int32_t guard_hits;  /* float64 re-checks taken at the 3-sigma cut / weight clamp */
     int32_t pairs_stored; /* min(pairs, capacity) (internal) */
-    int32_t pad;
+    int32_t blended;     /* E: (pair, 8x4 pixel block) entries with >= 1 blended pixel (backward work) */
 } s2d_view_stats;
 
 /* Introspection of the last forward of a view (device pointers; parity tests). */

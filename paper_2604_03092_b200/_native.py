@@ -54,7 +54,7 @@ class ViewStats(ctypes.Structure):
     _fields_ = [("visible", ctypes.c_int32), ("pairs", ctypes.c_int32),
                 ("degenerate", ctypes.c_int32), ("n_mask", ctypes.c_int32),
                 ("overflow", ctypes.c_int32), ("guard_hits", ctypes.c_int32),
-                ("pairs_stored", ctypes.c_int32), ("pad", ctypes.c_int32)]
+                ("pairs_stored", ctypes.c_int32), ("blended", ctypes.c_int32)]
 
 
 class ViewDebug(ctypes.Structure):

@@ -165,6 +165,7 @@ __global__ void k_stats_accumulate(const s2d_view_stats *s, s2d_view_stats *acc)
     atomicAdd(&acc->n_mask, s->n_mask);
     atomicAdd(&acc->guard_hits, s->guard_hits);
     atomicOr(&acc->overflow, s->overflow);
+    atomicMax(&acc->blended, s->blended);
 }
 
 }  // namespace

@@ -309,7 +309,10 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
         }
         cp_wait<0>();
     }
-    if (lane == 0) a.bcount[8 * tile + warp] = wc;
+    if (lane == 0) {
+        a.bcount[8 * tile + warp] = wc;
+        if (wc) atomicAdd(&a.stats->blended, wc);
+    }
     if (inside) {
         const int p = py * P.W + px;
         if (a.color) {
