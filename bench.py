@@ -34,6 +34,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = "2DGS fwd+bwd Mpix/s at 1M surfels; refine iters/s at 1/2/4/8 GPU"
 WORKLOAD = "config4: 1,000,000 surfels, 32 views 640x480 fx=fy=500, L1 RGB + 0.1 L1 depth, Adam"
+WORKLOAD5 = ("config5: 4,000,000 surfels in 16 rooms, 128 views 1296x968 fx=fy=1000, per-view exposure gain on the "
+             "targets, L1 RGB + 0.1 L1 depth, Adam")
 
 
 def parse():
@@ -46,6 +48,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-views", type=int, default=0, help="views in the CPU baseline sample (0 = auto)")
     ap.add_argument("--small", action="store_true", help="reduced workload for quick checks (not a bench value)")
+    ap.add_argument("--config", type=int, default=4, choices=[4, 5],
+                    help="BASELINE config: 4 (the headline workload) or 5 (4M surfels, 128 views 1296x968)")
     return ap.parse_args()
 
 
@@ -94,9 +98,11 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def make_workload(seed, small=False):
+def make_workload(seed, small=False, config=4):
     import numpy as np
     from paper_2604_03092_b200 import scenes
+    if config == 5:
+        return scenes.config5(seed)
     if small:
         sc = scenes.config4(seed, n_keyframes=2, per_keyframe=50_000, n_views=8)
     else:
@@ -115,10 +121,12 @@ def render_targets(sc, device):
     params = pack_params(sc.surfels, ctx.device)
     cam, cfg = camera_struct(sc.intr), config_struct(DEFAULT_RASTER_CONFIG)
     rgbs, deps = [], []
-    for pose in sc.poses:
+    gains = getattr(sc, "gains", None)
+    for v, pose in enumerate(sc.poses):
         img = ImageBuffers.allocate(sc.intr.height, sc.intr.width, ctx.device, normal=False)
         forward_checked(view, params, len(sc.surfels), pose, cam, cfg, img)
-        rgbs.append(img.color.clone())
+        # config 5: per-view exposure gain on the targets (BASELINE.json configs[4])
+        rgbs.append(img.color.clone() * float(gains[v]) if gains is not None else img.color.clone())
         deps.append(img.depth.clone())
     del params, view
     return rgbs, deps
@@ -219,7 +227,7 @@ def main():
     rank, world = init_from_env("nccl") if args.gpus > 1 else (0, 1)
     dev = torch.device("cuda", local_rank)
 
-    sc = make_workload(args.seed, args.small)
+    sc = make_workload(args.seed, args.small, args.config)
     rgbs, deps = render_targets(sc, dev)
     n_views = len(sc.poses)
     px = sc.intr.width * sc.intr.height
@@ -342,7 +350,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded config-4 generator; targets = renders of the unperturbed map)",
-            "config": {"workload": WORKLOAD + (" [SMALL]" if args.small else ""), "surfels": ref_n(sc),
+            "config": {"workload": (WORKLOAD if args.config == 4 else WORKLOAD5) + (" [SMALL]" if args.small else ""),
+                       "surfels": ref_n(sc),
                        "views": n_views, "image": [sc.intr.width, sc.intr.height],
                        "parallelism": f"view-sharded dp{world}",
                        "l2": "working set per step > L2 (params+grads+moments 208 MB, targets 157 MB)",

@@ -7,7 +7,7 @@ from paper_2604_03092_b200.mapper import AdamRefiner, ViewLoss, AdamConfig
 import bench
 
 nviews = int(os.environ.get("PROFILE_VIEWS", "4"))
-sc = scenes.config4(0)
+sc = scenes.config5(0) if os.environ.get("PROFILE_CONFIG", "4") == "5" else scenes.config4(0)
 sc.poses = sc.poses[12:12 + nviews]
 rgbs, deps = bench.render_targets(sc, torch.device("cuda", 0))
 ref = AdamRefiner(sc.extra["perturbed"], sc.intr, sc.poses, rgbs, deps, ViewLoss(), AdamConfig())
