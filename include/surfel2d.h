@@ -56,7 +56,18 @@ typedef struct s2d_raster_config {
     double max_condition;             /* 1e8 */
     double max_view_angle_deg;        /* 80 */
     double center_margin_frac;        /* 0.5 */
+    int32_t splat_mode;               /* S2D_SPLAT_AFFINE (the reference) or S2D_SPLAT_RAY */
+    int32_t reserved;
 } s2d_raster_config;
+
+/* Splat footprint models.  AFFINE is the reference's: the tangent-plane covariance pushed
+ * through the projection Jacobian (rasterizer.py:212-225), evaluated as |M^-1 d|^2 with
+ * M = J Bc; every parity claim is about this mode.  RAY intersects each pixel's ray with
+ * the surfel plane exactly (the 2D-Gaussian-splatting homography: (u, v, 1/z) ~
+ * (K [t_u t_v p])^-1 (x, y, 1)), blends the intersection depth, and has no reference
+ * counterpart. */
+#define S2D_SPLAT_AFFINE 0
+#define S2D_SPLAT_RAY 1
 
 /* RenderBuffers (rasterizer.py:174-179) + the new normal channel; NULL = not wanted */
 typedef struct s2d_image {

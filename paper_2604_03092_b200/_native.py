@@ -17,6 +17,8 @@ LIB_PATH = os.environ.get("S2D_LIB_PATH") or os.path.join(_HERE, "lib", "libsurf
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "surfel2d.h")
 
 S2D_OK = 0
+SPLAT_AFFINE = 0
+SPLAT_RAY = 1
 S2D_ERR_INVALID = 1
 S2D_ERR_CUDA = 2
 S2D_ERR_OOM = 3
@@ -42,7 +44,8 @@ class RasterCfg(ctypes.Structure):
     _fields_ = [("weight_clamp", ctypes.c_double), ("termination_transmittance", ctypes.c_double),
                 ("footprint_sigma", ctypes.c_double), ("near_plane", ctypes.c_double),
                 ("max_condition", ctypes.c_double), ("max_view_angle_deg", ctypes.c_double),
-                ("center_margin_frac", ctypes.c_double)]
+                ("center_margin_frac", ctypes.c_double), ("splat_mode", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
 
 
 class Image(ctypes.Structure):

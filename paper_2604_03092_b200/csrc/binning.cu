@@ -95,44 +95,54 @@ __global__ void __launch_bounds__(kProjThreads) k_project(const ProjectArgs a) {
     } else if (i < P.n) {
         ExactProj e;
         project_exact(P, pv, i, e);
-        on = e.on_screen;
         degen = e.in_front && !e.valid;
+        double Hi[9];
+        int64_t bb[4] = {e.x0, e.x1, e.y0, e.y1};
+        on = P.mode == S2D_SPLAT_RAY ? (e.valid && ray_setup(P, e, Hi, bb)) : e.on_screen;
         a.flags[i] = (uint8_t)((e.in_front ? 1 : 0) | (e.valid ? 2 : 0) | (on ? 4 : 0));
         if (on) {
-            // M = J Bc (2x2), Minv = M^-1; Sigma = M M^T equals the reference cov2.
-            const double M00 = e.J[0][0] * e.Bc[0][0] + e.J[0][2] * e.Bc[2][0];
-            const double M01 = e.J[0][0] * e.Bc[0][1] + e.J[0][2] * e.Bc[2][1];
-            const double M10 = e.J[1][1] * e.Bc[1][0] + e.J[1][2] * e.Bc[2][0];
-            const double M11 = e.J[1][1] * e.Bc[1][1] + e.J[1][2] * e.Bc[2][1];
-            const double det = M00 * M11 - M01 * M10;
-            const double id = 1.0 / det;
-            SplatRecord r;
-            const float cxh = (float)e.cx, cyh = (float)e.cy;
-            const __half2 lo = __floats2half2_rn((float)(e.cx - (double)cxh), (float)(e.cy - (double)cyh));
-            r.q0 = make_float4(cxh, cyh, __uint_as_float(*reinterpret_cast<const uint32_t *>(&lo)),
-                               pv.opac[i]);
-            r.q1 = make_float4((float)(M11 * id), (float)(-M01 * id), (float)(-M10 * id), (float)(M00 * id));
-            r.q2 = make_float4(pv.colors[3 * i], pv.colors[3 * i + 1], pv.colors[3 * i + 2], (float)e.p[2]);
             // camera-frame normal R_cw R(q)[:,2], oriented toward the camera (N1)
             double nn[3];
 #pragma unroll
             for (int k = 0; k < 3; ++k)
                 nn[k] = P.r_cw[3 * k] * e.R[2] + P.r_cw[3 * k + 1] * e.R[5] + P.r_cw[3 * k + 2] * e.R[8];
             const double sg = (nn[0] * e.p[0] + nn[1] * e.p[1] + nn[2] * e.p[2]) > 0.0 ? -1.0 : 1.0;
-            // guard band of the float32 Mahalanobis distance (covers float32 rounding of Minv,
-            // of the pixel offset and of u, v, m)
-            const double kappa = sqrt(e.lmax / e.lmin);
-            const double gb = 4e-5 * kappa + 1e-5 / sqrt(e.lmin) + 4e-6;
-            r.q3 = make_float4((float)(sg * nn[0]), (float)(sg * nn[1]), (float)(sg * nn[2]), (float)gb);
+            SplatRecord r;
+            if (P.mode == S2D_SPLAT_RAY) {
+                // q0 = (Hi00, Hi01, Hi02, opacity), q1 = (Hi10, Hi11, Hi12, Hi20),
+                // q2 = (r, g, b, Hi21), q3 = (normal, Hi22)
+                r.q0 = make_float4((float)Hi[0], (float)Hi[1], (float)Hi[2], pv.opac[i]);
+                r.q1 = make_float4((float)Hi[3], (float)Hi[4], (float)Hi[5], (float)Hi[6]);
+                r.q2 = make_float4(pv.colors[3 * i], pv.colors[3 * i + 1], pv.colors[3 * i + 2], (float)Hi[7]);
+                r.q3 = make_float4((float)(sg * nn[0]), (float)(sg * nn[1]), (float)(sg * nn[2]), (float)Hi[8]);
+            } else {
+                // M = J Bc (2x2), Minv = M^-1; Sigma = M M^T equals the reference cov2.
+                const double M00 = e.J[0][0] * e.Bc[0][0] + e.J[0][2] * e.Bc[2][0];
+                const double M01 = e.J[0][0] * e.Bc[0][1] + e.J[0][2] * e.Bc[2][1];
+                const double M10 = e.J[1][1] * e.Bc[1][0] + e.J[1][2] * e.Bc[2][0];
+                const double M11 = e.J[1][1] * e.Bc[1][1] + e.J[1][2] * e.Bc[2][1];
+                const double det = M00 * M11 - M01 * M10;
+                const double id = 1.0 / det;
+                const float cxh = (float)e.cx, cyh = (float)e.cy;
+                const __half2 lo = __floats2half2_rn((float)(e.cx - (double)cxh), (float)(e.cy - (double)cyh));
+                r.q0 = make_float4(cxh, cyh, __uint_as_float(*reinterpret_cast<const uint32_t *>(&lo)), pv.opac[i]);
+                r.q1 = make_float4((float)(M11 * id), (float)(-M01 * id), (float)(-M10 * id), (float)(M00 * id));
+                r.q2 = make_float4(pv.colors[3 * i], pv.colors[3 * i + 1], pv.colors[3 * i + 2], (float)e.p[2]);
+                // guard band of the float32 Mahalanobis distance (covers float32 rounding of Minv,
+                // of the pixel offset and of u, v, m)
+                const double kappa = sqrt(e.lmax / e.lmin);
+                const double gb = 4e-5 * kappa + 1e-5 / sqrt(e.lmin) + 4e-6;
+                r.q3 = make_float4((float)(sg * nn[0]), (float)(sg * nn[1]), (float)(sg * nn[2]), (float)gb);
+                ExactRec x;
+                x.cx = e.cx;
+                x.cy = e.cy;
+                x.ia = e.ia;
+                x.ib = e.ib;
+                x.ic = e.ic;
+                a.exact[i] = x;
+            }
             a.rec[i] = r;
-            ExactRec x;
-            x.cx = e.cx;
-            x.cy = e.cy;
-            x.ia = e.ia;
-            x.ib = e.ib;
-            x.ic = e.ic;
-            a.exact[i] = x;
-            a.rect[i] = make_short4((short)e.x0, (short)e.x1, (short)e.y0, (short)e.y1);
+            a.rect[i] = make_short4((short)bb[0], (short)bb[1], (short)bb[2], (short)bb[3]);
             a.z64[i] = e.p[2];
             key = (uint32_t)((uint64_t)__double_as_longlong(e.p[2]) >> 32);  // z > 0: monotone
         }

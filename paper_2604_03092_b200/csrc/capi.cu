@@ -127,6 +127,7 @@ void make_view_params(const double pose[8], const s2d_camera &cam, const s2d_ras
     P.ntx = (cam.width + kTile - 1) / kTile;
     P.nty = (cam.height + kTile - 1) / kTile;
     P.n = n;
+    P.mode = cfg.splat_mode;
 }
 
 int bits_for(int64_t v) {  // bits needed to represent values in [0, v)
@@ -301,6 +302,8 @@ int view_forward(s2d_view *v, cudaStream_t s, const float *params, int64_t n, co
     int rc = validate_camera(cam);
     if (rc) return rc;
     if (!cfg) return fail(S2D_ERR_INVALID, "raster config is NULL");
+    if (cfg->splat_mode != S2D_SPLAT_AFFINE && cfg->splat_mode != S2D_SPLAT_RAY)
+        return fail(S2D_ERR_INVALID, "unknown splat_mode");
     if (!pose) return fail(S2D_ERR_INVALID, "pose is NULL");
     if (n < 0 || n >= (int64_t)1 << 30) return fail(S2D_ERR_INVALID, "surfel count out of range");
     if (n > 0 && !params) return fail(S2D_ERR_INVALID, "params is NULL");
@@ -611,6 +614,7 @@ int s2d_backward(s2d_view *v, void *stream, const float *params, int64_t n, cons
         pb.P = v->P;
         pb.params = params;
         pb.flags = v->flags;
+        pb.rect = v->rect;
         pb.grad2d = v->grad2d;
         pb.grads = grads;
         launch_project_backward(pb, s);

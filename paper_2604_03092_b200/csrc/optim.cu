@@ -1,11 +1,13 @@
 // optim.cu — projection backward (N2) and the fused Adam step (N4).
 //
 // k_project_bwd: per on-screen surfel, chains the per-view 2D gradients
-//   [dL/d opacity, dL/d rgb(3), dL/dz, K = sum dL/dm w w^T (3), e = sum dL/dm w (2), dL/d normal(3)]
-// through Minv = (J(p) Bc)^-1, centre(p), z, normal = R_cw R(q)[:,2] back to
-// the parameters (means, raw quats, scales, opacity, colours), in float64, and
-// ACCUMULATES into the packed gradient block with atomic reductions (views sum with no
-// extra pass, mapper.py:300-307, and views in flight on several streams may share it).  It zeroes the consumed 2D gradients so the per-view
+//   affine: [dL/d opacity, dL/d rgb(3), dL/dz, K = sum dL/dm w w^T (3), e = sum dL/dm w (2), dL/d normal(3)]
+//   ray:    [dL/d opacity, dL/d rgb(3), dL/dHi (9), dL/d normal(3)]
+// through Minv = (J(p) Bc)^-1, centre(p), z (affine) or the ray-splat homography
+// Hi = (K [Bc p])^-1 (ray), and normal = R_cw R(q)[:,2], back to the parameters (means, raw
+// quats, scales, opacity, colours), in float64, and ACCUMULATES into the packed gradient block
+// with atomic reductions (views sum with no extra pass, mapper.py:300-307, and views in flight
+// on several streams may share it).  It zeroes the consumed 2D gradients so the per-view
 // buffer is clean for the next view without a memset.
 // k_adam: torch.optim.Adam arithmetic on the packed block, one thread per
 // surfel (so the per-surfel mask and the quaternion renormalisation are
@@ -36,6 +38,7 @@ __device__ __forceinline__ void dR_dq(const double q[4], const double G[9], doub
     out[3] = d;
 }
 
+template <bool kRay>
 __global__ void __launch_bounds__(128) k_project_bwd(const ProjectBwdArgs a) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const ViewParams &P = a.P;
@@ -45,85 +48,137 @@ __global__ void __launch_bounds__(128) k_project_bwd(const ProjectBwdArgs a) {
     // all independent loads are issued up front (one exposed memory latency); stores at the end
     const int64_t n = P.n;
     const float4 *__restrict__ g4 = reinterpret_cast<const float4 *>(a.grad2d + (size_t)i * 16);
-    const float4 G0 = g4[0], G1 = g4[1], G2 = g4[2];
-    const float G3 = a.grad2d[(size_t)i * 16 + 12];
+    const float4 G0 = g4[0], G1 = g4[1], G2 = g4[2], G3 = g4[3];
     float *gmeans = a.grads, *gquats = a.grads + 3 * n;
     float *gscales = a.grads + 7 * n, *gopac = a.grads + 9 * n;
     float *gcol = a.grads + 10 * n;
 
-    // Geometry for the chain rule: plain float64 (contractions allowed, one division for 1/z and
-    // one for 1/det M) — only the forward's decisions need the reference's exact arithmetic.
+    // Geometry for the chain rule: plain float64 (contractions allowed) — only the forward's
+    // decisions need the reference's exact arithmetic.
     const ParamView pv(a.params, n);
-    struct {
-        double p[3], R[9], Bc[3][2], J[2][3];
-    } e;
+    double p[3], R[9], Bc[3][2];
     {
         const double mu[3] = {(double)pv.means[3 * i], (double)pv.means[3 * i + 1], (double)pv.means[3 * i + 2]};
 #pragma unroll
         for (int r = 0; r < 3; ++r)
-            e.p[r] = P.m_cw[3 * r] * mu[0] + P.m_cw[3 * r + 1] * mu[1] + P.m_cw[3 * r + 2] * mu[2] + P.inv[1 + r];
+            p[r] = P.m_cw[3 * r] * mu[0] + P.m_cw[3 * r + 1] * mu[1] + P.m_cw[3 * r + 2] * mu[2] + P.inv[1 + r];
         const double w = pv.quats[4 * i], x = pv.quats[4 * i + 1], y = pv.quats[4 * i + 2], z = pv.quats[4 * i + 3];
-        e.R[0] = 1.0 - 2.0 * (y * y + z * z);
-        e.R[1] = 2.0 * (x * y - w * z);
-        e.R[2] = 2.0 * (x * z + w * y);
-        e.R[3] = 2.0 * (x * y + w * z);
-        e.R[4] = 1.0 - 2.0 * (x * x + z * z);
-        e.R[5] = 2.0 * (y * z - w * x);
-        e.R[6] = 2.0 * (x * z - w * y);
-        e.R[7] = 2.0 * (y * z + w * x);
-        e.R[8] = 1.0 - 2.0 * (x * x + y * y);
+        R[0] = 1.0 - 2.0 * (y * y + z * z);
+        R[1] = 2.0 * (x * y - w * z);
+        R[2] = 2.0 * (x * z + w * y);
+        R[3] = 2.0 * (x * y + w * z);
+        R[4] = 1.0 - 2.0 * (x * x + z * z);
+        R[5] = 2.0 * (y * z - w * x);
+        R[6] = 2.0 * (x * z - w * y);
+        R[7] = 2.0 * (y * z + w * x);
+        R[8] = 1.0 - 2.0 * (x * x + y * y);
         const double s0 = pv.scales[2 * i], s1 = pv.scales[2 * i + 1];
 #pragma unroll
         for (int r = 0; r < 3; ++r) {
-            e.Bc[r][0] = (P.m_cw[3 * r] * e.R[0] + P.m_cw[3 * r + 1] * e.R[3] + P.m_cw[3 * r + 2] * e.R[6]) * s0;
-            e.Bc[r][1] = (P.m_cw[3 * r] * e.R[1] + P.m_cw[3 * r + 1] * e.R[4] + P.m_cw[3 * r + 2] * e.R[7]) * s1;
+            Bc[r][0] = (P.m_cw[3 * r] * R[0] + P.m_cw[3 * r + 1] * R[3] + P.m_cw[3 * r + 2] * R[6]) * s0;
+            Bc[r][1] = (P.m_cw[3 * r] * R[1] + P.m_cw[3 * r + 1] * R[4] + P.m_cw[3 * r + 2] * R[7]) * s1;
         }
-        const double iz = 1.0 / e.p[2];
-        e.J[0][0] = P.fx * iz;
-        e.J[0][1] = 0.0;
-        e.J[0][2] = -P.fx * e.p[0] * iz * iz;
-        e.J[1][0] = 0.0;
-        e.J[1][1] = P.fy * iz;
-        e.J[1][2] = -P.fy * e.p[1] * iz * iz;
     }
-    const double M00 = e.J[0][0] * e.Bc[0][0] + e.J[0][2] * e.Bc[2][0];
-    const double M01 = e.J[0][0] * e.Bc[0][1] + e.J[0][2] * e.Bc[2][1];
-    const double M10 = e.J[1][1] * e.Bc[1][0] + e.J[1][2] * e.Bc[2][0];
-    const double M11 = e.J[1][1] * e.Bc[1][1] + e.J[1][2] * e.Bc[2][1];
-    const double id = 1.0 / (M00 * M11 - M01 * M10);
-    const double N[2][2] = {{M11 * id, -M01 * id}, {-M10 * id, M00 * id}};
-    // 2D gradient record (k_raster_bwd): [opacity, rgb(3), z, K(uu, uv, vv), e(u, v), normal(3)]
-    // with K = sum dL/dm w w^T and e = sum dL/dm w over the pixels, w = N d the whitened
-    // offset (d = pixel - centre, m = |w|^2):   dL/dN = 2 K M^T,   dL/dcentre = -2 N^T e
-    const double K[2][2] = {{G1.y, G1.z}, {G1.z, G1.w}};
-    const double Mm[2][2] = {{M00, M01}, {M10, M11}};
-    double GN[2][2];
+    const double fx = P.fx, fy = P.fy;
+    // -> dL/dBc (camera-frame tangent axes), dL/dp (camera-frame centre), dL/d normal
+    double gBc[3][2], gp[3], gn[3];
+    if (kRay) {
+        // record (k_raster_bwd, ray): [opacity, rgb(3), dL/dHi' (3x3 row-major), normal(3)] with
+        // Hi' = Hi T(x0, y0) for the bbox corner (x0, y0), and
+        // Hi = H^-1, H = K [a b p]:  dL/dH = -Hi^T dL/dHi Hi^T,  dL/d[a b p] = K^T dL/dH
+        const double H[9] = {fx * Bc[0][0] + P.cx * Bc[2][0], fx * Bc[0][1] + P.cx * Bc[2][1], fx * p[0] + P.cx * p[2],
+                             fy * Bc[1][0] + P.cy * Bc[2][0], fy * Bc[1][1] + P.cy * Bc[2][1], fy * p[1] + P.cy * p[2],
+                             Bc[2][0], Bc[2][1], p[2]};
+        const double A0 = H[4] * H[8] - H[5] * H[7], A1 = H[5] * H[6] - H[3] * H[8], A2 = H[3] * H[7] - H[4] * H[6];
+        const double id = 1.0 / (H[0] * A0 + H[1] * A1 + H[2] * A2);
+        const double Hi[9] = {A0 * id, (H[2] * H[7] - H[1] * H[8]) * id, (H[1] * H[5] - H[2] * H[4]) * id,
+                              A1 * id, (H[0] * H[8] - H[2] * H[6]) * id, (H[2] * H[3] - H[0] * H[5]) * id,
+                              A2 * id, (H[1] * H[6] - H[0] * H[7]) * id, (H[0] * H[4] - H[1] * H[3]) * id};
+        // the raster kernel summed g (x - x0, y - y0, 1), the gradient w.r.t. Hi' = Hi T(x0, y0):
+        // dL/dHi = dL/dHi' T^T
+        const short4 bb = a.rect[i];
+        const double x0 = bb.x, y0 = bb.z;
+        const double GHi[9] = {G1.x + G1.z * x0, G1.y + G1.z * y0, G1.z,
+                               G1.w + G2.y * x0, G2.x + G2.y * y0, G2.y,
+                               G2.z + G3.x * x0, G2.w + G3.x * y0, G3.x};
+        double T[9], GH[9];
 #pragma unroll
-    for (int r = 0; r < 2; ++r)
+        for (int r = 0; r < 3; ++r)
 #pragma unroll
-        for (int c = 0; c < 2; ++c) GN[r][c] = 2.0 * (K[r][0] * Mm[c][0] + K[r][1] * Mm[c][1]);
-    const double gcx = -2.0 * (N[0][0] * G2.x + N[1][0] * G2.y);
-    const double gcy = -2.0 * (N[0][1] * G2.x + N[1][1] * G2.y);
-    // dL/dM = -N^T GN N^T
-    double T[2][2], GM[2][2];
+            for (int c = 0; c < 3; ++c)
+                T[3 * r + c] = Hi[r] * GHi[c] + Hi[3 + r] * GHi[3 + c] + Hi[6 + r] * GHi[6 + c];  // Hi^T GHi
 #pragma unroll
-    for (int r = 0; r < 2; ++r)
+        for (int r = 0; r < 3; ++r)
 #pragma unroll
-        for (int c = 0; c < 2; ++c) T[r][c] = N[0][r] * GN[0][c] + N[1][r] * GN[1][c];  // N^T GN
+            for (int c = 0; c < 3; ++c)
+                GH[3 * r + c] = -(T[3 * r] * Hi[3 * c] + T[3 * r + 1] * Hi[3 * c + 1] + T[3 * r + 2] * Hi[3 * c + 2]);
 #pragma unroll
-    for (int r = 0; r < 2; ++r)
+        for (int j = 0; j < 3; ++j) {
+            const double g0 = fx * GH[j], g1 = fy * GH[3 + j], g2 = P.cx * GH[j] + P.cy * GH[3 + j] + GH[6 + j];
+            if (j < 2) {
+                gBc[0][j] = g0;
+                gBc[1][j] = g1;
+                gBc[2][j] = g2;
+            } else {
+                gp[0] = g0;
+                gp[1] = g1;
+                gp[2] = g2;
+            }
+        }
+        gn[0] = G3.y;
+        gn[1] = G3.z;
+        gn[2] = G3.w;
+    } else {
+        const double iz = 1.0 / p[2], iz2 = iz * iz, iz3 = iz2 * iz;
+        const double J[2][3] = {{fx * iz, 0.0, -fx * p[0] * iz2}, {0.0, fy * iz, -fy * p[1] * iz2}};
+        const double M00 = J[0][0] * Bc[0][0] + J[0][2] * Bc[2][0];
+        const double M01 = J[0][0] * Bc[0][1] + J[0][2] * Bc[2][1];
+        const double M10 = J[1][1] * Bc[1][0] + J[1][2] * Bc[2][0];
+        const double M11 = J[1][1] * Bc[1][1] + J[1][2] * Bc[2][1];
+        const double id = 1.0 / (M00 * M11 - M01 * M10);
+        const double N[2][2] = {{M11 * id, -M01 * id}, {-M10 * id, M00 * id}};
+        // record (k_raster_bwd, affine): [opacity, rgb(3), z, K(uu, uv, vv), e(u, v), normal(3)]
+        // with K = sum dL/dm w w^T and e = sum dL/dm w over the pixels, w = N d the whitened
+        // offset (d = pixel - centre, m = |w|^2):   dL/dN = 2 K M^T,   dL/dcentre = -2 N^T e
+        const double K[2][2] = {{G1.y, G1.z}, {G1.z, G1.w}};
+        const double Mm[2][2] = {{M00, M01}, {M10, M11}};
+        double GN[2][2];
 #pragma unroll
-        for (int c = 0; c < 2; ++c) GM[r][c] = -(T[r][0] * N[c][0] + T[r][1] * N[c][1]);  // (N^T GN) N^T
-    // M = J Bc
-    double gJ[2][3], gBc[3][2];
+        for (int r = 0; r < 2; ++r)
 #pragma unroll
-    for (int r = 0; r < 2; ++r)
+            for (int c = 0; c < 2; ++c) GN[r][c] = 2.0 * (K[r][0] * Mm[c][0] + K[r][1] * Mm[c][1]);
+        const double gcx = -2.0 * (N[0][0] * G2.x + N[1][0] * G2.y);
+        const double gcy = -2.0 * (N[0][1] * G2.x + N[1][1] * G2.y);
+        // dL/dM = -N^T GN N^T
+        double T[2][2], GM[2][2];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) gJ[r][c] = GM[r][0] * e.Bc[c][0] + GM[r][1] * e.Bc[c][1];
+        for (int r = 0; r < 2; ++r)
 #pragma unroll
-    for (int c = 0; c < 3; ++c)
+            for (int c = 0; c < 2; ++c) T[r][c] = N[0][r] * GN[0][c] + N[1][r] * GN[1][c];  // N^T GN
 #pragma unroll
-        for (int k = 0; k < 2; ++k) gBc[c][k] = e.J[0][c] * GM[0][k] + e.J[1][c] * GM[1][k];
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) GM[r][c] = -(T[r][0] * N[c][0] + T[r][1] * N[c][1]);  // (N^T GN) N^T
+        // M = J Bc
+        double gJ[2][3];
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) gJ[r][c] = GM[r][0] * Bc[c][0] + GM[r][1] * Bc[c][1];
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int k = 0; k < 2; ++k) gBc[c][k] = J[0][c] * GM[0][k] + J[1][c] * GM[1][k];
+        // camera-frame mean: J(p), centre(p), z
+        const double x = p[0], y = p[1];
+        gp[0] = gJ[0][2] * (-fx * iz2) + gcx * (fx * iz);
+        gp[1] = gJ[1][2] * (-fy * iz2) + gcy * (fy * iz);
+        gp[2] = (double)G1.x + gJ[0][0] * (-fx * iz2) + gJ[0][2] * (2.0 * fx * x * iz3) + gJ[1][1] * (-fy * iz2) +
+                gJ[1][2] * (2.0 * fy * y * iz3) + gcx * (-fx * x * iz2) + gcy * (-fy * y * iz2);
+        gn[0] = G2.z;
+        gn[1] = G2.w;
+        gn[2] = G3.x;
+    }
     // Bc[:,k] = m_cw R[:,k] s_k
     const double s0 = (double)pv.scales[2 * i], s1 = (double)pv.scales[2 * i + 1];
     double gR[9];
@@ -138,17 +193,15 @@ __global__ void __launch_bounds__(128) k_project_bwd(const ProjectBwdArgs a) {
         }
         gR[3 * b + 0] = t0 * s0;
         gR[3 * b + 1] = t1 * s1;
-        gs0 += t0 * e.R[3 * b + 0];
-        gs1 += t1 * e.R[3 * b + 1];
+        gs0 += t0 * R[3 * b + 0];
+        gs1 += t1 * R[3 * b + 1];
     }
     // normal = sg * R_cw R[:,2]
     {
         double nn[3];
 #pragma unroll
-        for (int k = 0; k < 3; ++k)
-            nn[k] = P.r_cw[3 * k] * e.R[2] + P.r_cw[3 * k + 1] * e.R[5] + P.r_cw[3 * k + 2] * e.R[8];
-        const double sg = (nn[0] * e.p[0] + nn[1] * e.p[1] + nn[2] * e.p[2]) > 0.0 ? -1.0 : 1.0;
-        const double gn[3] = {G2.z, G2.w, G3};
+        for (int k = 0; k < 3; ++k) nn[k] = P.r_cw[3 * k] * R[2] + P.r_cw[3 * k + 1] * R[5] + P.r_cw[3 * k + 2] * R[8];
+        const double sg = (nn[0] * p[0] + nn[1] * p[1] + nn[2] * p[2]) > 0.0 ? -1.0 : 1.0;
 #pragma unroll
         for (int b = 0; b < 3; ++b)
             gR[3 * b + 2] = sg * (P.r_cw[b] * gn[0] + P.r_cw[3 + b] * gn[1] + P.r_cw[6 + b] * gn[2]);
@@ -157,24 +210,12 @@ __global__ void __launch_bounds__(128) k_project_bwd(const ProjectBwdArgs a) {
                          (double)pv.quats[4 * i + 3]};
     double gq[4];
     dR_dq(q, gR, gq);
-    // camera-frame mean: J(p), centre(p), z
-    const double x = e.p[0], y = e.p[1], z = e.p[2];
-    const double fx = P.fx, fy = P.fy;
-    const double iz = 1.0 / z, iz2 = iz * iz, iz3 = iz2 * iz;
-    double gp0 = 0.0, gp1 = 0.0, gp2 = (double)G1.x;
-    gp0 += gJ[0][2] * (-fx * iz2);
-    gp2 += gJ[0][0] * (-fx * iz2) + gJ[0][2] * (2.0 * fx * x * iz3);
-    gp1 += gJ[1][2] * (-fy * iz2);
-    gp2 += gJ[1][1] * (-fy * iz2) + gJ[1][2] * (2.0 * fy * y * iz3);
-    gp0 += gcx * (fx * iz);
-    gp2 += gcx * (-fx * x * iz2);
-    gp1 += gcy * (fy * iz);
-    gp2 += gcy * (-fy * y * iz2);
     // p = s_inv R(q_inv) mu + t_inv.  Accumulation is atomic (fire-and-forget reductions), so
     // views running concurrently on different streams may share one gradient block.
 #pragma unroll
     for (int b = 0; b < 3; ++b)
-        atomicAdd(gmeans + 3 * i + b, (float)(P.inv[0] * (P.r_cw[b] * gp0 + P.r_cw[3 + b] * gp1 + P.r_cw[6 + b] * gp2)));
+        atomicAdd(gmeans + 3 * i + b,
+                  (float)(P.inv[0] * (P.r_cw[b] * gp[0] + P.r_cw[3 + b] * gp[1] + P.r_cw[6 + b] * gp[2])));
 #pragma unroll
     for (int k = 0; k < 4; ++k) atomicAdd(gquats + 4 * i + k, (float)gq[k]);
     atomicAdd(gscales + 2 * i, (float)gs0);
@@ -268,7 +309,8 @@ void launch_project_backward(const ProjectBwdArgs &a, cudaStream_t s) {
     const int64_t blocks = (a.P.n + 127) / 128;
     if (blocks > 0) {
         count_launch();
-        k_project_bwd<<<(unsigned)blocks, 128, 0, s>>>(a);
+        if (a.P.mode == S2D_SPLAT_RAY) k_project_bwd<true><<<(unsigned)blocks, 128, 0, s>>>(a);
+        else k_project_bwd<false><<<(unsigned)blocks, 128, 0, s>>>(a);
     }
 }
 

@@ -116,6 +116,29 @@ __device__ __forceinline__ float fwd_weight(const ViewParams &P, const RasterArg
     return clamped ? P.w_clamp_f : fmaxf(w, 0.f);
 }
 
+// Ray-splat mode (S2D_SPLAT_RAY): (U, V, S) = Hi' (x - x0, y - y0, 1) with Hi' the record's
+// homography relative to the bbox corner (x0, y0), (u, v) = (U, V) / S, z = 1 / S;
+// blends when S > 0 and u^2 + v^2 <= sigma^2 (float32 decisions, no reference counterpart).
+// Shared by forward and backward (identical operations, so both see the same weights).
+struct RayEval {
+    float U, V, iS, u, v, m, g;
+};
+
+__device__ __forceinline__ bool ray_eval(const ViewParams &P, const SplatRecord &r, float pxf, float pyf,
+                                         RayEval &e) {
+    const float S = __fmaf_rn(r.q2.w, pyf, __fmaf_rn(r.q1.w, pxf, r.q3.w));
+    if (!(S > 0.f)) return false;
+    e.U = __fmaf_rn(r.q0.y, pyf, __fmaf_rn(r.q0.x, pxf, r.q0.z));
+    e.V = __fmaf_rn(r.q1.y, pyf, __fmaf_rn(r.q1.x, pxf, r.q1.z));
+    e.iS = __frcp_rn(S);
+    e.u = __fmul_rn(e.U, e.iS);
+    e.v = __fmul_rn(e.V, e.iS);
+    e.m = __fmaf_rn(e.u, e.u, __fmul_rn(e.v, e.v));
+    if (!(e.m <= P.maha_cut_f)) return false;
+    e.g = fast_exp2(__fmul_rn(e.m, -0.72134752044448170368f));
+    return true;
+}
+
 // Warp-private candidate ring (forward).  Each warp streams ITS OWN candidates from the tile's
 // list: list entries are read 32 at a time (key + surfel id), the warp keeps those whose bbox
 // bit for its 8x4 block is set, and copies their 64-B records into a 2-deep ring of 32 slots
@@ -209,7 +232,7 @@ __device__ __forceinline__ int stream_fill(WarpRing &rg, int buf, const uint4 *w
     return n;
 }
 
-template <bool kArg, bool kMaxW, bool kNormal>
+template <bool kArg, bool kMaxW, bool kNormal, bool kRay>
 __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(const RasterArgs a) {
     __shared__ WarpRing s_ring[kRasterThreads / 32];
     const ViewParams &P = a.P;
@@ -245,8 +268,9 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
             cp_commit();
             cp_wait<1>();
             __syncwarp();
-            // lane-parallel ellipse cull of the staged candidates
-            uint32_t hm = __ballot_sync(kFull, lane < n && block_reach(wx0, wy0, ring.rec[buf][lane], P.maha_cut_f));
+            // lane-parallel ellipse cull of the staged candidates (ray mode: the bbox bits only)
+            uint32_t hm = __ballot_sync(kFull, lane < n && (kRay || block_reach(wx0, wy0, ring.rec[buf][lane],
+                                                                              P.maha_cut_f)));
             while (hm) {
                 const int k = __ffs(hm) - 1;
                 hm &= hm - 1;
@@ -254,7 +278,21 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
                 float contrib = 0.f;
                 bool bl = false, clamped = false;
                 if (!done) {
-                    const float w = fwd_weight(P, a, r, ring.id[buf][k], pxf, pyf, px, py, clamped, guard);
+                    float w, zpix;
+                    if (kRay) {
+                        RayEval e;
+                        w = 0.f;
+                        const short4 bb = a.rect[ring.id[buf][k]];
+                        if (ray_eval(P, r, pxf - (float)bb.x, pyf - (float)bb.z, e)) {
+                            w = __fmul_rn(r.q0.w, e.g);
+                            clamped = w > P.w_clamp_f;
+                            w = clamped ? P.w_clamp_f : fmaxf(w, 0.f);
+                        }
+                        zpix = e.iS;
+                    } else {
+                        w = fwd_weight(P, a, r, ring.id[buf][k], pxf, pyf, px, py, clamped, guard);
+                        zpix = r.q2.w;
+                    }
                     if (w > 0.f) {  // blend (blend_forward, _raster_kernels.py:47-55)
                         bl = true;
                         contrib = w * T;
@@ -262,7 +300,7 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
                         c0 = fmaf(contrib, q2.x, c0);
                         c1 = fmaf(contrib, q2.y, c1);
                         c2 = fmaf(contrib, q2.z, c2);
-                        dep = fmaf(contrib, q2.w, dep);
+                        dep = fmaf(contrib, zpix, dep);
                         if (kNormal) {
                             const float4 q3 = r.q3;
                             n0 = fmaf(contrib, q3.x, n0);
@@ -394,7 +432,7 @@ __device__ __forceinline__ void red_map(int lane, int &vi, bool &own) {
 
 __device__ __forceinline__ float sgnf(float x) { return x > 0.f ? 1.f : (x < 0.f ? -1.f : 0.f); }
 
-template <bool kExt>  // kExt: normal / accumulation seeds present (external loss)
+template <bool kExt, bool kRay>  // kExt: normal / accumulation seeds present (external loss)
 __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(const RasterArgs a) {
     __shared__ WarpRing s_ring[kRasterThreads / 32];
     __shared__ float s_loss[8];
@@ -486,7 +524,7 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
     //   [5..7] K = sum dL/dm w w^T (uu, uv, vv), [8..9] e = sum dL/dm w, [10..12] dL/d normal
     // with w = (u, v) = Minv d the whitened pixel offset (dL/dMinv = 2 K M^T and
     // dL/dcentre = -2 Minv^T e are formed in k_project_bwd).
-    constexpr int NV = kExt ? 13 : 10;
+    constexpr int NV = kRay ? (kExt ? 16 : 13) : (kExt ? 13 : 10);
     int vi;
     bool own;
     red_map<NV>(lane, vi, own);
@@ -510,34 +548,47 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
 #pragma unroll
             for (int t = 0; t < 16; ++t) v[t] = 0.f;
             if ((ring.lm[buf][s] >> lane) & 1u) {
-                // the forward's arithmetic (fwd_weight), minus the decisions it already took
+                // the forward's arithmetic (fwd_weight / ray_eval), minus the decisions it took
                 const SplatRecord &r = ring.rec[buf][s];
-                const float4 q0 = r.q0, q1 = r.q1, q2 = r.q2;
-                const uint32_t lob = __float_as_uint(q0.z);
-                const __half2 lo = *reinterpret_cast<const __half2 *>(&lob);
-                const float dx = __fsub_rn(__fsub_rn(pxf, q0.x), __low2float(lo));
-                const float dy = __fsub_rn(__fsub_rn(pyf, q0.y), __high2float(lo));
-                const float u = __fmaf_rn(q1.x, dx, __fmul_rn(q1.y, dy));
-                const float vv = __fmaf_rn(q1.z, dx, __fmul_rn(q1.w, dy));
-                const float m = __fmaf_rn(u, u, __fmul_rn(vv, vv));
-                const float g = fast_exp2(__fmul_rn(m, -0.72134752044448170368f));
                 const bool clamped = (ring.cm[buf][s] >> lane) & 1u;
-                const float w = clamped ? P.w_clamp_f : __fmul_rn(q0.w, g);
+                const float4 q2 = r.q2;
+                float w, g, z;
+                float u = 0.f, vv = 0.f;  // affine: whitened offset
+                RayEval re;
+                const short4 bb = kRay ? a.rect[ring.id[buf][s]] : make_short4(0, 0, 0, 0);
+                const float rx = pxf - (float)bb.x, ry = pyf - (float)bb.z;  // ray: offset from the bbox corner
+                if (kRay) {
+                    ray_eval(P, r, rx, ry, re);  // blended in the forward: S > 0, m <= cut
+                    g = re.g;
+                    z = re.iS;
+                    w = clamped ? P.w_clamp_f : __fmul_rn(r.q0.w, g);
+                } else {
+                    const float4 q0 = r.q0, q1 = r.q1;
+                    const uint32_t lob = __float_as_uint(q0.z);
+                    const __half2 lo = *reinterpret_cast<const __half2 *>(&lob);
+                    const float dx = __fsub_rn(__fsub_rn(pxf, q0.x), __low2float(lo));
+                    const float dy = __fsub_rn(__fsub_rn(pyf, q0.y), __high2float(lo));
+                    u = __fmaf_rn(q1.x, dx, __fmul_rn(q1.y, dy));
+                    vv = __fmaf_rn(q1.z, dx, __fmul_rn(q1.w, dy));
+                    const float m = __fmaf_rn(u, u, __fmul_rn(vv, vv));
+                    g = fast_exp2(__fmul_rn(m, -0.72134752044448170368f));
+                    z = q2.w;
+                    w = clamped ? P.w_clamp_f : __fmul_rn(q0.w, g);
+                }
                 const float Ti = Tn * fast_rcp(1.0f - w);  // T before this contributor; w <= clamp < 1
                 Tn = Ti;
                 const float alpha = w * Ti;
                 v[1] = gc0 * alpha;
                 v[2] = gc1 * alpha;
                 v[3] = gc2 * alpha;
-                v[4] = gd * alpha;
                 // dL/dw = T_i [ G.(c - S) + gd (z - Sd) + Gn.(n - Sn) ] + ga T_i R
-                float dLdw = gc0 * (q2.x - S0) + gc1 * (q2.y - S1) + gc2 * (q2.z - S2) + gd * (q2.w - Sd);
+                float dLdw = gc0 * (q2.x - S0) + gc1 * (q2.y - S1) + gc2 * (q2.z - S2) + gd * (z - Sd);
                 const float omw = 1.0f - w;
                 if (kExt) {
                     const float4 q3 = r.q3;
-                    v[10] = gn0 * alpha;
-                    v[11] = gn1 * alpha;
-                    v[12] = gn2 * alpha;
+                    v[kRay ? 13 : 10] = gn0 * alpha;
+                    v[kRay ? 14 : 11] = gn1 * alpha;
+                    v[kRay ? 15 : 12] = gn2 * alpha;
                     dLdw += gn0 * (q3.x - Sn0) + gn1 * (q3.y - Sn1) + gn2 * (q3.z - Sn2) + ga * R;
                     Sn0 = w * q3.x + omw * Sn0;
                     Sn1 = w * q3.y + omw * Sn1;
@@ -545,19 +596,43 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
                     R *= omw;
                 }
                 dLdw *= Ti;
-                if (!clamped) {
-                    v[0] = dLdw * g;
-                    const float gm = -0.5f * w * dLdw;  // dL/dm
-                    v[8] = gm * u;  // whitened offset w = (u, v)
-                    v[9] = gm * vv;
-                    v[5] = v[8] * u;
-                    v[6] = v[8] * vv;
-                    v[7] = v[9] * vv;
+                if (kRay) {
+                    // dL/d(U, V, S) with u = U/S, v = V/S, z = 1/S; then dL/dHi = g (x, y, 1)^T
+                    float gU = 0.f, gV = 0.f;
+                    float gS = -gd * alpha * z * z;
+                    if (!clamped) {
+                        v[0] = dLdw * g;
+                        const float gm2 = -w * dLdw * re.iS;  // 2 dL/dm / S
+                        gU = gm2 * re.u;
+                        gV = gm2 * re.v;
+                        gS -= gm2 * re.m;
+                    }
+                    // dL/dHi' in the bbox-corner frame (k_project_bwd shifts it back in float64)
+                    v[4] = gU * rx;
+                    v[5] = gU * ry;
+                    v[6] = gU;
+                    v[7] = gV * rx;
+                    v[8] = gV * ry;
+                    v[9] = gV;
+                    v[10] = gS * rx;
+                    v[11] = gS * ry;
+                    v[12] = gS;
+                } else {
+                    v[4] = gd * alpha;
+                    if (!clamped) {
+                        v[0] = dLdw * g;
+                        const float gm = -0.5f * w * dLdw;  // dL/dm
+                        v[8] = gm * u;  // whitened offset w = (u, v)
+                        v[9] = gm * vv;
+                        v[5] = v[8] * u;
+                        v[6] = v[8] * vv;
+                        v[7] = v[9] * vv;
+                    }
                 }
                 S0 = w * q2.x + omw * S0;
                 S1 = w * q2.y + omw * S1;
                 S2 = w * q2.z + omw * S2;
-                Sd = w * q2.w + omw * Sd;
+                Sd = w * z + omw * Sd;
             }
             red_stage<NV, 16>(v, lane);
             if (own && v[0] != 0.f) atomicAdd(a.grad2d + (size_t)ring.id[buf][s] * 16 + vi, v[0]);
@@ -580,29 +655,38 @@ static void ensure_smem(int bytes) {
     }
 }
 
-template <bool kArg, bool kMaxW>
+template <bool kArg, bool kMaxW, bool kRay>
 static void fwd_dispatch(const RasterArgs &a, int tiles, cudaStream_t s) {
-    if (a.normal) k_raster_fwd<kArg, kMaxW, true><<<tiles, kRasterThreads, 0, s>>>(a);
-    else k_raster_fwd<kArg, kMaxW, false><<<tiles, kRasterThreads, 0, s>>>(a);
+    if (a.normal) k_raster_fwd<kArg, kMaxW, true, kRay><<<tiles, kRasterThreads, 0, s>>>(a);
+    else k_raster_fwd<kArg, kMaxW, false, kRay><<<tiles, kRasterThreads, 0, s>>>(a);
+}
+
+template <bool kRay>
+static void fwd_dispatch_mode(const RasterArgs &a, int tiles, cudaStream_t s) {
+    const bool arg = a.max_w != nullptr || a.arg_w != nullptr;
+    const bool mw = a.max_all != nullptr;
+    if (arg && mw) fwd_dispatch<true, true, kRay>(a, tiles, s);
+    else if (arg) fwd_dispatch<true, false, kRay>(a, tiles, s);
+    else if (mw) fwd_dispatch<false, true, kRay>(a, tiles, s);
+    else fwd_dispatch<false, false, kRay>(a, tiles, s);
 }
 
 void launch_raster_forward(const RasterArgs &a, cudaStream_t s) {
     const int tiles = a.P.ntx * a.P.nty;
-    const bool arg = a.max_w != nullptr || a.arg_w != nullptr;
-    const bool mw = a.max_all != nullptr;
     count_launch();
-    if (arg && mw) fwd_dispatch<true, true>(a, tiles, s);
-    else if (arg) fwd_dispatch<true, false>(a, tiles, s);
-    else if (mw) fwd_dispatch<false, true>(a, tiles, s);
-    else fwd_dispatch<false, false>(a, tiles, s);
+    if (a.P.mode == S2D_SPLAT_RAY) fwd_dispatch_mode<true>(a, tiles, s);
+    else fwd_dispatch_mode<false>(a, tiles, s);
 }
 
 void launch_raster_backward(const RasterArgs &a, cudaStream_t s) {
     const int tiles = a.P.ntx * a.P.nty;
     const bool full = a.loss_kind == S2D_LOSS_EXTERNAL && (a.d_normal != nullptr || a.d_accum != nullptr);
     count_launch();
-    if (full) k_raster_bwd<true><<<tiles, kRasterThreads, 0, s>>>(a);
-    else k_raster_bwd<false><<<tiles, kRasterThreads, 0, s>>>(a);
+    const bool ray = a.P.mode == S2D_SPLAT_RAY;
+    if (full && ray) k_raster_bwd<true, true><<<tiles, kRasterThreads, 0, s>>>(a);
+    else if (full) k_raster_bwd<true, false><<<tiles, kRasterThreads, 0, s>>>(a);
+    else if (ray) k_raster_bwd<false, true><<<tiles, kRasterThreads, 0, s>>>(a);
+    else k_raster_bwd<false, false><<<tiles, kRasterThreads, 0, s>>>(a);
 }
 
 }  // namespace s2d

@@ -32,6 +32,7 @@ struct ViewParams {
     float w_clamp_f, term_t_f, maha_cut_f;
     int W, H, ntx, nty;
     int64_t n;
+    int mode;  // S2D_SPLAT_AFFINE / S2D_SPLAT_RAY
 };
 
 // 64-byte splat record, one per on-screen surfel, indexed by input index.
@@ -227,6 +228,58 @@ __device__ __forceinline__ void project_exact(const ViewParams &P, const ParamVi
 struct ExactRec {
     double cx, cy, ia, ib, ic;
 };
+
+// Ray-splat footprint (S2D_SPLAT_RAY).  With the camera-frame tangent axes
+// a = Bc[:,0], b = Bc[:,1] and centre p, H = K [a b p] maps tangent-plane (u, v, 1) to
+// z (x, y, 1), so Hi = H^-1 gives (U, V, S) = Hi (x, y, 1) with (u, v) = (U, V) / S and
+// z = 1 / S; the record holds Hi T(x0, y0), acting on pixel offsets from the bbox corner.  The bbox is the pixel AABB of the projected sigma-square [-s, s]^2 of the
+// tangent plane, which contains the projected sigma-disk when all four corners are in front
+// of the camera (the surfel is dropped otherwise).  Plain float64 (no parity claim).
+__device__ __forceinline__ bool ray_setup(const ViewParams &P, const ExactProj &e, double Hi[9], int64_t bb[4]) {
+    const double a[3] = {e.Bc[0][0], e.Bc[1][0], e.Bc[2][0]}, b[3] = {e.Bc[0][1], e.Bc[1][1], e.Bc[2][1]};
+    const double *c = e.p;
+    const double k = P.sigma;
+    double xmin = 1e300, xmax = -1e300, ymin = 1e300, ymax = -1e300;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const double su = (q & 1) ? k : -k, sv = (q & 2) ? k : -k;
+        const double X = c[0] + su * a[0] + sv * b[0], Y = c[1] + su * a[1] + sv * b[1];
+        const double Z = c[2] + su * a[2] + sv * b[2];
+        if (!(Z > P.near_plane)) return false;
+        const double x = P.fx * X / Z + P.cx, y = P.fy * Y / Z + P.cy;
+        xmin = fmin(xmin, x);
+        xmax = fmax(xmax, x);
+        ymin = fmin(ymin, y);
+        ymax = fmax(ymax, y);
+    }
+    if (!(xmax >= 0.0 && xmin <= P.wm1 && ymax >= 0.0 && ymin <= P.hm1)) return false;
+    bb[0] = clip64((int64_t)ceil(fmax(xmin, -1.0)), 0, P.W - 1);
+    bb[1] = clip64((int64_t)floor(fmin(xmax, P.wm1 + 1.0)), 0, P.W - 1);
+    bb[2] = clip64((int64_t)ceil(fmax(ymin, -1.0)), 0, P.H - 1);
+    bb[3] = clip64((int64_t)floor(fmin(ymax, P.hm1 + 1.0)), 0, P.H - 1);
+    const double H[9] = {P.fx * a[0] + P.cx * a[2], P.fx * b[0] + P.cx * b[2], P.fx * c[0] + P.cx * c[2],
+                         P.fy * a[1] + P.cy * a[2], P.fy * b[1] + P.cy * b[2], P.fy * c[1] + P.cy * c[2],
+                         a[2], b[2], c[2]};
+    const double A0 = H[4] * H[8] - H[5] * H[7], A1 = H[5] * H[6] - H[3] * H[8], A2 = H[3] * H[7] - H[4] * H[6];
+    const double det = H[0] * A0 + H[1] * A1 + H[2] * A2;
+    if (!(fabs(det) > 1e-300) || !isfinite(det)) return false;  // the plane contains the camera centre
+    const double id = 1.0 / det;
+    Hi[0] = A0 * id;
+    Hi[1] = (H[2] * H[7] - H[1] * H[8]) * id;
+    Hi[2] = (H[1] * H[5] - H[2] * H[4]) * id;
+    Hi[3] = A1 * id;
+    Hi[4] = (H[0] * H[8] - H[2] * H[6]) * id;
+    Hi[5] = (H[2] * H[3] - H[0] * H[5]) * id;
+    Hi[6] = A2 * id;
+    Hi[7] = (H[1] * H[6] - H[0] * H[7]) * id;
+    Hi[8] = (H[0] * H[4] - H[1] * H[3]) * id;
+    // relative to the bbox corner: Hi T(x0, y0) acts on (x - x0, y - y0, 1), so the float32
+    // per-pixel evaluation has no cancellation between large pixel coordinates
+    const double x0 = (double)bb[0], y0 = (double)bb[2];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) Hi[3 * r + 2] += Hi[3 * r] * x0 + Hi[3 * r + 1] * y0;
+    return true;
+}
 
 // Reference Mahalanobis distance at integer pixel (x, y), float64 with the
 // reference's association (_raster_kernels.py:38-39), for guard-band re-checks.

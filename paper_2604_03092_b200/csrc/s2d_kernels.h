@@ -118,6 +118,7 @@ struct ProjectBwdArgs {
     ViewParams P;
     const float *params;
     const uint8_t *flags;
+    const short4 *rect;  // per-surfel bbox (ray mode: reference corner of the 2D gradients)
     float *grad2d;
     float *grads;
 };

@@ -59,9 +59,10 @@ def camera_struct(intr) -> N.Camera:
 
 
 def config_struct(cfg) -> N.RasterCfg:
+    mode = {"affine": 0, "ray": 1}[getattr(cfg, "splat_mode", "affine")]
     return N.RasterCfg(float(cfg.weight_clamp), float(cfg.termination_transmittance),
                        float(cfg.footprint_sigma), float(cfg.near_plane), float(cfg.max_condition),
-                       float(cfg.max_view_angle_deg), float(cfg.center_margin_frac))
+                       float(cfg.max_view_angle_deg), float(cfg.center_margin_frac), mode, 0)
 
 
 @dataclass

@@ -163,7 +163,12 @@ class SurfelArrays:
 
 @dataclass(frozen=True)
 class RasterConfig:
-    """Rendering policy knobs (rasterizer.py:150-168)."""
+    """Rendering policy knobs (rasterizer.py:150-168).
+
+    ``splat_mode`` is new: "affine" (default) is the reference's footprint model and the
+    only one parity is claimed for; "ray" evaluates the exact ray / surfel-plane
+    intersection (2D-Gaussian-splatting homography) and blends the per-pixel intersection
+    depth (no reference counterpart)."""
 
     weight_clamp: float = 0.999
     termination_transmittance: float = 1e-4
@@ -172,6 +177,11 @@ class RasterConfig:
     max_condition: float = 1e8
     max_view_angle_deg: float = 80.0
     center_margin_frac: float = 0.5
+    splat_mode: str = "affine"
+
+    def __post_init__(self):
+        if self.splat_mode not in ("affine", "ray"):
+            raise ValueError("splat_mode must be 'affine' or 'ray'")
 
 
 DEFAULT_RASTER_CONFIG = RasterConfig()
