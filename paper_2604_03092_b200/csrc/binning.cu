@@ -21,6 +21,10 @@
 
 #include "s2d_kernels.h"
 
+#ifndef S2D_PROJ_MINB
+#define S2D_PROJ_MINB 3
+#endif
+
 namespace s2d {
 
 namespace {
@@ -82,7 +86,8 @@ __device__ __forceinline__ bool clearly_out(const ViewParams &P, const ParamView
            cyl - tol > (float)P.hmax;
 }
 
-__global__ void __launch_bounds__(kProjThreads) k_project(const ProjectArgs a) {
+template <bool kRay>
+__global__ void __launch_bounds__(kProjThreads, S2D_PROJ_MINB) k_project(const ProjectArgs a) {
     const int64_t i = (int64_t)blockIdx.x * kProjThreads + threadIdx.x;
     const ViewParams &P = a.P;
     bool on = false, degen = false;
@@ -98,7 +103,7 @@ __global__ void __launch_bounds__(kProjThreads) k_project(const ProjectArgs a) {
         degen = e.in_front && !e.valid;
         double Hi[9];
         int64_t bb[4] = {e.x0, e.x1, e.y0, e.y1};
-        on = P.mode == S2D_SPLAT_RAY ? (e.valid && ray_setup(P, e, Hi, bb)) : e.on_screen;
+        on = kRay ? (e.valid && ray_setup(P, e, Hi, bb)) : e.on_screen;
         a.flags[i] = (uint8_t)((e.in_front ? 1 : 0) | (e.valid ? 2 : 0) | (on ? 4 : 0));
         if (on) {
             // camera-frame normal R_cw R(q)[:,2], oriented toward the camera (N1)
@@ -108,7 +113,7 @@ __global__ void __launch_bounds__(kProjThreads) k_project(const ProjectArgs a) {
                 nn[k] = P.r_cw[3 * k] * e.R[2] + P.r_cw[3 * k + 1] * e.R[5] + P.r_cw[3 * k + 2] * e.R[8];
             const double sg = (nn[0] * e.p[0] + nn[1] * e.p[1] + nn[2] * e.p[2]) > 0.0 ? -1.0 : 1.0;
             SplatRecord r;
-            if (P.mode == S2D_SPLAT_RAY) {
+            if (kRay) {
                 // q0 = (Hi00, Hi01, Hi02, opacity), q1 = (Hi10, Hi11, Hi12, Hi20),
                 // q2 = (r, g, b, Hi21), q3 = (normal, Hi22)
                 r.q0 = make_float4((float)Hi[0], (float)Hi[1], (float)Hi[2], pv.opac[i]);
@@ -388,7 +393,8 @@ void launch_project(const ProjectArgs &a, cudaStream_t s) {
     const int blocks = (int)((a.P.n + kProjThreads - 1) / kProjThreads);  // one surfel per thread
     if (blocks > 0) {
         count_launch();
-        k_project<<<blocks, kProjThreads, 0, s>>>(a);
+        if (a.P.mode == S2D_SPLAT_RAY) k_project<true><<<blocks, kProjThreads, 0, s>>>(a);
+        else k_project<false><<<blocks, kProjThreads, 0, s>>>(a);
     }
 }
 

@@ -51,17 +51,6 @@ __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a,
 __device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
 __device__ __forceinline__ double dfma(double a, double b, double c) { return __fma_rn(a, b, c); }
 
-// Correctly rounded a / b from rb = RN(1/b) (Markstein): q = RN(a rb), r = a - b q (exact by
-// fma), RN(q + r rb) = RN(a / b) whenever no intermediate overflows or underflows, which the
-// range test guarantees; anything else (zeros, huge / tiny operands, NaN, inf) takes the full
-// division.  Lets several divisions by one denominator share one reciprocal.
-__device__ __forceinline__ double ddiv_r(double a, double b, double rb) {
-    const double aa = fabs(a), ab = fabs(b);
-    if (!(ab > 0x1p-300 && ab < 0x1p300 && aa > 0x1p-300 && aa < 0x1p300)) return __ddiv_rn(a, b);
-    const double q = __dmul_rn(a, rb);
-    return __fma_rn(__fma_rn(-b, q, a), rb, q);
-}
-
 // numpy float64 -> int64 cast on x86-64 (cvttsd2si): NaN / out of range -> INT64_MIN
 __device__ __forceinline__ int64_t f2i_x86(double v) {
     if (!(v > -9223372036854775808.0 && v < 9223372036854775808.0)) return INT64_MIN;
@@ -135,9 +124,8 @@ __device__ __forceinline__ void project_exact(const ViewParams &P, const ParamVi
     const double z = o.p[2];
     bool in_front = (z > P.near_plane) && (hypot(o.p[0], o.p[1]) <= dmul(P.tan_max, z));
     const double zs = in_front ? z : 1.0;
-    const double rzs = __drcp_rn(zs);
-    o.cx = dadd(ddiv_r(dmul(P.fx, o.p[0]), zs, rzs), P.cx);
-    o.cy = dadd(ddiv_r(dmul(P.fy, o.p[1]), zs, rzs), P.cy);
+    o.cx = dadd(ddiv(dmul(P.fx, o.p[0]), zs), P.cx);
+    o.cy = dadd(ddiv(dmul(P.fy, o.p[1]), zs), P.cy);
     in_front = in_front && (o.cx >= -P.mx) && (o.cx <= P.wmax) && (o.cy >= -P.my) && (o.cy <= P.hmax);
     o.in_front = in_front;
     if (!in_front) {  // not in front: valid = on_screen = false, nothing else is used
@@ -169,13 +157,12 @@ __device__ __forceinline__ void project_exact(const ViewParams &P, const ParamVi
 #pragma unroll
         for (int b = 0; b < 3; ++b) C[a][b] = dfma(o.Bc[a][1], o.Bc[b][1], dmul(o.Bc[a][0], o.Bc[b][0]));
     const double zz = dmul(zs, zs);
-    const double rzz = __drcp_rn(zz);
-    o.J[0][0] = ddiv_r(P.fx, zs, rzs);
+    o.J[0][0] = ddiv(P.fx, zs);
     o.J[0][1] = 0.0;
-    o.J[0][2] = ddiv_r(dmul(-P.fx, o.p[0]), zz, rzz);
+    o.J[0][2] = ddiv(dmul(-P.fx, o.p[0]), zz);
     o.J[1][0] = 0.0;
-    o.J[1][1] = ddiv_r(P.fy, zs, rzs);
-    o.J[1][2] = ddiv_r(dmul(-P.fy, o.p[1]), zz, rzz);
+    o.J[1][1] = ddiv(P.fy, zs);
+    o.J[1][2] = ddiv(dmul(-P.fy, o.p[1]), zz);
     // (jac @ cov_cam) @ jac^T (rasterizer.py:224)
     double T1[2][3], X[2][2];
 #pragma unroll
@@ -202,15 +189,13 @@ __device__ __forceinline__ void project_exact(const ViewParams &P, const ParamVi
     const bool well = (o.lmin > 0.0) && (o.lmax <= dmul(P.max_cond, o.lmin));
     o.valid = well;  // in_front holds here
     const double det = o.valid ? dsub(dmul(o.a, o.c), dmul(o.b, o.b)) : 1.0;
-    const double rdet = __drcp_rn(det);
-    o.ia = ddiv_r(o.c, det, rdet);
-    o.ib = ddiv_r(-o.b, det, rdet);
-    o.ic = ddiv_r(o.a, det, rdet);
+    o.ia = ddiv(o.c, det);
+    o.ib = ddiv(-o.b, det);
+    o.ic = ddiv(o.a, det);
 
     double dinv = dsub(dmul(o.ia, o.ic), dmul(o.ib, o.ib));
     if (!(dinv > 0.0)) dinv = 1.0;
-    const double rdinv = __drcp_rn(dinv);
-    double qx = ddiv_r(o.ic, dinv, rdinv), qy = ddiv_r(o.ia, dinv, rdinv);
+    double qx = ddiv(o.ic, dinv), qy = ddiv(o.ia, dinv);
     if (qx < 0.0) qx = 0.0;
     if (qy < 0.0) qy = 0.0;
     o.rx = dmul(P.sigma, __dsqrt_rn(qx));

@@ -12,4 +12,4 @@ tail -1 gpurun_out/${TAG}_bench.log
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \
   --log-file gpurun_out/${TAG}_launches.csv python tools/profile_view.py > gpurun_out/${TAG}_ncu_launch.log 2>&1; echo "ncu launch rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off \
-  -k regex:'k_raster|k_project' -c 8 -o gpurun_out/${TAG}_full python tools/profile_view.py > gpurun_out/${TAG}_ncu_full.log 2>&1; echo "ncu full rc=$?"
+  -k regex:"k_raster|k_project|k_onesweep|k_scan_emit" -c 16 -o gpurun_out/${TAG}_full python tools/profile_view.py > gpurun_out/${TAG}_ncu_full.log 2>&1; echo "ncu full rc=$?"
