@@ -25,7 +25,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .distributed import allreduce_grads, shard_views, world
+from .distributed import ShardedOptimizerState, allreduce_grads, shard_views, sharded_step, world
 from .engine import (DeviceContext, ImageBuffers, View, camera_struct, config_struct, forward_checked,
                      pack_params, unpack_params)
 from .geometry import as_packed_pose
@@ -364,6 +364,10 @@ class _Lane:
 class AdamRefiner:
     """Multi-view fused-Adam refinement of all surfel parameters, views sharded over ranks.
 
+    With N > 1 ranks the optimizer is sharded by default (``shard_optimizer``): the packed
+    gradients are reduce-scattered by surfel range, each rank runs the fused Adam kernel on
+    its shard (moments for 1/N of the surfels), and the parameters are all-gathered.
+
     ``targets_rgb[v]`` (H,W,3) / ``targets_depth[v]`` (H,W) may be numpy arrays, device
     tensors, or (``host_targets=True``) host tensors that are pinned and copied in every
     step on the view's stream, overlapping the other streams' compute (the end-to-end path).
@@ -373,7 +377,7 @@ class AdamRefiner:
     def __init__(self, surfels, intr: CameraIntrinsics, poses, targets_rgb, targets_depth,
                  loss: ViewLoss = ViewLoss(), adam: AdamConfig = AdamConfig(),
                  raster_cfg: RasterConfig = DEFAULT_RASTER_CONFIG, mask=None, group=None, device=None,
-                 host_targets: bool = False, inflight: int = 4):
+                 host_targets: bool = False, inflight: int = 4, shard_optimizer: bool | None = None):
         self.ctx = DeviceContext.get(device)
         self.dev = self.ctx.device
         self.group = group
@@ -388,8 +392,15 @@ class AdamRefiner:
             self.n = len(surfels)
             self.params = pack_params(surfels, self.dev)
         self.grads = torch.zeros_like(self.params)
-        self.m1 = torch.zeros_like(self.params)
-        self.m2 = torch.zeros_like(self.params)
+        # N > 1: ZeRO-1 style optimizer sharding (reduce-scatter, Adam on this rank's surfels,
+        # all-gather) unless disabled; N = 1: one full Adam step
+        self.sharded = (self.world_size > 1) if shard_optimizer is None else bool(shard_optimizer)
+        if self.sharded:
+            self.opt_state = ShardedOptimizerState(self.n, group, self.dev)
+            self.m1, self.m2 = self.opt_state.m1, self.opt_state.m2
+        else:
+            self.m1 = torch.zeros_like(self.params)
+            self.m2 = torch.zeros_like(self.params)
         self.mask = None if mask is None else torch.as_tensor(np.asarray(mask, dtype=np.uint8)).to(self.dev)
         self.all_poses = [as_packed_pose(p) for p in poses]
         self.my_views = shard_views(len(self.all_poses), self.rank, self.world_size)
@@ -478,14 +489,21 @@ class AdamRefiner:
             if not int(self.host_stats[4]):
                 break
             self._reserve(int(self.host_stats[1]) * 5 // 4 + 4096)
-        allreduce_grads(self.grads, self.loss_acc, self.group)
         self.step_count += 1
-        N.check(N.lib().s2d_adam_step(torch.cuda.current_stream(self.dev).cuda_stream, N.dptr(self.params),
-                                      N.dptr(self.grads), N.dptr(self.m1), N.dptr(self.m2), self.n,
-                                      self.step_count, self.adam, N.dptr(self.mask)), "s2d_adam_step")
+        if self.sharded:
+            allreduce_grads(self.loss_acc, None, self.group)
+            sharded_step(self.params, self.grads, self.opt_state, self._adam, self.mask, self.group)
+        else:
+            allreduce_grads(self.grads, self.loss_acc, self.group)
+            self._adam(self.params, self.grads, self.m1, self.m2, self.n, self.mask)
         self.host_loss.copy_(self.loss_acc, non_blocking=True)
         torch.cuda.current_stream(self.dev).synchronize()
         return float(self.host_loss[0])
+
+    def _adam(self, params, grads, m1, m2, n, mask):
+        N.check(N.lib().s2d_adam_step(torch.cuda.current_stream(self.dev).cuda_stream, N.dptr(params), N.dptr(grads),
+                                      N.dptr(m1), N.dptr(m2), int(n), self.step_count, self.adam, N.dptr(mask)),
+                "s2d_adam_step")
 
     def surfel_arrays(self) -> SurfelArrays:
         P = unpack_params(self.params, self.n)

@@ -138,3 +138,33 @@ def test_host_target_path_matches_device_path():
     d = (a.params - b.params).abs()
     assert float((d > 1e-6).float().mean()) < 1e-3
     assert float(d.max()) <= 3 * 2 * 5e-3
+
+
+def test_sharded_optimizer_path_on_nccl_world_of_one():
+    """The N > 1 optimizer path (reduce-scatter -> fused Adam on the shard -> all-gather) run
+    through NCCL on a one-rank group equals the replicated path (up to the order of the
+    float32 gradient atomics)."""
+    import os
+    import socket
+    import torch.distributed as dist
+    sc, rgbs, deps = _c4_small(2, 3)
+    n = len(sc.surfels)
+    mask = np.arange(n) % 5 != 0
+    plain = AdamRefiner(sc.extra["perturbed"], sc.intr, sc.poses, rgbs, deps, ViewLoss(), AdamConfig(), mask=mask)
+    l_plain = [plain.step() for _ in range(3)]
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        sh = AdamRefiner(sc.extra["perturbed"], sc.intr, sc.poses, rgbs, deps, ViewLoss(), AdamConfig(), mask=mask,
+                         shard_optimizer=True)
+        assert sh.sharded
+        l_sh = [sh.step() for _ in range(3)]
+        torch.cuda.synchronize()
+        assert np.allclose(l_sh, l_plain, rtol=1e-6)
+        assert torch.allclose(sh.params, plain.params, rtol=1e-5, atol=1e-6)
+    finally:
+        dist.destroy_process_group()
