@@ -137,7 +137,11 @@ __global__ void __launch_bounds__(kProjThreads, S2D_PROJ_MINB) k_project(const P
                 // of the pixel offset and of u, v, m)
                 const double kappa = sqrt(e.lmax / e.lmin);
                 const double gb = 4e-5 * kappa + 1e-5 / sqrt(e.lmin) + 4e-6;
-                r.q3 = make_float4((float)(sg * nn[0]), (float)(sg * nn[1]), (float)(sg * nn[2]), (float)gb);
+                // the guard band is stored negated when the opacity is within 8e-6 of the weight
+                // clamp, so the raster kernels test both with one load
+                const bool nearclamp = pv.opac[i] > P.w_clamp_f - 8e-6f;
+                r.q3 = make_float4((float)(sg * nn[0]), (float)(sg * nn[1]), (float)(sg * nn[2]),
+                                   nearclamp ? -(float)gb : (float)gb);
                 ExactRec x;
                 x.cx = e.cx;
                 x.cy = e.cy;

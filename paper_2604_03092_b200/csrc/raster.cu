@@ -100,11 +100,12 @@ __device__ __forceinline__ float fwd_weight(const ViewParams &P, const RasterArg
                                             uint32_t id, float pxf, float pyf, int px, int py, bool &clamped,
                                             int &guard_hits) {
     const float m = pair_maha(r, pxf, pyf);
-    const float op = r.q0.w, gb = r.q3.w;
+    // q3.w = guard band, negated when the opacity is within 8e-6 of the clamp (k_project)
+    const float op = r.q0.w, gbs = r.q3.w, gb = fabsf(gbs);
     clamped = false;
     if (m > P.maha_cut_f + gb) return 0.f;
     const float w = __fmul_rn(op, fast_exp2(__fmul_rn(m, -0.72134752044448170368f)));
-    const bool nearclamp = op > P.w_clamp_f - 8e-6f;
+    const bool nearclamp = gbs < 0.f;
     if (m >= P.maha_cut_f - gb || (nearclamp && fabsf(w - P.w_clamp_f) <= 4e-6f)) {
         ++guard_hits;
         const int rr = guard_resolve(P, a, id, op, px, py);
@@ -255,7 +256,7 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
 
     // this warp's blend stream: one (surfel, lane mask) entry per pair its pixels blended, in
     // list order (the backward's work list)
-    uint4 *ws = a.bstream + 8 * (size_t)rg.x + (size_t)warp * (size_t)max(rg.y - rg.x, 0);
+    uint4 *wp = a.bstream + 8 * (size_t)rg.x + (size_t)warp * (size_t)max(rg.y - rg.x, 0);
     int wc = 0;
     if (rg.y > rg.x && !__all_sync(kFull, done)) {
         ListCursor cur;
@@ -335,7 +336,8 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
                 }
                 if (bm) {
                     const uint32_t cm = __ballot_sync(kFull, bl && clamped);
-                    if (lane == 0) ws[wc] = make_uint4(ring.id[buf][k], bm, cm, 0u);
+                    if (lane == 0) *wp = make_uint4(ring.id[buf][k], bm, cm, 0u);
+                    ++wp;
                     ++wc;
                     if (__all_sync(kFull, done)) break;
                 }
@@ -528,6 +530,7 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
     int vi;
     bool own;
     red_map<NV>(lane, vi, own);
+    float *const g2 = a.grad2d + vi;  // this lane's value column of the 2D gradient record
     float R = 1.f;     // prod_{j later} (1 - w_j)
     float S0 = 0.f, S1 = 0.f, S2 = 0.f, Sd = 0.f, Sn0 = 0.f, Sn1 = 0.f, Sn2 = 0.f;
     WarpRing &ring = s_ring[warp];
@@ -635,7 +638,7 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
                 Sd = w * z + omw * Sd;
             }
             red_stage<NV, 16>(v, lane);
-            if (own && v[0] != 0.f) atomicAdd(a.grad2d + (size_t)ring.id[buf][s] * 16 + vi, v[0]);
+            if (own && v[0] != 0.f) atomicAdd(g2 + (size_t)ring.id[buf][s] * 16, v[0]);
         }
         __syncwarp();  // slot `buf` is refilled by the next ring_fill
         buf ^= 1;
@@ -678,15 +681,20 @@ void launch_raster_forward(const RasterArgs &a, cudaStream_t s) {
     else fwd_dispatch_mode<false>(a, tiles, s);
 }
 
+template <bool kExt, bool kRay>
+static void bwd_launch(const RasterArgs &a, int tiles, cudaStream_t s) {
+    k_raster_bwd<kExt, kRay><<<tiles, kRasterThreads, 0, s>>>(a);
+}
+
 void launch_raster_backward(const RasterArgs &a, cudaStream_t s) {
     const int tiles = a.P.ntx * a.P.nty;
     const bool full = a.loss_kind == S2D_LOSS_EXTERNAL && (a.d_normal != nullptr || a.d_accum != nullptr);
     count_launch();
     const bool ray = a.P.mode == S2D_SPLAT_RAY;
-    if (full && ray) k_raster_bwd<true, true><<<tiles, kRasterThreads, 0, s>>>(a);
-    else if (full) k_raster_bwd<true, false><<<tiles, kRasterThreads, 0, s>>>(a);
-    else if (ray) k_raster_bwd<false, true><<<tiles, kRasterThreads, 0, s>>>(a);
-    else k_raster_bwd<false, false><<<tiles, kRasterThreads, 0, s>>>(a);
+    if (full && ray) bwd_launch<true, true>(a, tiles, s);
+    else if (full) bwd_launch<true, false>(a, tiles, s);
+    else if (ray) bwd_launch<false, true>(a, tiles, s);
+    else bwd_launch<false, false>(a, tiles, s);
 }
 
 }  // namespace s2d

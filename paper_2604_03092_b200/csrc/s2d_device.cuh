@@ -312,7 +312,7 @@ __device__ __forceinline__ bool block_reach(int bx0, int by0, const SplatRecord 
     const uint32_t lob = __float_as_uint(r.q0.z);
     const __half2 lo = *reinterpret_cast<const __half2 *>(&lob);
     const float cx = r.q0.x + __low2float(lo), cy = r.q0.y + __high2float(lo);
-    const float thr = cut + 2.f * r.q3.w + 1e-3f;
+    const float thr = cut + 2.f * fabsf(r.q3.w) + 1e-3f;
     return rect_min_maha((float)bx0 - cx, (float)(bx0 + 7) - cx, (float)by0 - cy, (float)(by0 + 3) - cy, r.q1.x,
                          r.q1.y, r.q1.z, r.q1.w) <= thr;
 }
