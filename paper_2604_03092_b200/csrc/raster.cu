@@ -140,6 +140,19 @@ __device__ __forceinline__ bool ray_eval(const ViewParams &P, const SplatRecord 
     return true;
 }
 
+// 32x32 bit-matrix transpose across the warp: bit j of lane i's x becomes bit i of lane j's
+// result (recursive off-diagonal block swaps, 5 shuffles).
+__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
+    constexpr uint32_t M[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+    for (int t = 0; t < 5; ++t) {
+        const int s = 16 >> t;
+        const uint32_t p = __shfl_xor_sync(kFull, x, s);
+        x = (lane & s) ? ((x & ~M[t]) | ((p & ~M[t]) >> s)) : ((x & M[t]) | ((p & M[t]) << s));
+    }
+    return x;
+}
+
 // Warp-private candidate ring (forward).  Each warp streams ITS OWN candidates from the tile's
 // list: list entries are read 32 at a time (key + surfel id), the warp keeps those whose bbox
 // bit for its 8x4 block is set, and copies their 64-B records into a 2-deep ring of 32 slots
@@ -272,13 +285,16 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
             // lane-parallel ellipse cull of the staged candidates (ray mode: the bbox bits only)
             uint32_t hm = __ballot_sync(kFull, lane < n && (kRay || block_reach(wx0, wy0, ring.rec[buf][lane],
                                                                               P.maha_cut_f)));
+            // per lane, bit k of bl_bits / cl_bits: this pixel blended slot k / with a clamped
+            // weight; transposed into per-slot lane masks once per chunk
+            uint32_t bl_bits = 0u, cl_bits = 0u;
             while (hm) {
                 const int k = __ffs(hm) - 1;
                 hm &= hm - 1;
                 const SplatRecord &r = ring.rec[buf][k];
                 float contrib = 0.f;
-                bool bl = false, clamped = false;
                 if (!done) {
+                    bool clamped = false;
                     float w, zpix;
                     if (kRay) {
                         RayEval e;
@@ -295,7 +311,8 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
                         zpix = r.q2.w;
                     }
                     if (w > 0.f) {  // blend (blend_forward, _raster_kernels.py:47-55)
-                        bl = true;
+                        bl_bits |= 1u << k;
+                        if (clamped) cl_bits |= 1u << k;
                         contrib = w * T;
                         const float4 q2 = r.q2;
                         c0 = fmaf(contrib, q2.x, c0);
@@ -317,8 +334,6 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
                         done = T < term_t;
                     }
                 }
-                // the exact set of this block's pixels that blended the pair -> blend stream
-                const uint32_t bm = __ballot_sync(kFull, bl);
                 if (kMaxW) {
                     const uint32_t id = ring.id[buf][k];
                     float mx = contrib;
@@ -334,13 +349,16 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
                             atomicMax(reinterpret_cast<int *>(a.max_marked + id), __float_as_int(mm));
                     }
                 }
-                if (bm) {
-                    const uint32_t cm = __ballot_sync(kFull, bl && clamped);
-                    if (lane == 0) *wp = make_uint4(ring.id[buf][k], bm, cm, 0u);
-                    ++wp;
-                    ++wc;
-                    if (__all_sync(kFull, done)) break;
-                }
+            }
+            // blend stream: lane k now holds slot k's masks; the slots some pixel blended are
+            // appended in slot (= list) order with one coalesced store
+            {
+                const uint32_t bm = transpose32(bl_bits, lane);
+                const uint32_t cm = __any_sync(kFull, cl_bits != 0u) ? transpose32(cl_bits, lane) : 0u;
+                const uint32_t has = __ballot_sync(kFull, bm != 0u);
+                if (bm != 0u) wp[__popc(has & lanemask_lt())] = make_uint4(ring.id[buf][lane], bm, cm, 0u);
+                wp += __popc(has);
+                wc += __popc(has);
             }
             if (__all_sync(kFull, done)) break;
             __syncwarp();  // slot `buf` is refilled by the next ring_fill
