@@ -399,13 +399,13 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
     if (lane == 0 && nm) atomicAdd(&a.stats->n_mask, nm);
 }
 
-// Transposed warp reduction of C per-lane values (C <= 16): at each butterfly stage the
+// Transposed warp reduction of C per-lane values (C <= 32): at each butterfly stage the
 // lanes exchange half of their values, so the whole reduction costs about C shuffles
 // instead of 5 C.  Afterwards every lane's v[0] is the warp sum of one value; red_map
 // (run once per kernel) says which value (vi) and whether this lane owns it (each value
 // is owned by exactly one lane).
-template <int C, int O>
-__device__ __forceinline__ void red_stage(float (&v)[16], int lane) {
+template <int C, int O, int NA>
+__device__ __forceinline__ void red_stage(float (&v)[NA], int lane) {
     constexpr int H = (C + 1) / 2, F = C / 2;
     const bool up = lane & O;
 #pragma unroll
@@ -415,11 +415,11 @@ __device__ __forceinline__ void red_stage(float (&v)[16], int lane) {
         v[j] = keep + __shfl_xor_sync(kFull, send, O);
     }
     if constexpr (H > F) v[F] += __shfl_xor_sync(kFull, v[F], O);
-    if constexpr (O > 1) red_stage<H, O / 2>(v, lane);
+    if constexpr (O > 1) red_stage<H, O / 2, NA>(v, lane);
 }
 
 template <int C, int O>
-__device__ __forceinline__ void map_stage(int (&ix)[16], bool (&own)[16], int lane) {
+__device__ __forceinline__ void map_stage(int (&ix)[32], bool (&own)[32], int lane) {
     constexpr int H = (C + 1) / 2, F = C / 2;
     const bool up = lane & O;
 #pragma unroll
@@ -438,10 +438,10 @@ __device__ __forceinline__ void map_stage(int (&ix)[16], bool (&own)[16], int la
 
 template <int C>
 __device__ __forceinline__ void red_map(int lane, int &vi, bool &own) {
-    int ix[16];
-    bool ow[16];
+    int ix[32];
+    bool ow[32];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
+    for (int j = 0; j < 32; ++j) {
         ix[j] = j;
         ow[j] = true;
     }
@@ -545,10 +545,13 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
     // with w = (u, v) = Minv d the whitened pixel offset (dL/dMinv = 2 K M^T and
     // dL/dcentre = -2 Minv^T e are formed in k_project_bwd).
     constexpr int NV = kRay ? (kExt ? 16 : 13) : (kExt ? 13 : 10);
+    // two entries per step: their 2 NV values share one transposed reduction (about 2 NV
+    // shuffles instead of 2 x (NV + 2)); lane ownership of the 2 NV sums is fixed per kernel
     int vi;
     bool own;
-    red_map<NV>(lane, vi, own);
-    float *const g2 = a.grad2d + vi;  // this lane's value column of the 2D gradient record
+    red_map<2 * NV>(lane, vi, own);
+    const bool second = vi >= NV;        // this lane's sum belongs to the older entry of the pair
+    const int col = second ? vi - NV : vi;
     float R = 1.f;     // prod_{j later} (1 - w_j)
     float S0 = 0.f, S1 = 0.f, S2 = 0.f, Sd = 0.f, Sn0 = 0.f, Sn1 = 0.f, Sn2 = 0.f;
     WarpRing &ring = s_ring[warp];
@@ -558,105 +561,113 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
     int n = stream_fill(ring, 0, ws, max(e1 - 32, 0), e1, a.rec, lane);
     e1 -= n;
     cp_commit();
+    float v[2 * NV];
+    // one entry of the reverse traversal for this lane: updates the pixel state, writes the
+    // entry's NV gradient values at v[off ...]
+    auto entry = [&](int sl, int off) {
+        if ((ring.lm[buf][sl] >> lane) & 1u) {
+            // the forward's arithmetic (fwd_weight / ray_eval), minus the decisions it took
+            const SplatRecord &r = ring.rec[buf][sl];
+            const bool clamped = (ring.cm[buf][sl] >> lane) & 1u;
+            const float4 q2 = r.q2;
+            float w, g, z;
+            float u = 0.f, vv = 0.f;  // affine: whitened offset
+            RayEval re;
+            const short4 bb = kRay ? a.rect[ring.id[buf][sl]] : make_short4(0, 0, 0, 0);
+            const float rx = pxf - (float)bb.x, ry = pyf - (float)bb.z;  // ray: offset from the bbox corner
+            if (kRay) {
+                ray_eval(P, r, rx, ry, re);  // blended in the forward: S > 0, m <= cut
+                g = re.g;
+                z = re.iS;
+                w = clamped ? P.w_clamp_f : __fmul_rn(r.q0.w, g);
+            } else {
+                const float4 q0 = r.q0, q1 = r.q1;
+                const uint32_t lob = __float_as_uint(q0.z);
+                const __half2 lo = *reinterpret_cast<const __half2 *>(&lob);
+                const float dx = __fsub_rn(__fsub_rn(pxf, q0.x), __low2float(lo));
+                const float dy = __fsub_rn(__fsub_rn(pyf, q0.y), __high2float(lo));
+                u = __fmaf_rn(q1.x, dx, __fmul_rn(q1.y, dy));
+                vv = __fmaf_rn(q1.z, dx, __fmul_rn(q1.w, dy));
+                const float m = __fmaf_rn(u, u, __fmul_rn(vv, vv));
+                g = fast_exp2(__fmul_rn(m, -0.72134752044448170368f));
+                z = q2.w;
+                w = clamped ? P.w_clamp_f : __fmul_rn(q0.w, g);
+            }
+            const float Ti = Tn * fast_rcp(1.0f - w);  // T before this contributor; w <= clamp < 1
+            Tn = Ti;
+            const float alpha = w * Ti;
+            v[off + 1] = gc0 * alpha;
+            v[off + 2] = gc1 * alpha;
+            v[off + 3] = gc2 * alpha;
+            // dL/dw = T_i [ G.(c - S) + gd (z - Sd) + Gn.(n - Sn) ] + ga T_i R
+            float dLdw = gc0 * (q2.x - S0) + gc1 * (q2.y - S1) + gc2 * (q2.z - S2) + gd * (z - Sd);
+            const float omw = 1.0f - w;
+            if (kExt) {
+                const float4 q3 = r.q3;
+                v[off + (kRay ? 13 : 10)] = gn0 * alpha;
+                v[off + (kRay ? 14 : 11)] = gn1 * alpha;
+                v[off + (kRay ? 15 : 12)] = gn2 * alpha;
+                dLdw += gn0 * (q3.x - Sn0) + gn1 * (q3.y - Sn1) + gn2 * (q3.z - Sn2) + ga * R;
+                Sn0 = w * q3.x + omw * Sn0;
+                Sn1 = w * q3.y + omw * Sn1;
+                Sn2 = w * q3.z + omw * Sn2;
+                R *= omw;
+            }
+            dLdw *= Ti;
+            if (kRay) {
+                // dL/d(U, V, S) with u = U/S, v = V/S, z = 1/S; then dL/dHi = g (x, y, 1)^T
+                float gU = 0.f, gV = 0.f;
+                float gS = -gd * alpha * z * z;
+                if (!clamped) {
+                    v[off + 0] = dLdw * g;
+                    const float gm2 = -w * dLdw * re.iS;  // 2 dL/dm / S
+                    gU = gm2 * re.u;
+                    gV = gm2 * re.v;
+                    gS -= gm2 * re.m;
+                }
+                // dL/dHi' in the bbox-corner frame (k_project_bwd shifts it back in float64)
+                v[off + 4] = gU * rx;
+                v[off + 5] = gU * ry;
+                v[off + 6] = gU;
+                v[off + 7] = gV * rx;
+                v[off + 8] = gV * ry;
+                v[off + 9] = gV;
+                v[off + 10] = gS * rx;
+                v[off + 11] = gS * ry;
+                v[off + 12] = gS;
+            } else {
+                v[off + 4] = gd * alpha;
+                if (!clamped) {
+                    v[off + 0] = dLdw * g;
+                    const float gm = -0.5f * w * dLdw;  // dL/dm
+                    v[off + 8] = gm * u;  // whitened offset w = (u, v)
+                    v[off + 9] = gm * vv;
+                    v[off + 5] = v[off + 8] * u;
+                    v[off + 6] = v[off + 8] * vv;
+                    v[off + 7] = v[off + 9] * vv;
+                }
+            }
+            S0 = w * q2.x + omw * S0;
+            S1 = w * q2.y + omw * S1;
+            S2 = w * q2.z + omw * S2;
+            Sd = w * z + omw * Sd;
+        }
+    };
     while (n > 0) {
         const int nn = stream_fill(ring, buf ^ 1, ws, max(e1 - 32, 0), e1, a.rec, lane);
         e1 -= nn;
         cp_commit();
         cp_wait<1>();
         __syncwarp();
-        for (int s = 0; s < n; ++s) {
-            float v[16];
+        for (int s = 0; s < n; s += 2) {
+            const bool two = s + 1 < n;
 #pragma unroll
-            for (int t = 0; t < 16; ++t) v[t] = 0.f;
-            if ((ring.lm[buf][s] >> lane) & 1u) {
-                // the forward's arithmetic (fwd_weight / ray_eval), minus the decisions it took
-                const SplatRecord &r = ring.rec[buf][s];
-                const bool clamped = (ring.cm[buf][s] >> lane) & 1u;
-                const float4 q2 = r.q2;
-                float w, g, z;
-                float u = 0.f, vv = 0.f;  // affine: whitened offset
-                RayEval re;
-                const short4 bb = kRay ? a.rect[ring.id[buf][s]] : make_short4(0, 0, 0, 0);
-                const float rx = pxf - (float)bb.x, ry = pyf - (float)bb.z;  // ray: offset from the bbox corner
-                if (kRay) {
-                    ray_eval(P, r, rx, ry, re);  // blended in the forward: S > 0, m <= cut
-                    g = re.g;
-                    z = re.iS;
-                    w = clamped ? P.w_clamp_f : __fmul_rn(r.q0.w, g);
-                } else {
-                    const float4 q0 = r.q0, q1 = r.q1;
-                    const uint32_t lob = __float_as_uint(q0.z);
-                    const __half2 lo = *reinterpret_cast<const __half2 *>(&lob);
-                    const float dx = __fsub_rn(__fsub_rn(pxf, q0.x), __low2float(lo));
-                    const float dy = __fsub_rn(__fsub_rn(pyf, q0.y), __high2float(lo));
-                    u = __fmaf_rn(q1.x, dx, __fmul_rn(q1.y, dy));
-                    vv = __fmaf_rn(q1.z, dx, __fmul_rn(q1.w, dy));
-                    const float m = __fmaf_rn(u, u, __fmul_rn(vv, vv));
-                    g = fast_exp2(__fmul_rn(m, -0.72134752044448170368f));
-                    z = q2.w;
-                    w = clamped ? P.w_clamp_f : __fmul_rn(q0.w, g);
-                }
-                const float Ti = Tn * fast_rcp(1.0f - w);  // T before this contributor; w <= clamp < 1
-                Tn = Ti;
-                const float alpha = w * Ti;
-                v[1] = gc0 * alpha;
-                v[2] = gc1 * alpha;
-                v[3] = gc2 * alpha;
-                // dL/dw = T_i [ G.(c - S) + gd (z - Sd) + Gn.(n - Sn) ] + ga T_i R
-                float dLdw = gc0 * (q2.x - S0) + gc1 * (q2.y - S1) + gc2 * (q2.z - S2) + gd * (z - Sd);
-                const float omw = 1.0f - w;
-                if (kExt) {
-                    const float4 q3 = r.q3;
-                    v[kRay ? 13 : 10] = gn0 * alpha;
-                    v[kRay ? 14 : 11] = gn1 * alpha;
-                    v[kRay ? 15 : 12] = gn2 * alpha;
-                    dLdw += gn0 * (q3.x - Sn0) + gn1 * (q3.y - Sn1) + gn2 * (q3.z - Sn2) + ga * R;
-                    Sn0 = w * q3.x + omw * Sn0;
-                    Sn1 = w * q3.y + omw * Sn1;
-                    Sn2 = w * q3.z + omw * Sn2;
-                    R *= omw;
-                }
-                dLdw *= Ti;
-                if (kRay) {
-                    // dL/d(U, V, S) with u = U/S, v = V/S, z = 1/S; then dL/dHi = g (x, y, 1)^T
-                    float gU = 0.f, gV = 0.f;
-                    float gS = -gd * alpha * z * z;
-                    if (!clamped) {
-                        v[0] = dLdw * g;
-                        const float gm2 = -w * dLdw * re.iS;  // 2 dL/dm / S
-                        gU = gm2 * re.u;
-                        gV = gm2 * re.v;
-                        gS -= gm2 * re.m;
-                    }
-                    // dL/dHi' in the bbox-corner frame (k_project_bwd shifts it back in float64)
-                    v[4] = gU * rx;
-                    v[5] = gU * ry;
-                    v[6] = gU;
-                    v[7] = gV * rx;
-                    v[8] = gV * ry;
-                    v[9] = gV;
-                    v[10] = gS * rx;
-                    v[11] = gS * ry;
-                    v[12] = gS;
-                } else {
-                    v[4] = gd * alpha;
-                    if (!clamped) {
-                        v[0] = dLdw * g;
-                        const float gm = -0.5f * w * dLdw;  // dL/dm
-                        v[8] = gm * u;  // whitened offset w = (u, v)
-                        v[9] = gm * vv;
-                        v[5] = v[8] * u;
-                        v[6] = v[8] * vv;
-                        v[7] = v[9] * vv;
-                    }
-                }
-                S0 = w * q2.x + omw * S0;
-                S1 = w * q2.y + omw * S1;
-                S2 = w * q2.z + omw * S2;
-                Sd = w * z + omw * Sd;
-            }
-            red_stage<NV, 16>(v, lane);
-            if (own && v[0] != 0.f) atomicAdd(g2 + (size_t)ring.id[buf][s] * 16, v[0]);
+            for (int t = 0; t < 2 * NV; ++t) v[t] = 0.f;
+            entry(s, 0);
+            if (two) entry(s + 1, NV);
+            red_stage<2 * NV, 16>(v, lane);
+            if (own && v[0] != 0.f && (!second || two))
+                atomicAdd(a.grad2d + (size_t)ring.id[buf][second ? s + 1 : s] * 16 + col, v[0]);
         }
         __syncwarp();  // slot `buf` is refilled by the next ring_fill
         buf ^= 1;
