@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(kProjThreads, S2D_PROJ_MINB) k_project(const P
                 const double M10 = e.J[1][1] * e.Bc[1][0] + e.J[1][2] * e.Bc[2][0];
                 const double M11 = e.J[1][1] * e.Bc[1][1] + e.J[1][2] * e.Bc[2][1];
                 const double det = M00 * M11 - M01 * M10;
-                const double id = 1.0 / det;
+                const double id = __drcp_rn(det);
                 const float cxh = (float)e.cx, cyh = (float)e.cy;
                 const __half2 lo = __floats2half2_rn((float)(e.cx - (double)cxh), (float)(e.cy - (double)cyh));
                 r.q0 = make_float4(cxh, cyh, __uint_as_float(*reinterpret_cast<const uint32_t *>(&lo)), pv.opac[i]);
@@ -135,13 +135,14 @@ __global__ void __launch_bounds__(kProjThreads, S2D_PROJ_MINB) k_project(const P
                 r.q2 = make_float4(pv.colors[3 * i], pv.colors[3 * i + 1], pv.colors[3 * i + 2], (float)e.p[2]);
                 // guard band of the float32 Mahalanobis distance (covers float32 rounding of Minv,
                 // of the pixel offset and of u, v, m)
-                const double kappa = sqrt(e.lmax / e.lmin);
-                const double gb = 4e-5 * kappa + 1e-5 / sqrt(e.lmin) + 4e-6;
+                // (float32 with 1% headroom: it is a bound, not a decision)
+                const float lmin_f = (float)e.lmin, lmax_f = (float)e.lmax;
+                const float gb = 1.01f * (4e-5f * sqrtf(lmax_f / lmin_f) + 1e-5f * rsqrtf(lmin_f) + 4e-6f);
                 // the guard band is stored negated when the opacity is within 8e-6 of the weight
                 // clamp, so the raster kernels test both with one load
                 const bool nearclamp = pv.opac[i] > P.w_clamp_f - 8e-6f;
                 r.q3 = make_float4((float)(sg * nn[0]), (float)(sg * nn[1]), (float)(sg * nn[2]),
-                                   nearclamp ? -(float)gb : (float)gb);
+                                   nearclamp ? -gb : gb);
                 ExactRec x;
                 x.cx = e.cx;
                 x.cy = e.cy;

@@ -15,7 +15,10 @@ extern std::atomic<int64_t> g_launches;
 inline void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 constexpr int kSortThreads = 256;
-constexpr int kSortItems = 16;
+#ifndef S2D_SORT_ITEMS
+#define S2D_SORT_ITEMS 16
+#endif
+constexpr int kSortItems = S2D_SORT_ITEMS;
 constexpr int kSortTile = kSortThreads * kSortItems;  // keys per onesweep CTA
 constexpr int kRadixBits = 8;
 constexpr int kRadix = 1 << kRadixBits;
