@@ -74,3 +74,27 @@ def test_c4_backward_linear_in_seeds(c4):
     for f in g1:
         ok, mx, l2 = gate(g12[f], 2 * g1[f] - 3 * g2[f], tol=1e-4)
         assert ok, (f, mx, l2)
+
+
+@pytest.fixture(scope="module")
+def c5():
+    return scenes.config5(0, n_views=16)
+
+
+def test_c5_binning_bit_exact_and_images(c5):
+    """BASELINE config 5 at full size (4M surfels, 1296x968: 4941 tiles, 13-bit tile keys)."""
+    pose = c5.poses[5]
+    run = Run(c5.surfels, pose, c5.intr, normal=False, argmax=False)
+    proj = O.project(c5.surfels, pose, c5.intr)
+    order = O.depth_order(proj)
+    d = run.inspect()
+    st = d["stats"]
+    assert st.visible == len(order) and st.degenerate == proj.degenerate
+    assert np.array_equal(d["order"].cpu().numpy().astype(np.int64), order)
+    start, ids = O.tile_lists(proj, order, c5.intr)
+    assert np.array_equal(d["pair_ids"].cpu().numpy().astype(np.int64), ids)
+    ref = O.render(c5.surfels, pose, c5.intr, with_normal=False)
+    im = run.images()
+    for key in ("color", "depth", "accumulation"):
+        ok, mx, l2 = gate(im[key], getattr(ref, key))
+        assert ok, (key, mx, l2)
