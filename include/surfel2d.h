@@ -93,17 +93,20 @@ typedef struct s2d_view_stats {
 
 /* Introspection of the last forward of a view (device pointers; parity tests). */
 typedef struct s2d_view_debug {
-    const uint32_t *order;      /* (V,) input indices in depth order (rasterizer.py:318-320) */
+    const uint32_t *order;      /* (drawn,) input indices in depth order (rasterizer.py:318-320) of the
+                                   on-screen surfels whose integer bbox is non-empty */
     const uint32_t *pair_tiles; /* (P,) tile id (low 16 bits; bits 16-23: warp-block cull mask), sorted */
     const uint32_t *pair_ids;   /* (P,) surfel index of each pair: per-tile lists in depth order */
     const int32_t *ranges;      /* (ntiles, 2) [start, end) into the pair arrays */
     const int16_t *bbox;        /* (n, 4) x0, x1, y0, y1 (valid where flags & 4) */
     const double *z;            /* (n,) float64 camera depth (valid where flags & 4) */
-    const uint8_t *flags;       /* (n,) bit0 in_front, bit1 valid, bit2 on_screen */
+    const uint8_t *flags;       /* (n,) bit0 in_front, bit1 valid, bit2 on_screen, bit3 drawn (non-empty bbox) */
     const float *records;       /* (n, 16) splat records */
     const int32_t *pixel_state; /* (H*W, 2) number of blended pairs, float bits of the final T */
     int32_t ntiles, tiles_x;
     int64_t pair_capacity;
+    int32_t drawn; /* length of `order` (copied to the host by s2d_view_inspect; synchronous) */
+    int32_t reserved;
 } s2d_view_debug;
 
 /* Loss definition for the backward pass (seeds fused into the backward kernel) */

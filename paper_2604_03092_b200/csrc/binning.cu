@@ -104,7 +104,9 @@ __global__ void __launch_bounds__(kProjThreads, S2D_PROJ_MINB) k_project(const P
         double Hi[9];
         int64_t bb[4] = {e.x0, e.x1, e.y0, e.y1};
         on = kRay ? (e.valid && ray_setup(P, e, Hi, bb)) : e.on_screen;
-        a.flags[i] = (uint8_t)((e.in_front ? 1 : 0) | (e.valid ? 2 : 0) | (on ? 4 : 0));
+        // drawn: on screen with a non-empty integer bbox (the sorted, binned set; flag bit 3)
+        const bool drawn_b = on && bb[0] <= bb[1] && bb[2] <= bb[3];
+        a.flags[i] = (uint8_t)((e.in_front ? 1 : 0) | (e.valid ? 2 : 0) | (on ? 4 : 0) | (drawn_b ? 8 : 0));
         if (on) {
             // camera-frame normal R_cw R(q)[:,2], oriented toward the camera (N1)
             double nn[3];
@@ -154,22 +156,25 @@ __global__ void __launch_bounds__(kProjThreads, S2D_PROJ_MINB) k_project(const P
             a.rec[i] = r;
             a.rect[i] = make_short4((short)bb[0], (short)bb[1], (short)bb[2], (short)bb[3]);
             a.z64[i] = e.p[2];
-            key = (uint32_t)((uint64_t)__double_as_longlong(e.p[2]) >> 32);  // z > 0: monotone
+            if (drawn_b) key = (uint32_t)((uint64_t)__double_as_longlong(e.p[2]) >> 32);  // z > 0: monotone
         }
         a.keys[i] = key;
         a.vals[i] = (uint32_t)i;
     }
-    // per-view counters: visible, degenerate (rasterizer.py:244), key range
+    // per-view counters: visible, drawn, degenerate (rasterizer.py:244), key range
+    const bool drawn = key != 0xffffffffu;
     const uint32_t vm = __ballot_sync(kFull, on), dm = __ballot_sync(kFull, degen);
-    uint32_t kmin = on ? key : 0xffffffffu, kmax = on ? key : 0u;
+    const uint32_t wm = __ballot_sync(kFull, drawn);
+    uint32_t kmin = drawn ? key : 0xffffffffu, kmax = drawn ? key : 0u;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         kmin = min(kmin, __shfl_xor_sync(kFull, kmin, o));
         kmax = max(kmax, __shfl_xor_sync(kFull, kmax, o));
     }
     if ((threadIdx.x & 31) == 0) {
-        if (vm) {
-            atomicAdd(&a.stats->visible, __popc(vm));
+        if (vm) atomicAdd(&a.stats->visible, __popc(vm));
+        if (wm) {
+            atomicAdd(a.n_drawn, __popc(wm));
             atomicMax(a.key_range, ~kmin);  // the sync region starts zeroed: store ~min
             atomicMax(a.key_range + 1, kmax);
         }

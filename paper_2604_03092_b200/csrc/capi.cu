@@ -246,6 +246,7 @@ int layout_sync(s2d_view *v, int64_t n, int64_t pcap, int ntiles) {
     };
     const size_t o_stats = take(sizeof(s2d_view_stats));
     const size_t o_tickets = take(16 * sizeof(int));
+    const size_t o_drawn = take(sizeof(int));
     const size_t o_krange = take(2 * 4);
     const size_t o_dhist = take(3 * kRadix * 4);
     const size_t o_dstat = take((size_t)3 * sort_tiles * kRadix * 4);
@@ -260,6 +261,7 @@ int layout_sync(s2d_view *v, int64_t n, int64_t pcap, int ntiles) {
     uint8_t *b = v->sync;
     v->sr.stats = reinterpret_cast<s2d_view_stats *>(b + o_stats);
     v->sr.tickets = reinterpret_cast<int *>(b + o_tickets);
+    v->sr.n_drawn = reinterpret_cast<int *>(b + o_drawn);
     v->sr.key_range = reinterpret_cast<uint32_t *>(b + o_krange);
     v->sr.depth_hist = reinterpret_cast<uint32_t *>(b + o_dhist);
     v->sr.depth_status = reinterpret_cast<uint32_t *>(b + o_dstat);
@@ -326,7 +328,9 @@ int view_forward(s2d_view *v, cudaStream_t s, const float *params, int64_t n, co
     };
     mark();
     SyncRegion &sr = v->sr;
-    int *d_v = &sr.stats->visible;
+    // the depth sort and the pair emission run over the drawn surfels: on-screen with a
+    // non-empty integer bbox (an empty bbox touches no pixel, _raster_kernels.py:32-34)
+    int *d_v = sr.n_drawn;
     if (n > 0) {
         ProjectArgs pa;
         pa.P = P;
@@ -340,6 +344,7 @@ int view_forward(s2d_view *v, cudaStream_t s, const float *params, int64_t n, co
         pa.vals = v->vals[0];
         pa.stats = sr.stats;
         pa.key_range = sr.key_range;
+        pa.n_drawn = sr.n_drawn;
         launch_project(pa, s);
         mark();
         // depth order: keys rebased to 24 bits, 3 stable 8-bit passes; the first pass reads all
@@ -642,6 +647,7 @@ int s2d_view_inspect(s2d_view *v, s2d_view_debug *out) {
     if (!v || !out) return fail(S2D_ERR_INVALID, "NULL argument");
     if (!v->has_fwd) return fail(S2D_ERR_STATE, "no forward on this view");
     out->order = v->vals[v->order_buf];
+    S2D_CUDA(cudaMemcpy(&out->drawn, v->sr.n_drawn, sizeof(int), cudaMemcpyDeviceToHost));
     out->pair_tiles = v->pkeys[v->pair_buf];
     out->pair_ids = v->pvals[v->pair_buf];
     out->ranges = reinterpret_cast<int32_t *>(v->sr.ranges);

@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(128) k_project_bwd(const ProjectBwdArgs a) {
     const ViewParams &P = a.P;
     if (i >= P.n) return;
     const uint8_t fl = __ldg(a.flags + i);
-    if (!(fl & 4)) return;
+    if (!(fl & 8)) return;  // not drawn: no pixel, no 2D gradient
     // all independent loads are issued up front (one exposed memory latency); stores at the end
     const int64_t n = P.n;
     const float4 *__restrict__ g4 = reinterpret_cast<const float4 *>(a.grad2d + (size_t)i * 16);

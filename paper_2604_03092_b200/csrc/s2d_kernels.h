@@ -31,6 +31,7 @@ constexpr int kEmitTile = 256 * kEmitItems;
 struct SyncRegion {
     s2d_view_stats *stats;     // device stats (first, 32 B)
     int *tickets;              // [16]
+    int *n_drawn;              // on-screen surfels with a non-empty integer bbox (the sorted set)
     uint32_t *key_range;       // [2]: ~min, max depth key
     uint32_t *depth_hist;      // [3 * kRadix]
     uint32_t *depth_status;    // [3][ceil(n / kSortTile) * kRadix]
@@ -54,6 +55,7 @@ struct ProjectArgs {
     uint32_t *vals;
     s2d_view_stats *stats;
     uint32_t *key_range;  // [~min, max] of on-screen depth keys (sync region, zeroed)
+    int *n_drawn;         // count of drawn surfels (sync region, zeroed)
 };
 void launch_project(const ProjectArgs &a, cudaStream_t s);
 

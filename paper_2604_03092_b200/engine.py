@@ -214,9 +214,9 @@ class View:
         st = self.stats()
         n, h, w = self._last
         dev = self.device
-        v, p = st.visible, st.pairs_stored
+        v, p = d.drawn, st.pairs_stored
         out = {
-            "order": _wrap(d.order, (v,), "<i4", dev).clone(),
+            "order": _wrap(d.order, (v,), "<i4", dev).clone(),  # drawn surfels (non-empty bbox)
             "pair_tiles": _wrap(d.pair_tiles, (p,), "<i4", dev).clone() & 0xFFFF,  # low 16 bits: tile id
             "pair_ids": _wrap(d.pair_ids, (p,), "<i4", dev).clone(),
             "ranges": _wrap(d.ranges, (d.ntiles, 2), "<i4", dev).clone(),

@@ -66,3 +66,11 @@ def gate(a, b, tol=1e-4):
     mx = np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
     l2 = np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
     return (mx <= tol and l2 <= tol), mx, l2
+
+
+def drawn_order(bbox, order):
+    """The reference depth order restricted to the surfels whose integer bbox is non-empty
+    (the only ones that touch a pixel, _raster_kernels.py:32-34): the set the device sorts."""
+    order = np.asarray(order, dtype=np.int64)
+    b = np.asarray(bbox)[order]
+    return order[(b[:, 0] <= b[:, 1]) & (b[:, 2] <= b[:, 3])]

@@ -5,7 +5,7 @@ import pytest
 
 import oracle as O
 from conftest import GOLDEN_NAMES
-from gpu_helpers import Run, far_targets, gate
+from gpu_helpers import Run, drawn_order, far_targets, gate
 from paper_2604_03092_b200 import rasterizer as R
 from paper_2604_03092_b200 import scenes
 from paper_2604_03092_b200.geometry import SE3Pose, Sim3Transform, UnitQuaternion
@@ -25,7 +25,9 @@ def check_binning(run, proj, order, intr):
     assert st.degenerate == proj.degenerate
     assert np.array_equal(d["bbox"].cpu().numpy().astype(np.int64)[on], proj.bbox[on]), "bbox"
     assert np.array_equal(d["z"].cpu().numpy()[on], proj.z[on]), "float64 z"
-    assert np.array_equal(d["order"].cpu().numpy().astype(np.int64), order), "depth order"
+    assert np.array_equal(d["order"].cpu().numpy().astype(np.int64), drawn_order(proj.bbox, order)), "depth order"
+    drawn = on & (proj.bbox[:, 0] <= proj.bbox[:, 1]) & (proj.bbox[:, 2] <= proj.bbox[:, 3])
+    assert np.array_equal((flags >> 3) & 1, drawn.astype(np.uint8)), "drawn flag"
     start, ids = O.tile_lists(proj, order, intr)
     assert st.pairs == len(ids)
     assert np.array_equal(d["pair_ids"].cpu().numpy().astype(np.int64), ids), "tile lists"
@@ -51,7 +53,7 @@ def test_binning_bit_exact_vs_reference(goldens, name):
     assert d["stats"].degenerate == int(g["degenerate"])
     assert np.array_equal(d["bbox"].cpu().numpy().astype(np.int64)[on], g["bbox"][on])
     assert np.array_equal(d["z"].cpu().numpy()[on], g["z"][on])
-    assert np.array_equal(d["order"].cpu().numpy().astype(np.int64), g["order"])
+    assert np.array_equal(d["order"].cpu().numpy().astype(np.int64), drawn_order(g["bbox"], g["order"]))
     proj = O.project(g.surfels, g.pose, g.intr, g.cfg)
     check_binning(run, proj, g["order"], g.intr)
 
