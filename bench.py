@@ -235,15 +235,16 @@ def main():
 
     # ---- device-resident run (value) ----
     inflight = int(os.environ.get("S2D_INFLIGHT", "8"))
+    graph = os.environ.get("S2D_GRAPH", "1") == "1"
     ref = AdamRefiner(sc.extra["perturbed"], sc.intr, sc.poses, rgbs, deps, loss, AdamConfig(), device=dev,
-                      inflight=inflight)
+                      inflight=inflight, cuda_graph=graph)
     for _ in range(args.warmup):
         ref.step()
     clocks = ClockSampler(local_rank)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    launches0 = N.lib().s2d_launch_count()
+    launches0 = ref.kernel_launches
     clocks.start()
     time.sleep(0.2)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -254,7 +255,7 @@ def main():
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
-    launches = N.lib().s2d_launch_count() - launches0
+    launches = ref.kernel_launches - launches0
     ms = e0.elapsed_time(e1)
     t = torch.tensor([ms], device=dev, dtype=torch.float64)
     if world > 1:
@@ -266,6 +267,7 @@ def main():
     # ---- per-phase breakdown (separate timed pass with events between kernels; one stream,
     # so the phases do not overlap) ----
     ref.active_lanes = 1
+    ref.cuda_graph = False  # eager: events between the library's kernels
     ref.view.set_timing(True)
     ref.view.timing(reset=True)
     tb0 = torch.cuda.Event(enable_timing=True)
@@ -314,7 +316,7 @@ def main():
     del ref
     torch.cuda.empty_cache()
     ref2 = AdamRefiner(sc.extra["perturbed"], sc.intr, sc.poses, host_rgb, host_dep, loss, AdamConfig(), device=dev,
-                       host_targets=True, inflight=inflight)
+                       host_targets=True, inflight=inflight, cuda_graph=graph)
     for _ in range(args.warmup):
         ref2.step()
     if world > 1:

@@ -377,7 +377,8 @@ class AdamRefiner:
     def __init__(self, surfels, intr: CameraIntrinsics, poses, targets_rgb, targets_depth,
                  loss: ViewLoss = ViewLoss(), adam: AdamConfig = AdamConfig(),
                  raster_cfg: RasterConfig = DEFAULT_RASTER_CONFIG, mask=None, group=None, device=None,
-                 host_targets: bool = False, inflight: int = 8, shard_optimizer: bool | None = None):
+                 host_targets: bool = False, inflight: int = 8, shard_optimizer: bool | None = None,
+                 cuda_graph: bool = False):
         self.ctx = DeviceContext.get(device)
         self.dev = self.ctx.device
         self.group = group
@@ -428,6 +429,12 @@ class AdamRefiner:
         self.host_stats = torch.zeros(8, dtype=torch.int32).pin_memory()
         self.host_loss = torch.zeros(1, dtype=torch.float64).pin_memory()
         self.step_count = 0
+        # CUDA graph of one step's views (forward, stats, backward on every lane stream): one
+        # launch per step instead of ~4 library calls per view from Python
+        self.cuda_graph = bool(cuda_graph)
+        self._graph = None
+        self._graph_launches = 0
+        self.kernel_launches = 0  # library kernels launched by step() (graph replays included)
         self.h2d_bytes_per_step = (sum(self.rgb[v].numel() + self.depth[v].numel() for v in self.my_views) * 4
                                    if host_targets else 0)
         self._size_pairs()
@@ -480,22 +487,50 @@ class AdamRefiner:
         for lane in lanes:
             main.wait_stream(lane.stream)
 
-    def step(self) -> float:
-        """One refine iteration; returns the total loss over ALL views (all ranks)."""
-        for _ in range(3):
+    def _capture(self):
+        """Capture compute_grads (+ the stats read-back) into a CUDA graph.  The pair
+        capacities must already fit (an eager step sized them): the library does not
+        allocate while they do."""
+        torch.cuda.synchronize(self.dev)
+        g = torch.cuda.CUDAGraph()
+        l0 = N.lib().s2d_launch_count()
+        with torch.cuda.graph(g):
             self.compute_grads()
             self.host_stats.copy_(self.stats_acc, non_blocking=True)
+        self._graph_launches = N.lib().s2d_launch_count() - l0
+        self._graph = g
+
+    def _grads_checked(self):
+        """compute_grads, re-run with a grown pair capacity when a view overflowed it."""
+        for _ in range(3):
+            l0 = N.lib().s2d_launch_count()
+            if self.cuda_graph and self.step_count > 0:
+                if self._graph is None:
+                    self._capture()
+                self._graph.replay()
+                self.kernel_launches += self._graph_launches
+            else:
+                self.compute_grads()
+                self.host_stats.copy_(self.stats_acc, non_blocking=True)
+                self.kernel_launches += N.lib().s2d_launch_count() - l0
             torch.cuda.current_stream(self.dev).synchronize()
             if not int(self.host_stats[4]):
-                break
+                return
             self._reserve(int(self.host_stats[1]) * 5 // 4 + 4096)
+            self._graph = None  # buffers may have moved: capture again
+
+    def step(self) -> float:
+        """One refine iteration; returns the total loss over ALL views (all ranks)."""
+        self._grads_checked()
         self.step_count += 1
+        l0 = N.lib().s2d_launch_count()
         if self.sharded:
             allreduce_grads(self.loss_acc, None, self.group)
             sharded_step(self.params, self.grads, self.opt_state, self._adam, self.mask, self.group)
         else:
             allreduce_grads(self.grads, self.loss_acc, self.group)
             self._adam(self.params, self.grads, self.m1, self.m2, self.n, self.mask)
+        self.kernel_launches += N.lib().s2d_launch_count() - l0
         self.host_loss.copy_(self.loss_acc, non_blocking=True)
         torch.cuda.current_stream(self.dev).synchronize()
         return float(self.host_loss[0])

@@ -165,6 +165,27 @@ def test_sharded_optimizer_path_on_nccl_world_of_one():
         l_sh = [sh.step() for _ in range(3)]
         torch.cuda.synchronize()
         assert np.allclose(l_sh, l_plain, rtol=1e-6)
-        assert torch.allclose(sh.params, plain.params, rtol=1e-5, atol=1e-6)
+        # (gradient atomics sum in a run-dependent order; compare in norm, see the graph test)
+        assert float(torch.linalg.norm(sh.params - plain.params) / torch.linalg.norm(plain.params)) < 1e-4
     finally:
         dist.destroy_process_group()
+
+
+def test_cuda_graph_step_matches_eager_and_regrows():
+    """AdamRefiner(cuda_graph=True): one graph replay per step gives the eager steps' results;
+    a pair-capacity overflow inside a replay is detected, the capacity regrown and the graph
+    captured again."""
+    sc, rgbs, deps = _c4_small(3, 4)
+    eager = AdamRefiner(sc.extra["perturbed"], sc.intr, sc.poses, rgbs, deps, ViewLoss(), AdamConfig())
+    l_e = [eager.step() for _ in range(4)]
+    graph = AdamRefiner(sc.extra["perturbed"], sc.intr, sc.poses, rgbs, deps, ViewLoss(), AdamConfig(),
+                        cuda_graph=True)
+    l_g = [graph.step() for _ in range(2)]
+    graph._reserve(2048)  # too small: the next replay overflows and must be re-run
+    graph._graph = None
+    l_g += [graph.step() for _ in range(2)]
+    assert graph._graph is not None and graph.kernel_launches > 0
+    assert np.allclose(l_g, l_e, rtol=1e-5)
+    # gradient atomics sum in a run-dependent order, and Adam turns a sign flip of a ~0
+    # gradient into a full lr step: compare the parameter blocks in norm
+    assert float(torch.linalg.norm(graph.params - eager.params) / torch.linalg.norm(eager.params)) < 1e-4
