@@ -6,16 +6,22 @@
 //
 // Forward (k_raster_fwd): each warp streams its own candidates from the tile's depth-ordered
 // list (entries whose bbox bit for its block is set, k_scan_emit) into a warp-private
-// double-buffered ring of 64-B records (cp.async), culls them lane-parallel against the
-// block with the exact ellipse test, and blends the survivors in list order, one pixel per
-// lane.  A warp stops when every lane's transmittance is below the termination threshold.
-// For every pair its pixels blended the warp appends (surfel, lane mask of the pixels that
-// blended it, lane mask of those whose weight clamped) to its blend stream.
+// double-buffered ring of 80-B slots (cp.async).  A lane-parallel prep phase (one slot per
+// lane) culls them against the block with the exact ellipse test and rewrites each kept slot
+// to block-relative form (block_centre: exact per-lane pixel offsets, the two cut thresholds,
+// a slow-path flag), so the per-candidate work of a lane is 8 FMA-class ops for m, one
+// compare, and, on the fast path (m below the guard band, no clamp possible), the blend.  A
+// lane whose transmittance fell below the termination threshold carries a NaN x offset, so
+// its m fails the cut test with no extra check; the warp stops when every lane has.  For
+// every slot its pixels blended the warp appends (surfel, lane mask of the pixels that blended
+// it, lane mask of those whose weight clamped) to its blend stream.
 //
 // Backward (k_raster_bwd): each warp walks its blend stream newest first and runs the
 // reverse recurrence (transmittance recovered by division, normalised suffix
-// S <- w c + (1 - w) S) on exactly the forward's blended set; the per-entry 2D gradients are
-// reduced over the warp (transposed butterfly) and added with one atomic per value.
+// S <- w c + (1 - w) S) on exactly the forward's blended set.  Every lane runs every entry
+// (branch-free: lanes outside the entry's mask take w = 0, which leaves their state unchanged
+// and zeroes their values); the per-entry 2D gradients of two entries are reduced over the
+// warp together (transposed butterfly) and added with one atomic per value.
 //
 // Semantics follow blend_forward (_raster_kernels.py:22-55) exactly: the termination test
 // precedes blending, pixel (row y, col x) samples (x, y), the Mahalanobis cut is
@@ -79,34 +85,22 @@ __device__ __forceinline__ float fast_rcp(float x) {
     return y;
 }
 
-// Forward weight of pair (record r, pixel), fwd_weight: 0 if the pair does not blend, else the weight the reference blends with.  Fast path: m = |Minv d|^2 in float32.  m < cut - gb implies the
-// reference's float64 m is below the cut, hence the pixel lies inside the reference bbox (the
-// bbox is the ellipse's exact extent), so no bbox test is needed; m > cut + gb rejects.  Inside
-// the band, or when the weight is within 4e-6 of the clamp, guard_resolve decides in float64.
-// The backward recomputes w with the same float32 operations and takes the clamp decision from
-// the forward's blend stream, so both passes see bit-identical weights.
-__device__ __forceinline__ float pair_maha(const SplatRecord &r, float pxf, float pyf) {
-    const float4 q0 = r.q0, q1 = r.q1;
-    const uint32_t lob = __float_as_uint(q0.z);
-    const __half2 lo = *reinterpret_cast<const __half2 *>(&lob);
-    const float dx = __fsub_rn(__fsub_rn(pxf, q0.x), __low2float(lo));
-    const float dy = __fsub_rn(__fsub_rn(pyf, q0.y), __high2float(lo));
-    const float u = __fmaf_rn(q1.x, dx, __fmul_rn(q1.y, dy));
-    const float v = __fmaf_rn(q1.z, dx, __fmul_rn(q1.w, dy));
-    return __fmaf_rn(u, u, __fmul_rn(v, v));
-}
-
-__device__ __forceinline__ float fwd_weight(const ViewParams &P, const RasterArgs &a, const SplatRecord &r,
-                                            uint32_t id, float pxf, float pyf, int px, int py, bool &clamped,
-                                            int &guard_hits) {
-    const float m = pair_maha(r, pxf, pyf);
-    // q3.w = guard band, negated when the opacity is within 8e-6 of the clamp (k_project)
-    const float op = r.q0.w, gbs = r.q3.w, gb = fabsf(gbs);
+// Forward decision for a pair whose float32 m fell at or above the slot's lower threshold
+// cut - gb, or whose slot is flagged slow (q3.w < 0: opacity within 8e-6 of the weight clamp,
+// or not above 1e-30).  Returns 0 if the pair does not blend, else the weight the reference
+// blends with.  Below cut - gb the reference's float64 m is below the cut, so the pixel lies
+// inside the reference bbox (the bbox is the ellipse's exact extent) and the pair blends with
+// the float32 weight, which for a non-flagged slot is positive and below the clamp (the fast
+// path in k_raster_fwd).  Inside the band [cut - gb, cut + gb], or when the weight is within
+// 4e-6 of the clamp, guard_resolve decides in float64.  (A tiny-opacity slot takes the
+// near-clamp branches harmlessly: its weight is far below the clamp.)  The backward
+// recomputes w with the same float32 operations and takes the clamp decision from the
+// forward's blend stream, so both passes see bit-identical weights.
+__device__ __forceinline__ float slow_weight(const ViewParams &P, const RasterArgs &a, uint32_t id, float op, float m,
+                                          float w, float tlo, int px, int py, bool &clamped, int &guard_hits) {
+    const bool nearclamp = tlo < 0.f;
     clamped = false;
-    if (m > P.maha_cut_f + gb) return 0.f;
-    const float w = __fmul_rn(op, fast_exp2(__fmul_rn(m, -0.72134752044448170368f)));
-    const bool nearclamp = gbs < 0.f;
-    if (m >= P.maha_cut_f - gb || (nearclamp && fabsf(w - P.w_clamp_f) <= 4e-6f)) {
+    if (m >= fabsf(tlo) || (nearclamp && fabsf(w - P.w_clamp_f) <= 4e-6f)) {
         ++guard_hits;
         const int rr = guard_resolve(P, a, id, op, px, py);
         if (!(rr & 1)) return 0.f;
@@ -153,17 +147,58 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
     return x;
 }
 
-// Warp-private candidate ring (forward).  Each warp streams ITS OWN candidates from the tile's
-// list: list entries are read 32 at a time (key + surfel id), the warp keeps those whose bbox
-// bit for its 8x4 block is set, and copies their 64-B records into a 2-deep ring of 32 slots
-// with cp.async.  Warps never wait on each other, so a warp with a short candidate list (or
-// whose pixels all terminated) does not hold the others back at per-batch barriers.
-struct WarpRing {
-    SplatRecord rec[2][32];
-    uint32_t id[2][32];
-    uint32_t lm[2][32];  // backward: lane mask of the pixels that blended the pair
-    uint32_t cm[2][32];  // backward: ... of the pixels whose weight was clamped
+// Warp-private candidate ring.  Each warp streams ITS OWN candidates from the tile's list:
+// list entries are read 32 at a time (key + surfel id), the warp keeps those whose bbox bit
+// for its 8x4 block is set, and copies their 64-B records into a 2-deep ring of 32 slots with
+// cp.async.  Warps never wait on each other, so a warp with a short candidate list (or whose
+// pixels all terminated) does not hold the others back at per-batch barriers.
+//
+// A slot is 80 B (record + meta): the 20-word stride keeps the lane-parallel 16-B accesses of
+// the fill and prep phases free of bank conflicts, and a slot's meta is one immediate offset
+// from its record.  The prep phase (lane-parallel, one slot per lane) rewrites an affine slot
+// so that the per-pixel offset needs no centre arithmetic (see block_centre).
+struct __align__(16) Slot {
+    SplatRecord r;
+    uint4 meta;  // (surfel id, blend lane mask, clamp lane mask, -) as loaded; see the kernels
 };
+struct WarpRing {
+    Slot s[2][32];
+};
+
+// Centre of the splat relative to the warp block's origin pixel (x0, y0), split so the
+// per-lane offsets are exact.  With the record centre c = c_hi + c_lo (float32 + half):
+//   f = c_hi - x0 is exact when |f| <= |c_hi| (both are multiples of ulp(c_hi)), i.e. except
+//   for splats centred within a footprint radius of the image's left / top edge, where it is
+//   off by at most ulp(f) / 2 (< 1e-6 px, inside the guard band's 1e-5 / sigma_min term),
+//   (lx - f) = x - c_hi then exactly (the value the per-pixel form x - c_hi rounds to),
+//   Minv (x - c) = Minv (lx - f, ly - g) - Minv c_lo, with lo = -Minv c_lo taken once per slot.
+// So u = A ex + (B ey + lo.x), v = C ex + (D ey + lo.y) with ex = lx - f, ey = ly - g carries the
+// rounding of the per-pixel form (no error shared by the whole block), and the forward and the
+// backward, calling the same code, evaluate bit-identical weights.
+struct BlockCentre {
+    float f, g;    // c_hi - (x0, y0)
+    float2 lo;     // -Minv (cx_lo, cy_lo)
+};
+__device__ __forceinline__ BlockCentre block_centre(const float4 &q0, const float4 &q1, float x0f, float y0f) {
+    const uint32_t lob = __float_as_uint(q0.z);
+    const __half2 h = *reinterpret_cast<const __half2 *>(&lob);
+    const float lx = __low2float(h), ly = __high2float(h);
+    BlockCentre b;
+    b.f = __fsub_rn(q0.x, x0f);
+    b.g = __fsub_rn(q0.y, y0f);
+    b.lo = make_float2(-__fmaf_rn(q1.x, lx, __fmul_rn(q1.y, ly)), -__fmaf_rn(q1.z, lx, __fmul_rn(q1.w, ly)));
+    return b;
+}
+
+// m = |Minv (p - c)|^2 at lane offset (lx, ly) from the block origin (block_centre), with the
+// whitened offset (u, v).
+__device__ __forceinline__ float slot_maha(float f, float g, float2 lo, const float4 &q1, float lxf, float lyf,
+                                           float &u, float &v) {
+    const float ex = __fsub_rn(lxf, f), ey = __fsub_rn(lyf, g);
+    u = __fmaf_rn(q1.x, ex, __fmaf_rn(q1.y, ey, lo.x));
+    v = __fmaf_rn(q1.z, ex, __fmaf_rn(q1.w, ey, lo.y));
+    return __fmaf_rn(u, u, __fmul_rn(v, v));
+}
 
 // Cursor over list positions [lo, hi).  The current 32-wide chunk starts at `cb` (lane l holds
 // position cb + l); `pend` = the chunk's hits not yet handed out, `nxt` = the prefetched next
@@ -190,7 +225,7 @@ __device__ __forceinline__ void cursor_init(ListCursor &c, const RasterArgs &a, 
     c.nxt = load_chunk(a, lo, c, lane);
 }
 
-// Fill ring slot `buf` with up to 32 candidates in list order (records by cp.async): the
+// Fill ring half `buf` with up to 32 candidates in list order (records by cp.async): the
 // entries whose bbox bit for this warp's block is set.  Returns how many.
 __device__ __forceinline__ int ring_fill(WarpRing &rg, int buf, ListCursor &c, const RasterArgs &a, int warp,
                                          int lane) {
@@ -211,14 +246,14 @@ __device__ __forceinline__ int ring_fill(WarpRing &rg, int buf, ListCursor &c, c
         const int rank = __popc(c.pend & lt);
         const bool mine = ((c.pend >> lane) & 1u) && rank < take;
         if (mine) {
-            const int s = n + rank;
+            Slot &sl = rg.s[buf][31 - (n + rank)];  // forward ring: list position j at index 31 - j
             const float4 *g = reinterpret_cast<const float4 *>(a.rec + c.kid);
-            float4 *d = reinterpret_cast<float4 *>(&rg.rec[buf][s]);
+            float4 *d = reinterpret_cast<float4 *>(&sl.r);
             cp_async16(d + 0, g + 0);
             cp_async16(d + 1, g + 1);
             cp_async16(d + 2, g + 2);
             cp_async16(d + 3, g + 3);
-            rg.id[buf][s] = c.kid;
+            sl.meta.x = c.kid;
         }
         c.pend &= ~__ballot_sync(kFull, mine);
         n += take;
@@ -227,21 +262,21 @@ __device__ __forceinline__ int ring_fill(WarpRing &rg, int buf, ListCursor &c, c
 }
 
 // Backward ring fill: entries [e0, e1) of the warp's blend stream, newest first (slot s holds
-// entry e1 - 1 - s).  Every entry is work, so this is one coalesced 8-B load per lane.
+// entry e1 - 1 - s).  Every entry is work, so this is one coalesced 16-B load per lane; the
+// entry itself is the slot's meta.
 __device__ __forceinline__ int stream_fill(WarpRing &rg, int buf, const uint4 *ws, int e0, int e1,
                                            const SplatRecord *rec, int lane) {
     const int n = min(32, e1 - e0);
     if (lane < n) {
         const uint4 en = __ldcg(ws + (e1 - 1 - lane));
+        Slot &sl = rg.s[buf][lane];
         const float4 *g = reinterpret_cast<const float4 *>(rec + en.x);
-        float4 *d = reinterpret_cast<float4 *>(&rg.rec[buf][lane]);
+        float4 *d = reinterpret_cast<float4 *>(&sl.r);
         cp_async16(d + 0, g + 0);
         cp_async16(d + 1, g + 1);
         cp_async16(d + 2, g + 2);
         cp_async16(d + 3, g + 3);
-        rg.id[buf][lane] = en.x;
-        rg.lm[buf][lane] = en.y;
-        rg.cm[buf][lane] = en.z;
+        sl.meta = en;
     }
     return n;
 }
@@ -257,13 +292,18 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
     const int px = wx0 + (lane & 7), py = wy0 + (lane >> 3);
     const bool inside = px < P.W && py < P.H;
     const float pxf = (float)px, pyf = (float)py;
+    const float kNaN = __int_as_float(0x7fffffff);
+    // affine mode: a terminated (or outside) lane carries lxf = NaN, so its m is NaN and fails
+    // the cut test; no per-candidate `done` test is needed
+    float lxf = inside ? (float)(lane & 7) : kNaN;
+    const float lyf = (float)(lane >> 3);
     const int2 rg = a.ranges[tile];
 
     float T = 1.0f;
     float c0 = 0.f, c1 = 0.f, c2 = 0.f, dep = 0.f, n0 = 0.f, n1 = 0.f, n2 = 0.f;
     float maxw = 0.f;
     int argw = -1, nblend = 0, guard = 0;
-    bool done = !inside;
+    bool done = !inside;  // ray mode
     const float term_t = P.term_t_f;
     WarpRing &ring = s_ring[warp];
 
@@ -282,60 +322,103 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
             cp_commit();
             cp_wait<1>();
             __syncwarp();
-            // lane-parallel ellipse cull of the staged candidates (ray mode: the bbox bits only)
-            uint32_t hm = __ballot_sync(kFull, lane < n && (kRay || block_reach(wx0, wy0, ring.rec[buf][lane],
-                                                                              P.maha_cut_f)));
-            // per lane, bit k of bl_bits / cl_bits: this pixel blended slot k / with a clamped
-            // weight; transposed into per-slot lane masks once per chunk
-            uint32_t bl_bits = 0u, cl_bits = 0u;
-            while (hm) {
-                const int k = __ffs(hm) - 1;
-                hm &= hm - 1;
-                const SplatRecord &r = ring.rec[buf][k];
-                float contrib = 0.f;
-                if (!done) {
-                    bool clamped = false;
-                    float w, zpix;
-                    if (kRay) {
-                        RayEval e;
-                        w = 0.f;
-                        const short4 bb = a.rect[ring.id[buf][k]];
-                        if (ray_eval(P, r, pxf - (float)bb.x, pyf - (float)bb.z, e)) {
-                            w = __fmul_rn(r.q0.w, e.g);
-                            clamped = w > P.w_clamp_f;
-                            w = clamped ? P.w_clamp_f : fmaxf(w, 0.f);
-                        }
-                        zpix = e.iS;
-                    } else {
-                        w = fwd_weight(P, a, r, ring.id[buf][k], pxf, pyf, px, py, clamped, guard);
-                        zpix = r.q2.w;
+            // prep phase, lane-parallel over the staged candidates (lane = slot): the exact
+            // ellipse cull against the block (ray mode: the bbox bits only) and, for the kept
+            // affine slots, the block-origin offset and cut thresholds (slot_prep comment above)
+            bool keep = false;
+            if (lane < n) {
+                Slot &sl = ring.s[buf][31 - lane];
+                if (kRay) {
+                    keep = true;
+                } else {
+                    const float4 q0 = sl.r.q0, q1 = sl.r.q1;
+                    const float gbs = sl.r.q3.w, gb = fabsf(gbs), op = q0.w;
+                    // a non-positive (or NaN) opacity never blends: w = op g <= 0 (or NaN) is
+                    // skipped by the reference and by guard_resolve's caller alike
+                    keep = op > 0.f && block_reach(wx0, wy0, sl.r, P.maha_cut_f);
+                    if (keep) {
+                        const BlockCentre bc = block_centre(q0, q1, (float)wx0, (float)wy0);
+                        const float thi = __fadd_rn(P.maha_cut_f, gb), tlo = __fsub_rn(P.maha_cut_f, gb);
+                        const bool slow = gbs < 0.f || !(op > 1e-30f);
+                        // forward slot: q0 = (f, g, cut + gb, opacity), q3.w = +-(cut - gb),
+                        // meta = (id, lo.x, lo.y, -)
+                        sl.r.q0 = make_float4(bc.f, bc.g, thi, op);
+                        sl.r.q3.w = slow ? -tlo : tlo;
+                        sl.meta.y = __float_as_uint(bc.lo.x);
+                        sl.meta.z = __float_as_uint(bc.lo.y);
                     }
-                    if (w > 0.f) {  // blend (blend_forward, _raster_kernels.py:47-55)
-                        bl_bits |= 1u << k;
-                        if (clamped) cl_bits |= 1u << k;
-                        contrib = w * T;
-                        const float4 q2 = r.q2;
-                        c0 = fmaf(contrib, q2.x, c0);
-                        c1 = fmaf(contrib, q2.y, c1);
-                        c2 = fmaf(contrib, q2.z, c2);
-                        dep = fmaf(contrib, zpix, dep);
-                        if (kNormal) {
-                            const float4 q3 = r.q3;
-                            n0 = fmaf(contrib, q3.x, n0);
-                            n1 = fmaf(contrib, q3.y, n1);
-                            n2 = fmaf(contrib, q3.z, n2);
+                }
+            }
+            // bit p of rm = ring index p = list position 31 - p, so the highest set bit is the
+            // next candidate in list order
+            uint32_t rm = __brev(__ballot_sync(kFull, keep));
+            __syncwarp();
+            // per lane, bit 31 - j of bl_bits / cl_bits: this pixel blended list position j / with a
+            // clamped weight; transposed into per-slot lane masks once per chunk
+            uint32_t bl_bits = 0u, cl_bits = 0u;
+            while (rm) {
+                const int k = 31 - __clz(rm);  // ring index
+                const uint32_t bit = 1u << k;
+                rm ^= bit;
+                const Slot &sl = ring.s[buf][k];
+                float contrib = 0.f;
+                // blend (blend_forward, _raster_kernels.py:47-55)
+                auto blend = [&](float w, float zpix) {
+                    bl_bits |= bit;
+                    contrib = w * T;
+                    const float4 q2 = sl.r.q2;
+                    c0 = fmaf(contrib, q2.x, c0);
+                    c1 = fmaf(contrib, q2.y, c1);
+                    c2 = fmaf(contrib, q2.z, c2);
+                    dep = fmaf(contrib, zpix, dep);
+                    if (kNormal) {
+                        const float4 q3 = sl.r.q3;
+                        n0 = fmaf(contrib, q3.x, n0);
+                        n1 = fmaf(contrib, q3.y, n1);
+                        n2 = fmaf(contrib, q3.z, n2);
+                    }
+                    if (kArg && contrib > maxw) {
+                        maxw = contrib;
+                        argw = (int)sl.meta.x;
+                    }
+                    T -= contrib;  // T (1 - w)
+                    if (kRay) done = T < term_t;
+                    else lxf = T < term_t ? kNaN : lxf;
+                };
+                if (kRay) {
+                    if (!done) {
+                        RayEval e;
+                        const short4 bb = a.rect[sl.meta.x];
+                        if (ray_eval(P, sl.r, pxf - (float)bb.x, pyf - (float)bb.z, e)) {
+                            float w = __fmul_rn(sl.r.q0.w, e.g);
+                            const bool clamped = w > P.w_clamp_f;
+                            w = clamped ? P.w_clamp_f : fmaxf(w, 0.f);
+                            if (clamped) cl_bits |= bit;
+                            if (w > 0.f) blend(w, e.iS);
                         }
-                        if (kArg && contrib > maxw) {
-                            maxw = contrib;
-                            argw = (int)ring.id[buf][k];
+                    }
+                } else {
+                    const float4 q0 = sl.r.q0, q1 = sl.r.q1;
+                    float u, v;
+                    const float m = slot_maha(q0.x, q0.y, make_float2(__uint_as_float(sl.meta.y),
+                                                                      __uint_as_float(sl.meta.z)),
+                                              q1, lxf, lyf, u, v);
+                    if (m <= q0.z) {  // else certainly outside the reference's cut
+                        float w = __fmul_rn(q0.w, fast_exp2(__fmul_rn(m, -0.72134752044448170368f)));
+                        const float tlo = sl.r.q3.w;
+                        bool ok = true;
+                        // fast path (m < cut - gb, unflagged slot): 0 < w < clamp, blends
+                        if (m >= tlo) {
+                            bool clamped = false;
+                            w = slow_weight(P, a, sl.meta.x, q0.w, m, w, tlo, px, py, clamped, guard);
+                            ok = w > 0.f;
+                            if (clamped) cl_bits |= bit;
                         }
-                        T = T * (1.0f - w);
-                        ++nblend;
-                        done = T < term_t;
+                        if (ok) blend(w, sl.r.q2.w);
                     }
                 }
                 if (kMaxW) {
-                    const uint32_t id = ring.id[buf][k];
+                    const uint32_t id = sl.meta.x;
                     float mx = contrib;
                     float mm = (a.mask != nullptr && inside && a.mask[py * P.W + px]) ? contrib : 0.f;
 #pragma unroll
@@ -350,17 +433,18 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
                     }
                 }
             }
-            // blend stream: lane k now holds slot k's masks; the slots some pixel blended are
+            nblend += __popc(bl_bits);
+            // blend stream: lane j now holds list position j's masks; the slots some pixel blended are
             // appended in slot (= list) order with one coalesced store
             {
-                const uint32_t bm = transpose32(bl_bits, lane);
-                const uint32_t cm = __any_sync(kFull, cl_bits != 0u) ? transpose32(cl_bits, lane) : 0u;
+                const uint32_t bm = transpose32(__brev(bl_bits), lane);
+                const uint32_t cm = __any_sync(kFull, cl_bits != 0u) ? transpose32(__brev(cl_bits), lane) : 0u;
                 const uint32_t has = __ballot_sync(kFull, bm != 0u);
-                if (bm != 0u) wp[__popc(has & lanemask_lt())] = make_uint4(ring.id[buf][lane], bm, cm, 0u);
+                if (bm != 0u) wp[__popc(has & lanemask_lt())] = make_uint4(ring.s[buf][31 - lane].meta.x, bm, cm, 0u);
                 wp += __popc(has);
                 wc += __popc(has);
             }
-            if (__all_sync(kFull, done)) break;
+            if (__all_sync(kFull, kRay ? done : lxf != lxf)) break;
             __syncwarp();  // slot `buf` is refilled by the next ring_fill
             buf ^= 1;
             n = nn;
@@ -464,6 +548,7 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
     const int px = wx0 + (lane & 7), py = wy0 + (lane >> 3);
     const bool inside = px < P.W && py < P.H;
     const float pxf = (float)px, pyf = (float)py;
+    const float lxf = (float)(lane & 7), lyf = (float)(lane >> 3);
     const int2 rg = a.ranges[tile];
     const int p = py * P.W + px;
 
@@ -564,100 +649,113 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
     float v[2 * NV];
     // one entry of the reverse traversal for this lane: updates the pixel state, writes the
     // entry's NV gradient values at v[off ...]
-    auto entry = [&](int sl, int off) {
-        if ((ring.lm[buf][sl] >> lane) & 1u) {
-            // the forward's arithmetic (fwd_weight / ray_eval), minus the decisions it took
-            const SplatRecord &r = ring.rec[buf][sl];
-            const bool clamped = (ring.cm[buf][sl] >> lane) & 1u;
-            const float4 q2 = r.q2;
-            float w, g, z;
-            float u = 0.f, vv = 0.f;  // affine: whitened offset
-            RayEval re;
-            const short4 bb = kRay ? a.rect[ring.id[buf][sl]] : make_short4(0, 0, 0, 0);
-            const float rx = pxf - (float)bb.x, ry = pyf - (float)bb.z;  // ray: offset from the bbox corner
-            if (kRay) {
-                ray_eval(P, r, rx, ry, re);  // blended in the forward: S > 0, m <= cut
-                g = re.g;
-                z = re.iS;
-                w = clamped ? P.w_clamp_f : __fmul_rn(r.q0.w, g);
-            } else {
-                const float4 q0 = r.q0, q1 = r.q1;
-                const uint32_t lob = __float_as_uint(q0.z);
-                const __half2 lo = *reinterpret_cast<const __half2 *>(&lob);
-                const float dx = __fsub_rn(__fsub_rn(pxf, q0.x), __low2float(lo));
-                const float dy = __fsub_rn(__fsub_rn(pyf, q0.y), __high2float(lo));
-                u = __fmaf_rn(q1.x, dx, __fmul_rn(q1.y, dy));
-                vv = __fmaf_rn(q1.z, dx, __fmul_rn(q1.w, dy));
-                const float m = __fmaf_rn(u, u, __fmul_rn(vv, vv));
-                g = fast_exp2(__fmul_rn(m, -0.72134752044448170368f));
-                z = q2.w;
-                w = clamped ? P.w_clamp_f : __fmul_rn(q0.w, g);
-            }
-            const float Ti = Tn * fast_rcp(1.0f - w);  // T before this contributor; w <= clamp < 1
-            Tn = Ti;
-            const float alpha = w * Ti;
-            v[off + 1] = gc0 * alpha;
-            v[off + 2] = gc1 * alpha;
-            v[off + 3] = gc2 * alpha;
-            // dL/dw = T_i [ G.(c - S) + gd (z - Sd) + Gn.(n - Sn) ] + ga T_i R
-            float dLdw = gc0 * (q2.x - S0) + gc1 * (q2.y - S1) + gc2 * (q2.z - S2) + gd * (z - Sd);
-            const float omw = 1.0f - w;
-            if (kExt) {
-                const float4 q3 = r.q3;
-                v[off + (kRay ? 13 : 10)] = gn0 * alpha;
-                v[off + (kRay ? 14 : 11)] = gn1 * alpha;
-                v[off + (kRay ? 15 : 12)] = gn2 * alpha;
-                dLdw += gn0 * (q3.x - Sn0) + gn1 * (q3.y - Sn1) + gn2 * (q3.z - Sn2) + ga * R;
-                Sn0 = w * q3.x + omw * Sn0;
-                Sn1 = w * q3.y + omw * Sn1;
-                Sn2 = w * q3.z + omw * Sn2;
-                R *= omw;
-            }
-            dLdw *= Ti;
-            if (kRay) {
-                // dL/d(U, V, S) with u = U/S, v = V/S, z = 1/S; then dL/dHi = g (x, y, 1)^T
-                float gU = 0.f, gV = 0.f;
-                float gS = -gd * alpha * z * z;
-                if (!clamped) {
-                    v[off + 0] = dLdw * g;
-                    const float gm2 = -w * dLdw * re.iS;  // 2 dL/dm / S
-                    gU = gm2 * re.u;
-                    gV = gm2 * re.v;
-                    gS -= gm2 * re.m;
-                }
-                // dL/dHi' in the bbox-corner frame (k_project_bwd shifts it back in float64)
-                v[off + 4] = gU * rx;
-                v[off + 5] = gU * ry;
-                v[off + 6] = gU;
-                v[off + 7] = gV * rx;
-                v[off + 8] = gV * ry;
-                v[off + 9] = gV;
-                v[off + 10] = gS * rx;
-                v[off + 11] = gS * ry;
-                v[off + 12] = gS;
-            } else {
-                v[off + 4] = gd * alpha;
-                if (!clamped) {
-                    v[off + 0] = dLdw * g;
-                    const float gm = -0.5f * w * dLdw;  // dL/dm
-                    v[off + 8] = gm * u;  // whitened offset w = (u, v)
-                    v[off + 9] = gm * vv;
-                    v[off + 5] = v[off + 8] * u;
-                    v[off + 6] = v[off + 8] * vv;
-                    v[off + 7] = v[off + 9] * vv;
-                }
-            }
-            S0 = w * q2.x + omw * S0;
-            S1 = w * q2.y + omw * S1;
-            S2 = w * q2.z + omw * S2;
-            Sd = w * z + omw * Sd;
+    auto entry = [&](int k, int off) {
+        const Slot &sl = ring.s[buf][k];
+        const uint2 mk = make_uint2(sl.meta.y, sl.meta.z);  // blend / clamp lane masks
+        // every lane runs the entry; lanes outside the blend mask take w = 0, which leaves
+        // their state unchanged and makes all their values 0
+        const bool inl = (mk.x >> lane) & 1u;
+        // the forward's arithmetic (k_raster_fwd / ray_eval), minus the decisions it took
+        const SplatRecord &r = sl.r;
+        const bool clamped = (mk.y >> lane) & 1u;
+        const float4 q2 = r.q2;
+        float w, g, z;
+        float u = 0.f, vv = 0.f;  // affine: whitened offset
+        RayEval re;
+        const short4 bb = kRay ? a.rect[sl.meta.x] : make_short4(0, 0, 0, 0);
+        const float rx = pxf - (float)bb.x, ry = pyf - (float)bb.z;  // ray: offset from the bbox corner
+        if (kRay) {
+            // blended in the forward: S > 0, m <= cut; the other lanes get finite zeros
+            const bool ok = ray_eval(P, r, rx, ry, re) && inl;
+            re.u = ok ? re.u : 0.f;
+            re.v = ok ? re.v : 0.f;
+            re.m = ok ? re.m : 0.f;
+            re.iS = ok ? re.iS : 0.f;
+            g = ok ? re.g : 0.f;
+            z = re.iS;
+            w = clamped ? P.w_clamp_f : __fmul_rn(r.q0.w, g);
+        } else {
+            // backward slot: q0 = (f, g, lo.x, opacity), meta.w = lo.y
+            const float4 q0 = r.q0, q1 = r.q1;
+            const float m = slot_maha(q0.x, q0.y, make_float2(q0.z, __uint_as_float(sl.meta.w)), q1, lxf,
+                                      lyf, u, vv);
+            // lanes outside the mask: keep (u, v) finite (a near-singular Minv could overflow
+            // them far from the splat), so their zero gradient values stay zeros
+            u = inl ? u : 0.f;
+            vv = inl ? vv : 0.f;
+            g = fast_exp2(__fmul_rn(m, -0.72134752044448170368f));
+            z = q2.w;
+            w = clamped ? P.w_clamp_f : __fmul_rn(q0.w, g);
         }
+        w = inl ? w : 0.f;
+        const float Ti = inl ? Tn * fast_rcp(1.0f - w) : Tn;
+        Tn = Ti;
+        const float alpha = w * Ti;
+        v[off + 1] = gc0 * alpha;
+        v[off + 2] = gc1 * alpha;
+        v[off + 3] = gc2 * alpha;
+        // dL/dw = T_i [ G.(c - S) + gd (z - Sd) + Gn.(n - Sn) ] + ga T_i R; the differences
+        // (c - S) also update the suffix: S <- w c + (1 - w) S = S + w (c - S)
+        const float d0 = q2.x - S0, d1 = q2.y - S1, d2 = q2.z - S2, dd = z - Sd;
+        float dLdw = gc0 * d0 + gc1 * d1 + gc2 * d2 + gd * dd;
+        if (kExt) {
+            const float4 q3 = r.q3;
+            v[off + (kRay ? 13 : 10)] = gn0 * alpha;
+            v[off + (kRay ? 14 : 11)] = gn1 * alpha;
+            v[off + (kRay ? 15 : 12)] = gn2 * alpha;
+            const float e0 = q3.x - Sn0, e1 = q3.y - Sn1, e2 = q3.z - Sn2;
+            dLdw += gn0 * e0 + gn1 * e1 + gn2 * e2 + ga * R;
+            Sn0 = fmaf(w, e0, Sn0);
+            Sn1 = fmaf(w, e1, Sn1);
+            Sn2 = fmaf(w, e2, Sn2);
+            R *= 1.0f - w;
+        }
+        dLdw *= Ti;
+        // clamped weights (and lanes outside the mask) carry no opacity / geometry gradient
+        const float dg = (clamped || !inl) ? 0.f : dLdw;
+        if (kRay) {
+            const float gm2 = -w * dg * re.iS;  // 2 dL/dm / S
+            const float gU = gm2 * re.u, gV = gm2 * re.v;
+            const float gS = -gd * alpha * z * z - gm2 * re.m;
+            v[off + 0] = dg * g;
+            v[off + 4] = gU * rx;
+            v[off + 5] = gU * ry;
+            v[off + 6] = gU;
+            v[off + 7] = gV * rx;
+            v[off + 8] = gV * ry;
+            v[off + 9] = gV;
+            v[off + 10] = gS * rx;
+            v[off + 11] = gS * ry;
+            v[off + 12] = gS;
+        } else {
+            v[off + 4] = gd * alpha;
+            v[off + 0] = dg * g;
+            const float gm = -0.5f * w * dg;  // dL/dm
+            v[off + 8] = gm * u;
+            v[off + 9] = gm * vv;
+            v[off + 5] = v[off + 8] * u;
+            v[off + 6] = v[off + 8] * vv;
+            v[off + 7] = v[off + 9] * vv;
+        }
+        S0 = fmaf(w, d0, S0);
+        S1 = fmaf(w, d1, S1);
+        S2 = fmaf(w, d2, S2);
+        Sd = fmaf(w, dd, Sd);
     };
     while (n > 0) {
         const int nn = stream_fill(ring, buf ^ 1, ws, max(e1 - 32, 0), e1, a.rec, lane);
         e1 -= nn;
         cp_commit();
         cp_wait<1>();
+        __syncwarp();
+        if (!kRay && lane < n) {  // prep: block-relative centre, as the forward computed it
+            Slot &sl = ring.s[buf][lane];
+            const BlockCentre bc = block_centre(sl.r.q0, sl.r.q1, (float)wx0, (float)wy0);
+            sl.r.q0.x = bc.f;
+            sl.r.q0.y = bc.g;
+            sl.r.q0.z = bc.lo.x;
+            sl.meta.w = __float_as_uint(bc.lo.y);
+        }
         __syncwarp();
         for (int s = 0; s < n; s += 2) {
             const bool two = s + 1 < n;
@@ -667,7 +765,7 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
             if (two) entry(s + 1, NV);
             red_stage<2 * NV, 16>(v, lane);
             if (own && v[0] != 0.f && (!second || two))
-                atomicAdd(a.grad2d + (size_t)ring.id[buf][second ? s + 1 : s] * 16 + col, v[0]);
+                atomicAdd(a.grad2d + (size_t)ring.s[buf][second ? s + 1 : s].meta.x * 16 + col, v[0]);
         }
         __syncwarp();  // slot `buf` is refilled by the next ring_fill
         buf ^= 1;
