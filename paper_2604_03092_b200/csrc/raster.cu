@@ -39,6 +39,9 @@
 #ifndef S2D_BWD_MINB
 #define S2D_BWD_MINB 3
 #endif
+#ifndef S2D_BWD_HALVES
+#define S2D_BWD_HALVES 1
+#endif
 
 namespace s2d {
 
@@ -441,6 +444,13 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
                 const uint32_t cm = __any_sync(kFull, cl_bits != 0u) ? transpose32(__brev(cl_bits), lane) : 0u;
                 const uint32_t has = __ballot_sync(kFull, bm != 0u);
                 if (bm != 0u) wp[__popc(has & lanemask_lt())] = make_uint4(ring.s[buf][31 - lane].meta.x, bm, cm, 0u);
+#ifdef S2D_DIAG  // blend-stream statistics (tools/diag_stats.py); repurposes three counters
+                if (bm != 0u) {
+                    atomicAdd(&a.stats->guard_hits, ((bm & 0x0F0F0F0Fu) && (bm & 0xF0F0F0F0u)) ? 1 : 0);
+                    atomicAdd(&a.stats->degenerate, ((bm & 0x0000FFFFu) && (bm & 0xFFFF0000u)) ? 1 : 0);
+                    atomicAdd(&a.stats->pairs_stored, __popc(bm));
+                }
+#endif
                 wp += __popc(has);
                 wc += __popc(has);
             }
@@ -485,10 +495,13 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
 
 // Transposed warp reduction of C per-lane values (C <= 32): at each butterfly stage the
 // lanes exchange half of their values, so the whole reduction costs about C shuffles
-// instead of 5 C.  Afterwards every lane's v[0] is the warp sum of one value; red_map
-// (run once per kernel) says which value (vi) and whether this lane owns it (each value
-// is owned by exactly one lane).
-template <int C, int O, int NA>
+// instead of 5 C.  Afterwards every lane's v[0] is the sum of one value; red_map (run once
+// per kernel) says which value (vi) and whether this lane owns it (each value is owned by
+// exactly one lane).  kHalf: reduce within the two column halves of the 8x4 block (lanes
+// with lane bit 2 clear / set) separately, i.e. butterfly offsets 16, 8, 2, 1.
+__host__ __device__ constexpr int red_next(int O, bool half) { return (half && O == 8) ? 2 : O / 2; }
+
+template <int C, int O, bool kHalf, int NA>
 __device__ __forceinline__ void red_stage(float (&v)[NA], int lane) {
     constexpr int H = (C + 1) / 2, F = C / 2;
     const bool up = lane & O;
@@ -499,10 +512,10 @@ __device__ __forceinline__ void red_stage(float (&v)[NA], int lane) {
         v[j] = keep + __shfl_xor_sync(kFull, send, O);
     }
     if constexpr (H > F) v[F] += __shfl_xor_sync(kFull, v[F], O);
-    if constexpr (O > 1) red_stage<H, O / 2, NA>(v, lane);
+    if constexpr (O > 1) red_stage<H, red_next(O, kHalf), kHalf, NA>(v, lane);
 }
 
-template <int C, int O>
+template <int C, int O, bool kHalf>
 __device__ __forceinline__ void map_stage(int (&ix)[32], bool (&own)[32], int lane) {
     constexpr int H = (C + 1) / 2, F = C / 2;
     const bool up = lane & O;
@@ -517,10 +530,10 @@ __device__ __forceinline__ void map_stage(int (&ix)[32], bool (&own)[32], int la
         const bool pown = __shfl_xor_sync(kFull, (int)own[F], O) != 0;  // every lane shuffles
         own[F] = own[F] && pown && !up;
     }
-    if constexpr (O > 1) map_stage<H, O / 2>(ix, own, lane);
+    if constexpr (O > 1) map_stage<H, red_next(O, kHalf), kHalf>(ix, own, lane);
 }
 
-template <int C>
+template <int C, bool kHalf>
 __device__ __forceinline__ void red_map(int lane, int &vi, bool &own) {
     int ix[32];
     bool ow[32];
@@ -529,7 +542,7 @@ __device__ __forceinline__ void red_map(int lane, int &vi, bool &own) {
         ix[j] = j;
         ow[j] = true;
     }
-    map_stage<C, 16>(ix, ow, lane);
+    map_stage<C, 16, kHalf>(ix, ow, lane);
     vi = ix[0];
     own = ow[0];
 }
@@ -630,13 +643,23 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
     // with w = (u, v) = Minv d the whitened pixel offset (dL/dMinv = 2 K M^T and
     // dL/dcentre = -2 Minv^T e are formed in k_project_bwd).
     constexpr int NV = kRay ? (kExt ? 16 : 13) : (kExt ? 13 : 10);
+#if S2D_BWD_HALVES
+    // the two column halves of the block (lane bit 2 clear / set) walk the stream entries that
+    // touch them independently, one entry per half per step; each half reduces its NV values
+    // over its 16 lanes (transposed, offsets 16, 8, 2, 1); lane ownership fixed per kernel
+    constexpr int NR = NV;
+#else
     // two entries per step: their 2 NV values share one transposed reduction (about 2 NV
     // shuffles instead of 2 x (NV + 2)); lane ownership of the 2 NV sums is fixed per kernel
+    constexpr int NR = 2 * NV;
+#endif
     int vi;
     bool own;
-    red_map<2 * NV>(lane, vi, own);
+    red_map<NR, S2D_BWD_HALVES != 0>(lane, vi, own);
+#if !S2D_BWD_HALVES
     const bool second = vi >= NV;        // this lane's sum belongs to the older entry of the pair
     const int col = second ? vi - NV : vi;
+#endif
     float R = 1.f;     // prod_{j later} (1 - w_j)
     float S0 = 0.f, S1 = 0.f, S2 = 0.f, Sd = 0.f, Sn0 = 0.f, Sn1 = 0.f, Sn2 = 0.f;
     WarpRing &ring = s_ring[warp];
@@ -646,15 +669,15 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
     int n = stream_fill(ring, 0, ws, max(e1 - 32, 0), e1, a.rec, lane);
     e1 -= n;
     cp_commit();
-    float v[2 * NV];
+    float v[NR];
     // one entry of the reverse traversal for this lane: updates the pixel state, writes the
     // entry's NV gradient values at v[off ...]
-    auto entry = [&](int k, int off) {
+    auto entry = [&](int k, bool act, int off) {
         const Slot &sl = ring.s[buf][k];
         const uint2 mk = make_uint2(sl.meta.y, sl.meta.z);  // blend / clamp lane masks
-        // every lane runs the entry; lanes outside the blend mask take w = 0, which leaves
-        // their state unchanged and makes all their values 0
-        const bool inl = (mk.x >> lane) & 1u;
+        // every lane runs the entry; lanes outside the blend mask (or without an entry this
+        // step, !act) take w = 0, which leaves their state unchanged and makes their values 0
+        const bool inl = act && ((mk.x >> lane) & 1u);
         // the forward's arithmetic (k_raster_fwd / ray_eval), minus the decisions it took
         const SplatRecord &r = sl.r;
         const bool clamped = (mk.y >> lane) & 1u;
@@ -748,25 +771,47 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
         cp_commit();
         cp_wait<1>();
         __syncwarp();
-        if (!kRay && lane < n) {  // prep: block-relative centre, as the forward computed it
+        uint32_t lmv = 0u;  // lane = slot: the slot's blend lane mask
+        if (lane < n) {     // prep: block-relative centre, as the forward computed it
             Slot &sl = ring.s[buf][lane];
-            const BlockCentre bc = block_centre(sl.r.q0, sl.r.q1, (float)wx0, (float)wy0);
-            sl.r.q0.x = bc.f;
-            sl.r.q0.y = bc.g;
-            sl.r.q0.z = bc.lo.x;
-            sl.meta.w = __float_as_uint(bc.lo.y);
+            lmv = sl.meta.y;
+            if (!kRay) {
+                const BlockCentre bc = block_centre(sl.r.q0, sl.r.q1, (float)wx0, (float)wy0);
+                sl.r.q0.x = bc.f;
+                sl.r.q0.y = bc.g;
+                sl.r.q0.z = bc.lo.x;
+                sl.meta.w = __float_as_uint(bc.lo.y);
+            }
         }
+#if S2D_BWD_HALVES
+        // per half, the slots (newest first) whose mask touches it
+        const uint32_t p0 = __ballot_sync(kFull, (lmv & 0x0F0F0F0Fu) != 0u);
+        const uint32_t p1 = __ballot_sync(kFull, (lmv & 0xF0F0F0F0u) != 0u);
+        __syncwarp();
+        uint32_t pm = (lane & 4) ? p1 : p0;
+        const int steps = max(__popc(p0), __popc(p1));
+        for (int it = 0; it < steps; ++it) {
+            const bool act = pm != 0u;
+            const int k = act ? __ffs(pm) - 1 : 0;
+            pm &= pm - 1u;
+            entry(k, act, 0);
+            red_stage<NV, 16, true>(v, lane);
+            if (own && act && v[0] != 0.f) atomicAdd(a.grad2d + (size_t)ring.s[buf][k].meta.x * 16 + vi, v[0]);
+        }
+#else
+        (void)lmv;
         __syncwarp();
         for (int s = 0; s < n; s += 2) {
             const bool two = s + 1 < n;
 #pragma unroll
             for (int t = 0; t < 2 * NV; ++t) v[t] = 0.f;
-            entry(s, 0);
-            if (two) entry(s + 1, NV);
-            red_stage<2 * NV, 16>(v, lane);
+            entry(s, true, 0);
+            if (two) entry(s + 1, true, NV);
+            red_stage<2 * NV, 16, false>(v, lane);
             if (own && v[0] != 0.f && (!second || two))
                 atomicAdd(a.grad2d + (size_t)ring.s[buf][second ? s + 1 : s].meta.x * 16 + col, v[0]);
         }
+#endif
         __syncwarp();  // slot `buf` is refilled by the next ring_fill
         buf ^= 1;
         n = nn;
