@@ -264,15 +264,15 @@ __device__ __forceinline__ int ring_fill(WarpRing &rg, int buf, ListCursor &c, c
     return n;
 }
 
-// Backward ring fill: entries [e0, e1) of the warp's blend stream, newest first (slot s holds
-// entry e1 - 1 - s).  Every entry is work, so this is one coalesced 16-B load per lane; the
+// Backward ring fill: entries [e0, e1) of the warp's blend stream, newest first (ring index
+// 31 - j holds entry e1 - 1 - j).  Every entry is work, so this is one coalesced 16-B load per lane; the
 // entry itself is the slot's meta.
 __device__ __forceinline__ int stream_fill(WarpRing &rg, int buf, const uint4 *ws, int e0, int e1,
                                            const SplatRecord *rec, int lane) {
     const int n = min(32, e1 - e0);
     if (lane < n) {
         const uint4 en = __ldcg(ws + (e1 - 1 - lane));
-        Slot &sl = rg.s[buf][lane];
+        Slot &sl = rg.s[buf][31 - lane];  // entry e1 - 1 - j at ring index 31 - j
         const float4 *g = reinterpret_cast<const float4 *>(rec + en.x);
         float4 *d = reinterpret_cast<float4 *>(&sl.r);
         cp_async16(d + 0, g + 0);
@@ -656,9 +656,11 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
     int vi;
     bool own;
     red_map<NR, S2D_BWD_HALVES != 0>(lane, vi, own);
-#if !S2D_BWD_HALVES
+#if S2D_BWD_HALVES
+    float *const gcol = a.grad2d + vi;  // this lane's gradient column (when it owns a sum)
+#else
     const bool second = vi >= NV;        // this lane's sum belongs to the older entry of the pair
-    const int col = second ? vi - NV : vi;
+    float *const gcol = a.grad2d + (second ? vi - NV : vi);
 #endif
     float R = 1.f;     // prod_{j later} (1 - w_j)
     float S0 = 0.f, S1 = 0.f, S2 = 0.f, Sd = 0.f, Sn0 = 0.f, Sn1 = 0.f, Sn2 = 0.f;
@@ -672,9 +674,10 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
     float v[NR];
     // one entry of the reverse traversal for this lane: updates the pixel state, writes the
     // entry's NV gradient values at v[off ...]
-    auto entry = [&](int k, bool act, int off) {
+    auto entry = [&](int k, bool act, int off) -> uint32_t {
         const Slot &sl = ring.s[buf][k];
-        const uint2 mk = make_uint2(sl.meta.y, sl.meta.z);  // blend / clamp lane masks
+        const uint4 meta = sl.meta;  // (surfel id, blend / clamp lane masks, lo.y)
+        const uint2 mk = make_uint2(meta.y, meta.z);
         // every lane runs the entry; lanes outside the blend mask (or without an entry this
         // step, !act) take w = 0, which leaves their state unchanged and makes their values 0
         const bool inl = act && ((mk.x >> lane) & 1u);
@@ -700,7 +703,7 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
         } else {
             // backward slot: q0 = (f, g, lo.x, opacity), meta.w = lo.y
             const float4 q0 = r.q0, q1 = r.q1;
-            const float m = slot_maha(q0.x, q0.y, make_float2(q0.z, __uint_as_float(sl.meta.w)), q1, lxf,
+            const float m = slot_maha(q0.x, q0.y, make_float2(q0.z, __uint_as_float(meta.w)), q1, lxf,
                                       lyf, u, vv);
             // lanes outside the mask: keep (u, v) finite (a near-singular Minv could overflow
             // them far from the splat), so their zero gradient values stay zeros
@@ -764,6 +767,7 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
         S1 = fmaf(w, d1, S1);
         S2 = fmaf(w, d2, S2);
         Sd = fmaf(w, dd, Sd);
+        return meta.x;
     };
     while (n > 0) {
         const int nn = stream_fill(ring, buf ^ 1, ws, max(e1 - 32, 0), e1, a.rec, lane);
@@ -771,9 +775,9 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
         cp_commit();
         cp_wait<1>();
         __syncwarp();
-        uint32_t lmv = 0u;  // lane = slot: the slot's blend lane mask
+        uint32_t lmv = 0u;  // lane j: the blend lane mask of the j-th newest entry
         if (lane < n) {     // prep: block-relative centre, as the forward computed it
-            Slot &sl = ring.s[buf][lane];
+            Slot &sl = ring.s[buf][31 - lane];
             lmv = sl.meta.y;
             if (!kRay) {
                 const BlockCentre bc = block_centre(sl.r.q0, sl.r.q1, (float)wx0, (float)wy0);
@@ -784,19 +788,20 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
             }
         }
 #if S2D_BWD_HALVES
-        // per half, the slots (newest first) whose mask touches it
-        const uint32_t p0 = __ballot_sync(kFull, (lmv & 0x0F0F0F0Fu) != 0u);
-        const uint32_t p1 = __ballot_sync(kFull, (lmv & 0xF0F0F0F0u) != 0u);
+        // per half, the ring indices whose entry's mask touches it (bit 31 - j: j-th newest, so
+        // the highest set bit is the next entry in reverse order)
+        const uint32_t p0 = __brev(__ballot_sync(kFull, (lmv & 0x0F0F0F0Fu) != 0u));
+        const uint32_t p1 = __brev(__ballot_sync(kFull, (lmv & 0xF0F0F0F0u) != 0u));
         __syncwarp();
         uint32_t pm = (lane & 4) ? p1 : p0;
         const int steps = max(__popc(p0), __popc(p1));
         for (int it = 0; it < steps; ++it) {
             const bool act = pm != 0u;
-            const int k = act ? __ffs(pm) - 1 : 0;
-            pm &= pm - 1u;
-            entry(k, act, 0);
+            const int k = act ? 31 - __clz(pm) : 31;  // idle half: the newest entry (always loaded)
+            pm ^= act ? 1u << k : 0u;
+            const uint32_t id = entry(k, act, 0);
             red_stage<NV, 16, true>(v, lane);
-            if (own && act && v[0] != 0.f) atomicAdd(a.grad2d + (size_t)ring.s[buf][k].meta.x * 16 + vi, v[0]);
+            if (own && act && v[0] != 0.f) atomicAdd(gcol + (size_t)id * 16, v[0]);
         }
 #else
         (void)lmv;
@@ -805,11 +810,10 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
             const bool two = s + 1 < n;
 #pragma unroll
             for (int t = 0; t < 2 * NV; ++t) v[t] = 0.f;
-            entry(s, true, 0);
-            if (two) entry(s + 1, true, NV);
+            const uint32_t ida = entry(31 - s, true, 0);
+            const uint32_t idb = two ? entry(30 - s, true, NV) : 0u;
             red_stage<2 * NV, 16, false>(v, lane);
-            if (own && v[0] != 0.f && (!second || two))
-                atomicAdd(a.grad2d + (size_t)ring.s[buf][second ? s + 1 : s].meta.x * 16 + col, v[0]);
+            if (own && v[0] != 0.f && (!second || two)) atomicAdd(gcol + (size_t)(second ? idb : ida) * 16, v[0]);
         }
 #endif
         __syncwarp();  // slot `buf` is refilled by the next ring_fill

@@ -1,1 +1,2 @@
-timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:"k_raster" -c 2 -o gpurun_out/h1_full python tools/profile_view.py > gpurun_out/h1_ncu.log 2>&1; echo "ncu rc=$?"
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/n7_pytest.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/n7_pytest.log
+bash tools/ab.sh default
