@@ -444,13 +444,6 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
                 const uint32_t cm = __any_sync(kFull, cl_bits != 0u) ? transpose32(__brev(cl_bits), lane) : 0u;
                 const uint32_t has = __ballot_sync(kFull, bm != 0u);
                 if (bm != 0u) wp[__popc(has & lanemask_lt())] = make_uint4(ring.s[buf][31 - lane].meta.x, bm, cm, 0u);
-#ifdef S2D_DIAG  // blend-stream statistics (tools/diag_stats.py); repurposes three counters
-                if (bm != 0u) {
-                    atomicAdd(&a.stats->guard_hits, ((bm & 0x0F0F0F0Fu) && (bm & 0xF0F0F0F0u)) ? 1 : 0);
-                    atomicAdd(&a.stats->degenerate, ((bm & 0x0000FFFFu) && (bm & 0xFFFF0000u)) ? 1 : 0);
-                    atomicAdd(&a.stats->pairs_stored, __popc(bm));
-                }
-#endif
                 wp += __popc(has);
                 wc += __popc(has);
             }
@@ -795,6 +788,21 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
         __syncwarp();
         uint32_t pm = (lane & 4) ? p1 : p0;
         const int steps = max(__popc(p0), __popc(p1));
+#ifdef S2D_DIAG  // step counts of alternative splits (tools/diag_stats.py)
+        {
+            int rq = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) rq = max(rq, __popc(__ballot_sync(kFull, (lmv & (0xFFu << (8 * q))) != 0u)));
+            const int rh = max(__popc(__ballot_sync(kFull, (lmv & 0xFFFFu) != 0u)),
+                               __popc(__ballot_sync(kFull, (lmv & 0xFFFF0000u) != 0u)));
+            if (lane == 0) {
+                atomicAdd(&a.stats->guard_hits, steps);
+                atomicAdd(&a.stats->degenerate, rq);
+                atomicAdd(&a.stats->pairs_stored, n);
+                atomicAdd(&a.stats->n_mask, rh);
+            }
+        }
+#endif
         for (int it = 0; it < steps; ++it) {
             const bool act = pm != 0u;
             const int k = act ? 31 - __clz(pm) : 31;  // idle half: the newest entry (always loaded)

@@ -1,4 +1,6 @@
-"""Blend-stream statistics of one config-4 view (diagnostic build only: -DS2D_DIAG)."""
+"""Backward step statistics of one config-4 view (diagnostic build only: -DS2D_DIAG): guard_hits =
+steps of the column-half split, degenerate = steps of a row-quarter split, n_mask = steps of a row-half
+split, pairs_stored = entries (the counters are repurposed in that build)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
