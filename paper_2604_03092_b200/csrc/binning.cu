@@ -79,8 +79,10 @@ __device__ __forceinline__ bool clearly_out(const ViewParams &P, const ParamView
     // centre x range over the z / x uncertainty (fx > 0)
     const float xl = p[0] - slack, xh = p[0] + slack, yl = p[1] - slack, yh = p[1] + slack;
     const float fx = (float)P.fx, fy = (float)P.fy;
-    const float cxl = fx * fminf(xl / zl, xl / zh) + (float)P.cx, cxh = fx * fmaxf(xh / zl, xh / zh) + (float)P.cx;
-    const float cyl = fy * fminf(yl / zl, yl / zh) + (float)P.cy, cyh = fy * fmaxf(yh / zl, yh / zh) + (float)P.cy;
+    // approximate quotients (2 ulp) are far inside the 1e-3 relative tolerance below
+    const float izl = __frcp_rn(zl), izh = __frcp_rn(zh);
+    const float cxl = fx * fminf(xl * izl, xl * izh) + (float)P.cx, cxh = fx * fmaxf(xh * izl, xh * izh) + (float)P.cx;
+    const float cyl = fy * fminf(yl * izl, yl * izh) + (float)P.cy, cyh = fy * fmaxf(yh * izl, yh * izh) + (float)P.cy;
     const float tol = 1e-3f * (fabsf(cxl) + fabsf(cxh) + fabsf(cyl) + fabsf(cyh) + 1.f);
     return cxh + tol < -(float)P.mx || cxl - tol > (float)P.wmax || cyh + tol < -(float)P.my ||
            cyl - tol > (float)P.hmax;

@@ -39,8 +39,8 @@
 #ifndef S2D_BWD_MINB
 #define S2D_BWD_MINB 3
 #endif
-#ifndef S2D_BWD_HALVES
-#define S2D_BWD_HALVES 1
+#ifndef S2D_BWD_GROUPS  // lane groups walking the blend stream independently: 1, 2 or 4
+#define S2D_BWD_GROUPS 2
 #endif
 
 namespace s2d {
@@ -488,13 +488,25 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
 
 // Transposed warp reduction of C per-lane values (C <= 32): at each butterfly stage the
 // lanes exchange half of their values, so the whole reduction costs about C shuffles
-// instead of 5 C.  Afterwards every lane's v[0] is the sum of one value; red_map (run once
-// per kernel) says which value (vi) and whether this lane owns it (each value is owned by
-// exactly one lane).  kHalf: reduce within the two column halves of the 8x4 block (lanes
-// with lane bit 2 clear / set) separately, i.e. butterfly offsets 16, 8, 2, 1.
-__host__ __device__ constexpr int red_next(int O, bool half) { return (half && O == 8) ? 2 : O / 2; }
+// instead of 5 C.  kMode picks the lane groups reduced separately and the butterfly offsets:
+//   0: the whole warp (16, 8, 4, 2, 1);
+//   1: the two column halves of the 8x4 block, lane bit 2 clear / set (16, 8, 2, 1);
+//   2: the four rows of the block, lanes 8r .. 8r + 7 (4, 2, 1).
+// Afterwards each lane holds red_final(C, kMode) sums v[0 ..]; red_map (run once per kernel)
+// says which value each is (vi) and whether this lane owns it (each value of each group is
+// owned by exactly one lane of the group).
+__host__ __device__ constexpr int red_next(int O, int mode) { return (mode == 1 && O == 8) ? 2 : O / 2; }
+__host__ __device__ constexpr int red_first(int mode) { return mode == 2 ? 4 : 16; }
+__host__ __device__ constexpr int red_final(int C, int mode) {
+    int O = red_first(mode);
+    while (O >= 1) {
+        C = (C + 1) / 2;
+        O = red_next(O, mode);
+    }
+    return C;
+}
 
-template <int C, int O, bool kHalf, int NA>
+template <int C, int O, int kMode, int NA>
 __device__ __forceinline__ void red_stage(float (&v)[NA], int lane) {
     constexpr int H = (C + 1) / 2, F = C / 2;
     const bool up = lane & O;
@@ -505,10 +517,10 @@ __device__ __forceinline__ void red_stage(float (&v)[NA], int lane) {
         v[j] = keep + __shfl_xor_sync(kFull, send, O);
     }
     if constexpr (H > F) v[F] += __shfl_xor_sync(kFull, v[F], O);
-    if constexpr (O > 1) red_stage<H, red_next(O, kHalf), kHalf, NA>(v, lane);
+    if constexpr (O > 1) red_stage<H, red_next(O, kMode), kMode, NA>(v, lane);
 }
 
-template <int C, int O, bool kHalf>
+template <int C, int O, int kMode>
 __device__ __forceinline__ void map_stage(int (&ix)[32], bool (&own)[32], int lane) {
     constexpr int H = (C + 1) / 2, F = C / 2;
     const bool up = lane & O;
@@ -523,11 +535,11 @@ __device__ __forceinline__ void map_stage(int (&ix)[32], bool (&own)[32], int la
         const bool pown = __shfl_xor_sync(kFull, (int)own[F], O) != 0;  // every lane shuffles
         own[F] = own[F] && pown && !up;
     }
-    if constexpr (O > 1) map_stage<H, red_next(O, kHalf), kHalf>(ix, own, lane);
+    if constexpr (O > 1) map_stage<H, red_next(O, kMode), kMode>(ix, own, lane);
 }
 
-template <int C, bool kHalf>
-__device__ __forceinline__ void red_map(int lane, int &vi, bool &own) {
+template <int C, int kMode, int RF>
+__device__ __forceinline__ void red_map(int lane, int (&vi)[RF], bool (&own)[RF]) {
     int ix[32];
     bool ow[32];
 #pragma unroll
@@ -535,9 +547,12 @@ __device__ __forceinline__ void red_map(int lane, int &vi, bool &own) {
         ix[j] = j;
         ow[j] = true;
     }
-    map_stage<C, 16, kHalf>(ix, ow, lane);
-    vi = ix[0];
-    own = ow[0];
+    map_stage<C, red_first(kMode), kMode>(ix, ow, lane);
+#pragma unroll
+    for (int t = 0; t < RF; ++t) {
+        vi[t] = ix[t];
+        own[t] = ow[t];
+    }
 }
 
 __device__ __forceinline__ float sgnf(float x) { return x > 0.f ? 1.f : (x < 0.f ? -1.f : 0.f); }
@@ -636,24 +651,25 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
     // with w = (u, v) = Minv d the whitened pixel offset (dL/dMinv = 2 K M^T and
     // dL/dcentre = -2 Minv^T e are formed in k_project_bwd).
     constexpr int NV = kRay ? (kExt ? 16 : 13) : (kExt ? 13 : 10);
-#if S2D_BWD_HALVES
-    // the two column halves of the block (lane bit 2 clear / set) walk the stream entries that
-    // touch them independently, one entry per half per step; each half reduces its NV values
-    // over its 16 lanes (transposed, offsets 16, 8, 2, 1); lane ownership fixed per kernel
-    constexpr int NR = NV;
+#if S2D_BWD_GROUPS > 1
+    // the lane groups of the block (4: its rows; 2: its column halves) walk the stream entries
+    // that touch them independently, one entry per group per step; each group reduces its NV
+    // values over its lanes (transposed); lane ownership of the sums is fixed per kernel
+    constexpr int kMode = S2D_BWD_GROUPS == 4 ? 2 : 1, NR = NV;
 #else
     // two entries per step: their 2 NV values share one transposed reduction (about 2 NV
     // shuffles instead of 2 x (NV + 2)); lane ownership of the 2 NV sums is fixed per kernel
-    constexpr int NR = 2 * NV;
+    constexpr int kMode = 0, NR = 2 * NV;
 #endif
-    int vi;
-    bool own;
-    red_map<NR, S2D_BWD_HALVES != 0>(lane, vi, own);
-#if S2D_BWD_HALVES
-    float *const gcol = a.grad2d + vi;  // this lane's gradient column (when it owns a sum)
-#else
-    const bool second = vi >= NV;        // this lane's sum belongs to the older entry of the pair
-    float *const gcol = a.grad2d + (second ? vi - NV : vi);
+    constexpr int RF = red_final(NR, kMode);  // sums held per lane after the reduction
+    int vi[RF];
+    bool own[RF];
+    red_map<NR, kMode>(lane, vi, own);
+    float *gcol[RF];  // this lane's gradient columns (where it owns a sum)
+#pragma unroll
+    for (int t = 0; t < RF; ++t) gcol[t] = a.grad2d + (vi[t] >= NV ? vi[t] - NV : vi[t]);
+#if S2D_BWD_GROUPS == 1
+    const bool second = vi[0] >= NV;  // this lane's sum belongs to the older entry of the pair
 #endif
     float R = 1.f;     // prod_{j later} (1 - w_j)
     float S0 = 0.f, S1 = 0.f, S2 = 0.f, Sd = 0.f, Sn0 = 0.f, Sn1 = 0.f, Sn2 = 0.f;
@@ -780,23 +796,35 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
                 sl.meta.w = __float_as_uint(bc.lo.y);
             }
         }
-#if S2D_BWD_HALVES
-        // per half, the ring indices whose entry's mask touches it (bit 31 - j: j-th newest, so
+#if S2D_BWD_GROUPS > 1
+        // per group, the ring indices whose entry's mask touches it (bit 31 - j: j-th newest, so
         // the highest set bit is the next entry in reverse order)
+#if S2D_BWD_GROUPS == 4
+        const uint32_t p0 = __brev(__ballot_sync(kFull, (lmv & 0x000000FFu) != 0u));
+        const uint32_t p1 = __brev(__ballot_sync(kFull, (lmv & 0x0000FF00u) != 0u));
+        const uint32_t p2 = __brev(__ballot_sync(kFull, (lmv & 0x00FF0000u) != 0u));
+        const uint32_t p3 = __brev(__ballot_sync(kFull, (lmv & 0xFF000000u) != 0u));
+        const int grp = lane >> 3;
+        uint32_t pm = grp < 2 ? (grp ? p1 : p0) : (grp == 2 ? p2 : p3);
+        const int steps = max(max(__popc(p0), __popc(p1)), max(__popc(p2), __popc(p3)));
+#else
         const uint32_t p0 = __brev(__ballot_sync(kFull, (lmv & 0x0F0F0F0Fu) != 0u));
         const uint32_t p1 = __brev(__ballot_sync(kFull, (lmv & 0xF0F0F0F0u) != 0u));
-        __syncwarp();
         uint32_t pm = (lane & 4) ? p1 : p0;
         const int steps = max(__popc(p0), __popc(p1));
+#endif
+        __syncwarp();
 #ifdef S2D_DIAG  // step counts of alternative splits (tools/diag_stats.py)
         {
             int rq = 0;
 #pragma unroll
             for (int q = 0; q < 4; ++q) rq = max(rq, __popc(__ballot_sync(kFull, (lmv & (0xFFu << (8 * q))) != 0u)));
+            const int ch = max(__popc(__ballot_sync(kFull, (lmv & 0x0F0F0F0Fu) != 0u)),
+                               __popc(__ballot_sync(kFull, (lmv & 0xF0F0F0F0u) != 0u)));
             const int rh = max(__popc(__ballot_sync(kFull, (lmv & 0xFFFFu) != 0u)),
                                __popc(__ballot_sync(kFull, (lmv & 0xFFFF0000u) != 0u)));
             if (lane == 0) {
-                atomicAdd(&a.stats->guard_hits, steps);
+                atomicAdd(&a.stats->guard_hits, ch);
                 atomicAdd(&a.stats->degenerate, rq);
                 atomicAdd(&a.stats->pairs_stored, n);
                 atomicAdd(&a.stats->n_mask, rh);
@@ -805,11 +833,13 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
 #endif
         for (int it = 0; it < steps; ++it) {
             const bool act = pm != 0u;
-            const int k = act ? 31 - __clz(pm) : 31;  // idle half: the newest entry (always loaded)
+            const int k = act ? 31 - __clz(pm) : 31;  // idle group: the newest entry (always loaded)
             pm ^= act ? 1u << k : 0u;
             const uint32_t id = entry(k, act, 0);
-            red_stage<NV, 16, true>(v, lane);
-            if (own && act && v[0] != 0.f) atomicAdd(gcol + (size_t)id * 16, v[0]);
+            red_stage<NV, red_first(kMode), kMode>(v, lane);
+#pragma unroll
+            for (int t = 0; t < RF; ++t)
+                if (own[t] && act && v[t] != 0.f) atomicAdd(gcol[t] + (size_t)id * 16, v[t]);
         }
 #else
         (void)lmv;
@@ -820,8 +850,8 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
             for (int t = 0; t < 2 * NV; ++t) v[t] = 0.f;
             const uint32_t ida = entry(31 - s, true, 0);
             const uint32_t idb = two ? entry(30 - s, true, NV) : 0u;
-            red_stage<2 * NV, 16, false>(v, lane);
-            if (own && v[0] != 0.f && (!second || two)) atomicAdd(gcol + (size_t)(second ? idb : ida) * 16, v[0]);
+            red_stage<2 * NV, 16, 0>(v, lane);
+            if (own[0] && v[0] != 0.f && (!second || two)) atomicAdd(gcol[0] + (size_t)(second ? idb : ida) * 16, v[0]);
         }
 #endif
         __syncwarp();  // slot `buf` is refilled by the next ring_fill

@@ -1,2 +1,2 @@
-S2D_LIB_PATH=$PWD/paper_2604_03092_b200/lib/diag/libsurfel2d.so python tools/diag_stats.py
-bash tools/ab.sh default un2
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/n9_pytest.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/n9_pytest.log
+bash tools/ab.sh default g2 g1
