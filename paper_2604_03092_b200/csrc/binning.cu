@@ -135,7 +135,8 @@ __global__ void __launch_bounds__(kProjThreads, S2D_PROJ_MINB) k_project(const P
                 const float cxh = (float)e.cx, cyh = (float)e.cy;
                 const __half2 lo = __floats2half2_rn((float)(e.cx - (double)cxh), (float)(e.cy - (double)cyh));
                 r.q0 = make_float4(cxh, cyh, __uint_as_float(*reinterpret_cast<const uint32_t *>(&lo)), pv.opac[i]);
-                r.q1 = make_float4((float)(M11 * id), (float)(-M01 * id), (float)(-M10 * id), (float)(M00 * id));
+                // Minv = (A B; C D) stored by columns: (A, C, B, D)
+                r.q1 = make_float4((float)(M11 * id), (float)(-M10 * id), (float)(-M01 * id), (float)(M00 * id));
                 r.q2 = make_float4(pv.colors[3 * i], pv.colors[3 * i + 1], pv.colors[3 * i + 2], (float)e.p[2]);
                 // guard band of the float32 Mahalanobis distance (covers float32 rounding of Minv,
                 // of the pixel offset and of u, v, m)

@@ -189,17 +189,24 @@ __device__ __forceinline__ BlockCentre block_centre(const float4 &q0, const floa
     BlockCentre b;
     b.f = __fsub_rn(q0.x, x0f);
     b.g = __fsub_rn(q0.y, y0f);
-    b.lo = make_float2(-__fmaf_rn(q1.x, lx, __fmul_rn(q1.y, ly)), -__fmaf_rn(q1.z, lx, __fmul_rn(q1.w, ly)));
+    // lo = -((A, C) lx + (B, D) ly), per component fma(A, lx, B ly)
+    const float2 t = __ffma2_rn(make_float2(q1.x, q1.y), make_float2(lx, lx),
+                                __fmul2_rn(make_float2(q1.z, q1.w), make_float2(ly, ly)));
+    b.lo = make_float2(-t.x, -t.y);
     return b;
 }
 
 // m = |Minv (p - c)|^2 at lane offset (lx, ly) from the block origin (block_centre), with the
 // whitened offset (u, v).
-__device__ __forceinline__ float slot_maha(float f, float g, float2 lo, const float4 &q1, float lxf, float lyf,
-                                           float &u, float &v) {
-    const float ex = __fsub_rn(lxf, f), ey = __fsub_rn(lyf, g);
-    u = __fmaf_rn(q1.x, ex, __fmaf_rn(q1.y, ey, lo.x));
-    v = __fmaf_rn(q1.z, ex, __fmaf_rn(q1.w, ey, lo.y));
+// Packed f32x2 (FFMA2): (ex, ey) = (lx, ly) - (f, g), (u, v) = (A, C) ex + ((B, D) ey + lo); each
+// component is the scalar fma chain u = fma(A, ex, fma(B, ey, lo.x)).
+__device__ __forceinline__ float slot_maha(float2 fg, float2 lo, const float4 &q1, float2 lxy, float &u,
+                                           float &v) {
+    const float2 e = __ffma2_rn(fg, make_float2(-1.f, -1.f), lxy);
+    const float2 t = __ffma2_rn(make_float2(q1.z, q1.w), make_float2(e.y, e.y), lo);
+    const float2 uv = __ffma2_rn(make_float2(q1.x, q1.y), make_float2(e.x, e.x), t);
+    u = uv.x;
+    v = uv.y;
     return __fmaf_rn(u, u, __fmul_rn(v, v));
 }
 
@@ -296,14 +303,15 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
     const bool inside = px < P.W && py < P.H;
     const float pxf = (float)px, pyf = (float)py;
     const float kNaN = __int_as_float(0x7fffffff);
-    // affine mode: a terminated (or outside) lane carries lxf = NaN, so its m is NaN and fails
+    // affine mode: a terminated (or outside) lane carries lxy.x = NaN, so its m is NaN and fails
     // the cut test; no per-candidate `done` test is needed
-    float lxf = inside ? (float)(lane & 7) : kNaN;
-    const float lyf = (float)(lane >> 3);
+    float2 lxy = make_float2(inside ? (float)(lane & 7) : kNaN, (float)(lane >> 3));
     const int2 rg = a.ranges[tile];
 
     float T = 1.0f;
-    float c0 = 0.f, c1 = 0.f, c2 = 0.f, dep = 0.f, n0 = 0.f, n1 = 0.f, n2 = 0.f;
+    // accumulated (r, g), (b, depth), (nx, ny), nz: register pairs for the packed FFMA2
+    float2 c01 = make_float2(0.f, 0.f), c2d = make_float2(0.f, 0.f), n01 = make_float2(0.f, 0.f);
+    float n2 = 0.f;
     float maxw = 0.f;
     int argw = -1, nblend = 0, guard = 0;
     bool done = !inside;  // ray mode
@@ -344,11 +352,11 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
                         const float thi = __fadd_rn(P.maha_cut_f, gb), tlo = __fsub_rn(P.maha_cut_f, gb);
                         const bool slow = gbs < 0.f || !(op > 1e-30f);
                         // forward slot: q0 = (f, g, cut + gb, opacity), q3.w = +-(cut - gb),
-                        // meta = (id, lo.x, lo.y, -)
+                        // meta = (id, -, lo.x, lo.y)
                         sl.r.q0 = make_float4(bc.f, bc.g, thi, op);
                         sl.r.q3.w = slow ? -tlo : tlo;
-                        sl.meta.y = __float_as_uint(bc.lo.x);
-                        sl.meta.z = __float_as_uint(bc.lo.y);
+                        sl.meta.z = __float_as_uint(bc.lo.x);
+                        sl.meta.w = __float_as_uint(bc.lo.y);
                     }
                 }
             }
@@ -370,14 +378,12 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
                     bl_bits |= bit;
                     contrib = w * T;
                     const float4 q2 = sl.r.q2;
-                    c0 = fmaf(contrib, q2.x, c0);
-                    c1 = fmaf(contrib, q2.y, c1);
-                    c2 = fmaf(contrib, q2.z, c2);
-                    dep = fmaf(contrib, zpix, dep);
+                    const float2 cc = make_float2(contrib, contrib);
+                    c01 = __ffma2_rn(cc, make_float2(q2.x, q2.y), c01);
+                    c2d = __ffma2_rn(cc, make_float2(q2.z, kRay ? zpix : q2.w), c2d);
                     if (kNormal) {
                         const float4 q3 = sl.r.q3;
-                        n0 = fmaf(contrib, q3.x, n0);
-                        n1 = fmaf(contrib, q3.y, n1);
+                        n01 = __ffma2_rn(cc, make_float2(q3.x, q3.y), n01);
                         n2 = fmaf(contrib, q3.z, n2);
                     }
                     if (kArg && contrib > maxw) {
@@ -386,7 +392,7 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
                     }
                     T -= contrib;  // T (1 - w)
                     if (kRay) done = T < term_t;
-                    else lxf = T < term_t ? kNaN : lxf;
+                    else lxy.x = T < term_t ? kNaN : lxy.x;
                 };
                 if (kRay) {
                     if (!done) {
@@ -403,9 +409,9 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
                 } else {
                     const float4 q0 = sl.r.q0, q1 = sl.r.q1;
                     float u, v;
-                    const float m = slot_maha(q0.x, q0.y, make_float2(__uint_as_float(sl.meta.y),
-                                                                      __uint_as_float(sl.meta.z)),
-                                              q1, lxf, lyf, u, v);
+                    const float m = slot_maha(make_float2(q0.x, q0.y),
+                                              make_float2(__uint_as_float(sl.meta.z), __uint_as_float(sl.meta.w)),
+                                              q1, lxy, u, v);
                     if (m <= q0.z) {  // else certainly outside the reference's cut
                         float w = __fmul_rn(q0.w, fast_exp2(__fmul_rn(m, -0.72134752044448170368f)));
                         const float tlo = sl.r.q3.w;
@@ -447,7 +453,7 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
                 wp += __popc(has);
                 wc += __popc(has);
             }
-            if (__all_sync(kFull, kRay ? done : lxf != lxf)) break;
+            if (__all_sync(kFull, kRay ? done : lxy.x != lxy.x)) break;
             __syncwarp();  // slot `buf` is refilled by the next ring_fill
             buf ^= 1;
             n = nn;
@@ -461,15 +467,15 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
     if (inside) {
         const int p = py * P.W + px;
         if (a.color) {
-            a.color[3 * p] = c0;
-            a.color[3 * p + 1] = c1;
-            a.color[3 * p + 2] = c2;
+            a.color[3 * p] = c01.x;
+            a.color[3 * p + 1] = c01.y;
+            a.color[3 * p + 2] = c2d.x;
         }
-        if (a.depth) a.depth[p] = dep;
+        if (a.depth) a.depth[p] = c2d.y;
         if (a.accum) a.accum[p] = 1.0f - T;
         if (kNormal) {
-            a.normal[3 * p] = n0;
-            a.normal[3 * p + 1] = n1;
+            a.normal[3 * p] = n01.x;
+            a.normal[3 * p + 1] = n01.y;
             a.normal[3 * p + 2] = n2;
         }
         if (kArg) {
@@ -569,7 +575,7 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
     const int px = wx0 + (lane & 7), py = wy0 + (lane >> 3);
     const bool inside = px < P.W && py < P.H;
     const float pxf = (float)px, pyf = (float)py;
-    const float lxf = (float)(lane & 7), lyf = (float)(lane >> 3);
+    const float2 lxy = make_float2((float)(lane & 7), (float)(lane >> 3));
     const int2 rg = a.ranges[tile];
     const int p = py * P.W + px;
 
@@ -672,7 +678,10 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
     const bool second = vi[0] >= NV;  // this lane's sum belongs to the older entry of the pair
 #endif
     float R = 1.f;     // prod_{j later} (1 - w_j)
-    float S0 = 0.f, S1 = 0.f, S2 = 0.f, Sd = 0.f, Sn0 = 0.f, Sn1 = 0.f, Sn2 = 0.f;
+    // suffixes (S_r, S_g), (S_b, S_depth) as register pairs for the packed FFMA2
+    float2 S01 = make_float2(0.f, 0.f), S2d = make_float2(0.f, 0.f);
+    float Sn0 = 0.f, Sn1 = 0.f, Sn2 = 0.f;
+    const float2 gc01 = make_float2(gc0, gc1), gc2d = make_float2(gc2, gd);
     WarpRing &ring = s_ring[warp];
     const uint4 *ws = a.bstream + 8 * (size_t)rg.x + (size_t)warp * (size_t)(rg.y - rg.x);
     int e1 = cnt;
@@ -710,29 +719,35 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
             z = re.iS;
             w = clamped ? P.w_clamp_f : __fmul_rn(r.q0.w, g);
         } else {
-            // backward slot: q0 = (f, g, lo.x, opacity), meta.w = lo.y
+            // backward slot: q0 = (f, g, lo.x, lo.y), meta.w = opacity
             const float4 q0 = r.q0, q1 = r.q1;
-            const float m = slot_maha(q0.x, q0.y, make_float2(q0.z, __uint_as_float(meta.w)), q1, lxf,
-                                      lyf, u, vv);
+            const float m = slot_maha(make_float2(q0.x, q0.y), make_float2(q0.z, q0.w), q1, lxy, u, vv);
             // lanes outside the mask: keep (u, v) finite (a near-singular Minv could overflow
             // them far from the splat), so their zero gradient values stay zeros
             u = inl ? u : 0.f;
             vv = inl ? vv : 0.f;
             g = fast_exp2(__fmul_rn(m, -0.72134752044448170368f));
             z = q2.w;
-            w = clamped ? P.w_clamp_f : __fmul_rn(q0.w, g);
+            w = clamped ? P.w_clamp_f : __fmul_rn(__uint_as_float(meta.w), g);
         }
         w = inl ? w : 0.f;
         const float Ti = inl ? Tn * fast_rcp(1.0f - w) : Tn;
         Tn = Ti;
         const float alpha = w * Ti;
-        v[off + 1] = gc0 * alpha;
-        v[off + 2] = gc1 * alpha;
-        v[off + 3] = gc2 * alpha;
+        const float2 aa = make_float2(alpha, alpha), ww = make_float2(w, w);
+        {
+            const float2 g01 = __fmul2_rn(gc01, aa), g23 = __fmul2_rn(gc2d, aa);  // (rgb, z) gradients
+            v[off + 1] = g01.x;
+            v[off + 2] = g01.y;
+            v[off + 3] = g23.x;
+            if (!kRay) v[off + 4] = g23.y;
+        }
         // dL/dw = T_i [ G.(c - S) + gd (z - Sd) + Gn.(n - Sn) ] + ga T_i R; the differences
         // (c - S) also update the suffix: S <- w c + (1 - w) S = S + w (c - S)
-        const float d0 = q2.x - S0, d1 = q2.y - S1, d2 = q2.z - S2, dd = z - Sd;
-        float dLdw = gc0 * d0 + gc1 * d1 + gc2 * d2 + gd * dd;
+        const float2 d01 = __ffma2_rn(S01, make_float2(-1.f, -1.f), make_float2(q2.x, q2.y));
+        const float2 d2d = __ffma2_rn(S2d, make_float2(-1.f, -1.f), make_float2(q2.z, z));
+        const float2 pd = __ffma2_rn(gc2d, d2d, __fmul2_rn(gc01, d01));
+        float dLdw = pd.x + pd.y;
         if (kExt) {
             const float4 q3 = r.q3;
             v[off + (kRay ? 13 : 10)] = gn0 * alpha;
@@ -763,19 +778,19 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
             v[off + 11] = gS * ry;
             v[off + 12] = gS;
         } else {
-            v[off + 4] = gd * alpha;
             v[off + 0] = dg * g;
             const float gm = -0.5f * w * dg;  // dL/dm
-            v[off + 8] = gm * u;
-            v[off + 9] = gm * vv;
-            v[off + 5] = v[off + 8] * u;
-            v[off + 6] = v[off + 8] * vv;
-            v[off + 7] = v[off + 9] * vv;
+            const float2 uv = make_float2(u, vv);
+            const float2 e = __fmul2_rn(make_float2(gm, gm), uv);     // e = dL/dm (u, v)
+            const float2 k01 = __fmul2_rn(make_float2(e.x, e.x), uv);  // K = dL/dm (uu, uv)
+            v[off + 8] = e.x;
+            v[off + 9] = e.y;
+            v[off + 5] = k01.x;
+            v[off + 6] = k01.y;
+            v[off + 7] = e.y * vv;  // dL/dm vv
         }
-        S0 = fmaf(w, d0, S0);
-        S1 = fmaf(w, d1, S1);
-        S2 = fmaf(w, d2, S2);
-        Sd = fmaf(w, dd, Sd);
+        S01 = __ffma2_rn(ww, d01, S01);
+        S2d = __ffma2_rn(ww, d2d, S2d);
         return meta.x;
     };
     while (n > 0) {
@@ -792,8 +807,9 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
                 const BlockCentre bc = block_centre(sl.r.q0, sl.r.q1, (float)wx0, (float)wy0);
                 sl.r.q0.x = bc.f;
                 sl.r.q0.y = bc.g;
+                sl.meta.w = __float_as_uint(sl.r.q0.w);  // opacity
                 sl.r.q0.z = bc.lo.x;
-                sl.meta.w = __float_as_uint(bc.lo.y);
+                sl.r.q0.w = bc.lo.y;
             }
         }
 #if S2D_BWD_GROUPS > 1

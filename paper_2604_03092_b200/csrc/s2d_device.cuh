@@ -37,7 +37,8 @@ struct ViewParams {
 
 // 64-byte splat record, one per on-screen surfel, indexed by input index.
 //   q0: cx_hi, cy_hi, half2(cx_lo, cy_lo) bits, opacity
-//   q1: Minv = (A, B, C, D): (u, v) = (A dx + B dy, C dx + D dy), m = u^2 + v^2
+//   q1: Minv columns (A, C, B, D): (u, v) = (A dx + B dy, C dx + D dy), m = u^2 + v^2 (column
+//       order, so (A, C) and (B, D) are register pairs for the packed f32x2 evaluation)
 //   q2: r, g, b, z
 //   q3: nx, ny, nz, guard band of m around the 3-sigma cut
 struct __align__(16) SplatRecord {
@@ -314,7 +315,7 @@ __device__ __forceinline__ bool block_reach(int bx0, int by0, const SplatRecord 
     const float cx = r.q0.x + __low2float(lo), cy = r.q0.y + __high2float(lo);
     const float thr = cut + 2.f * fabsf(r.q3.w) + 1e-3f;
     return rect_min_maha((float)bx0 - cx, (float)(bx0 + 7) - cx, (float)by0 - cy, (float)(by0 + 3) - cy, r.q1.x,
-                         r.q1.y, r.q1.z, r.q1.w) <= thr;
+                         r.q1.z, r.q1.y, r.q1.w) <= thr;
 }
 
 // ---------------------------------------------------------- small utilities
