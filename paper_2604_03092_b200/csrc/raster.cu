@@ -368,8 +368,10 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
             // clamped weight; transposed into per-slot lane masks once per chunk
             uint32_t bl_bits = 0u, cl_bits = 0u;
             while (rm) {
-                const int k = 31 - __clz(rm);  // ring index
-                const uint32_t bit = 1u << k;
+                uint32_t kb, bit;  // ring index k = highest set bit of rm
+                asm("bfind.u32 %0, %1;" : "=r"(kb) : "r"(rm));
+                asm("shl.b32 %0, 1, %1;" : "=r"(bit) : "r"(kb));
+                const int k = (int)kb;
                 rm ^= bit;
                 const Slot &sl = ring.s[buf][k];
                 float contrib = 0.f;
@@ -517,7 +519,15 @@ __device__ __forceinline__ void red_stage(float (&v)[NA], int lane) {
     constexpr int H = (C + 1) / 2, F = C / 2;
     const bool up = lane & O;
 #pragma unroll
-    for (int j = 0; j < F; ++j) {
+    for (int j = 0; j + 1 < F; j += 2) {  // two sums per packed FADD2
+        const float s0 = up ? v[j] : v[j + H], s1 = up ? v[j + 1] : v[j + 1 + H];
+        const float2 keep = make_float2(up ? v[j + H] : v[j], up ? v[j + 1 + H] : v[j + 1]);
+        const float2 r = __fadd2_rn(keep, make_float2(__shfl_xor_sync(kFull, s0, O), __shfl_xor_sync(kFull, s1, O)));
+        v[j] = r.x;
+        v[j + 1] = r.y;
+    }
+    if constexpr (F % 2) {
+        constexpr int j = F - 1;
         const float send = up ? v[j] : v[j + H];
         const float keep = up ? v[j + H] : v[j];
         v[j] = keep + __shfl_xor_sync(kFull, send, O);
@@ -848,14 +858,18 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
         }
 #endif
         for (int it = 0; it < steps; ++it) {
+            // kb = index of pm's highest set bit, 0xffffffff when pm = 0 (an idle group, which
+            // reads the newest entry, always loaded, with w = 0); shl clamps, so pm is unchanged
+            uint32_t kb, bit;
+            asm("bfind.u32 %0, %1;" : "=r"(kb) : "r"(pm));
+            asm("shl.b32 %0, 1, %1;" : "=r"(bit) : "r"(kb));
             const bool act = pm != 0u;
-            const int k = act ? 31 - __clz(pm) : 31;  // idle group: the newest entry (always loaded)
-            pm ^= act ? 1u << k : 0u;
-            const uint32_t id = entry(k, act, 0);
+            pm ^= bit;
+            const uint32_t id = entry((int)min(kb, 31u), act, 0);
             red_stage<NV, red_first(kMode), kMode>(v, lane);
 #pragma unroll
             for (int t = 0; t < RF; ++t)
-                if (own[t] && act && v[t] != 0.f) atomicAdd(gcol[t] + (size_t)id * 16, v[t]);
+                if (own[t] && act) atomicAdd(gcol[t] + (size_t)id * 16, v[t]);
         }
 #else
         (void)lmv;
