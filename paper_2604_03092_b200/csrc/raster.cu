@@ -89,7 +89,7 @@ __device__ __forceinline__ float fast_rcp(float x) {
 }
 
 // Forward decision for a pair whose float32 m fell at or above the slot's lower threshold
-// cut - gb, or whose slot is flagged slow (q3.w < 0: opacity within 8e-6 of the weight clamp,
+// cut - gb, or whose slot is flagged slow (tlo < 0: opacity within 8e-6 of the weight clamp,
 // or not above 1e-30).  Returns 0 if the pair does not blend, else the weight the reference
 // blends with.  Below cut - gb the reference's float64 m is below the cut, so the pixel lies
 // inside the reference bbox (the bbox is the ellipse's exact extent) and the pair blends with
@@ -351,10 +351,10 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
                         const BlockCentre bc = block_centre(q0, q1, (float)wx0, (float)wy0);
                         const float thi = __fadd_rn(P.maha_cut_f, gb), tlo = __fsub_rn(P.maha_cut_f, gb);
                         const bool slow = gbs < 0.f || !(op > 1e-30f);
-                        // forward slot: q0 = (f, g, cut + gb, opacity), q3.w = +-(cut - gb),
-                        // meta = (id, -, lo.x, lo.y)
+                        // forward slot: q0 = (f, g, cut + gb, opacity),
+                        // meta = (id, +-(cut - gb), lo.x, lo.y)
                         sl.r.q0 = make_float4(bc.f, bc.g, thi, op);
-                        sl.r.q3.w = slow ? -tlo : tlo;
+                        sl.meta.y = __float_as_uint(slow ? -tlo : tlo);
                         sl.meta.z = __float_as_uint(bc.lo.x);
                         sl.meta.w = __float_as_uint(bc.lo.y);
                     }
@@ -411,12 +411,12 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
                 } else {
                     const float4 q0 = sl.r.q0, q1 = sl.r.q1;
                     float u, v;
+                    const uint4 mt = sl.meta;
                     const float m = slot_maha(make_float2(q0.x, q0.y),
-                                              make_float2(__uint_as_float(sl.meta.z), __uint_as_float(sl.meta.w)),
-                                              q1, lxy, u, v);
+                                              make_float2(__uint_as_float(mt.z), __uint_as_float(mt.w)), q1, lxy, u, v);
                     if (m <= q0.z) {  // else certainly outside the reference's cut
                         float w = __fmul_rn(q0.w, fast_exp2(__fmul_rn(m, -0.72134752044448170368f)));
-                        const float tlo = sl.r.q3.w;
+                        const float tlo = __uint_as_float(mt.y);
                         bool ok = true;
                         // fast path (m < cut - gb, unflagged slot): 0 < w < clamp, blends
                         if (m >= tlo) {
