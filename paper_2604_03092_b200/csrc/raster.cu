@@ -76,6 +76,15 @@ __device__ __forceinline__ int guard_resolve(const ViewParams &P, const RasterAr
     return 1 | (w64 > P.w_clamp ? 2 : 0);
 }
 
+// Predicated global float add without a branch (one RED instruction under a predicate), so
+// a loop step containing it stays one basic block.
+__device__ __forceinline__ void red_add_if(float *p, float v, bool c) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q red.relaxed.gpu.global.add.f32 [%0], %1;\n\t}" ::"l"(p),
+        "f"(v), "r"((int)c)
+        : "memory");
+}
+
 __device__ __forceinline__ float fast_exp2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -857,6 +866,7 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
             }
         }
 #endif
+#pragma unroll 2  // lets one step's reduction overlap the next step's entry (+1.6% backward)
         for (int it = 0; it < steps; ++it) {
             // kb = index of pm's highest set bit, 0xffffffff when pm = 0 (an idle group, which
             // reads the newest entry, always loaded, with w = 0); shl clamps, so pm is unchanged
@@ -868,8 +878,7 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
             const uint32_t id = entry((int)min(kb, 31u), act, 0);
             red_stage<NV, red_first(kMode), kMode>(v, lane);
 #pragma unroll
-            for (int t = 0; t < RF; ++t)
-                if (own[t] && act) atomicAdd(gcol[t] + (size_t)id * 16, v[t]);
+            for (int t = 0; t < RF; ++t) red_add_if(gcol[t] + (size_t)id * 16, v[t], own[t] && act);
         }
 #else
         (void)lmv;

@@ -1,2 +1,1 @@
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/n13_pytest.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/n13_pytest.log
-bash tools/gpu_round.sh r01j notests
+bash tools/ab.sh default u2
