@@ -389,18 +389,17 @@ __device__ __forceinline__ uint32_t lookback_batched(uint32_t *status, int strid
 #pragma unroll
         for (int k = 0; k < 16; ++k) s[k] = (j - k >= 0) ? ld_relaxed_u32(status + (size_t)(j - k) * stride) : kFlagInc;
         int consumed = 0;
-        bool done = false, stall = false;
+        bool done = false;
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
-            if (done || stall) continue;
+        for (int k = 0; k < 16; ++k) {  // stop at the first unpublished or inclusive word
             const uint32_t f = s[k] & ~kValMask;
-            if (f == 0) {
-                stall = true;
-                continue;
-            }
+            if (f == 0) break;
             prefix += s[k] & kValMask;
             ++consumed;
-            if (f == kFlagInc) done = true;
+            if (f == kFlagInc) {
+                done = true;
+                break;
+            }
         }
         if (done) break;
         j -= consumed;
