@@ -142,7 +142,11 @@ __global__ void __launch_bounds__(kProjThreads, S2D_PROJ_MINB) k_project(const P
                 // of the pixel offset and of u, v, m)
                 // (float32 with 1% headroom: it is a bound, not a decision)
                 const float lmin_f = (float)e.lmin, lmax_f = (float)e.lmax;
-                const float gb = 1.01f * (4e-5f * sqrtf(lmax_f / lmin_f) + 1e-5f * rsqrtf(lmin_f) + 4e-6f);
+                // (approximate sqrt / rsqrt: ~1e-7 relative, far inside the 1% headroom; a NaN or
+                // overflowing band becomes infinite, i.e. every pixel of the splat is re-checked)
+                const float rl = rsqrtf(lmin_f);
+                float gb = 1.01f * (4e-5f * (lmax_f * rsqrtf(lmax_f)) * rl + 1e-5f * rl + 4e-6f);
+                if (!(gb <= 3.0e38f)) gb = __int_as_float(0x7f800000);
                 // the guard band is stored negated when the opacity is within 8e-6 of the weight
                 // clamp, so the raster kernels test both with one load
                 const bool nearclamp = pv.opac[i] > P.w_clamp_f - 8e-6f;

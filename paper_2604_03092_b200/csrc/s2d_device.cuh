@@ -60,6 +60,12 @@ __device__ __forceinline__ int64_t f2i_x86(double v) {
 __device__ __forceinline__ int64_t clip64(int64_t v, int64_t lo, int64_t hi) {
     return v < lo ? lo : (v > hi ? hi : v);
 }
+// clip64(f2i_x86(v), 0, hi) for an integral double v without 64-bit integer arithmetic:
+// NaN / out of int64 range -> INT64_MIN -> 0; otherwise v clipped to [0, hi]
+__device__ __forceinline__ int64_t clip_coord(double v, int64_t hi) {
+    if (!(v > -9223372036854775808.0 && v < 9223372036854775808.0) || !(v > 0.0)) return 0;
+    return v >= (double)hi ? hi : (int64_t)(int)v;
+}
 
 // quat_rotate (geometry.py:59-64), numpy.cross association
 __device__ __forceinline__ void quat_rotate_exact(const double q[4], const double v[3], double o[3]) {
@@ -123,7 +129,17 @@ __device__ __forceinline__ void project_exact(const ViewParams &P, const ParamVi
     o.p[1] = dadd(dmul(P.inv[0], r[1]), P.inv[2]);
     o.p[2] = dadd(dmul(P.inv[0], r[2]), P.inv[3]);
     const double z = o.p[2];
-    bool in_front = (z > P.near_plane) && (hypot(o.p[0], o.p[1]) <= dmul(P.tan_max, z));
+    bool in_front = z > P.near_plane;
+    if (in_front) {
+        // hypot(x, y) <= tan_max z (rasterizer.py:206-210): decided on x^2 + y^2 against t^2 when
+        // they differ by more than 1e-12 relative (far beyond the few ulps separating
+        // sqrt(x^2 + y^2) from hypot), else by hypot itself; overflow / NaN fall through to hypot
+        const double t = dmul(P.tan_max, z), t2 = dmul(t, t);
+        const double s2 = dfma(o.p[0], o.p[0], dmul(o.p[1], o.p[1]));
+        if (s2 < t2 * (1.0 - 1e-12)) in_front = true;
+        else if (s2 > t2 * (1.0 + 1e-12)) in_front = false;
+        else in_front = hypot(o.p[0], o.p[1]) <= t;
+    }
     const double zs = in_front ? z : 1.0;
     o.cx = dadd(ddiv(dmul(P.fx, o.p[0]), zs), P.cx);
     o.cy = dadd(ddiv(dmul(P.fy, o.p[1]), zs), P.cy);
@@ -201,10 +217,10 @@ __device__ __forceinline__ void project_exact(const ViewParams &P, const ParamVi
     if (qy < 0.0) qy = 0.0;
     o.rx = dmul(P.sigma, __dsqrt_rn(qx));
     o.ry = dmul(P.sigma, __dsqrt_rn(qy));
-    o.x0 = clip64(f2i_x86(ceil(dsub(o.cx, o.rx))), 0, P.W - 1);
-    o.x1 = clip64(f2i_x86(floor(dadd(o.cx, o.rx))), 0, P.W - 1);
-    o.y0 = clip64(f2i_x86(ceil(dsub(o.cy, o.ry))), 0, P.H - 1);
-    o.y1 = clip64(f2i_x86(floor(dadd(o.cy, o.ry))), 0, P.H - 1);
+    o.x0 = clip_coord(ceil(dsub(o.cx, o.rx)), P.W - 1);
+    o.x1 = clip_coord(floor(dadd(o.cx, o.rx)), P.W - 1);
+    o.y0 = clip_coord(ceil(dsub(o.cy, o.ry)), P.H - 1);
+    o.y1 = clip_coord(floor(dadd(o.cy, o.ry)), P.H - 1);
     o.on_screen = o.valid && (dadd(o.cx, o.rx) >= 0.0) && (dsub(o.cx, o.rx) <= P.wm1) &&
                   (dadd(o.cy, o.ry) >= 0.0) && (dsub(o.cy, o.ry) <= P.hm1);
 }
