@@ -205,11 +205,43 @@ __device__ __forceinline__ void project_exact(const ViewParams &P, const ParamVi
     o.lmax = dadd(half_tr, dev);
     const bool well = (o.lmin > 0.0) && (o.lmax <= dmul(P.max_cond, o.lmin));
     o.valid = well;  // in_front holds here
-    const double det = o.valid ? dsub(dmul(o.a, o.c), dmul(o.b, o.b)) : 1.0;
+    if (!well) {  // no bbox, no inverse: nothing downstream reads them (on_screen = false)
+        o.on_screen = false;
+        return;
+    }
+    // inv_abc (rasterizer.py:247-248): the raster's guard path re-checks m with it
+    const double det = dsub(dmul(o.a, o.c), dmul(o.b, o.b));
     o.ia = ddiv(o.c, det);
     o.ib = ddiv(-o.b, det);
     o.ic = ddiv(o.a, det);
-
+    // Footprint radii.  The reference takes rx = sigma sqrt(inv_c / det(inv_abc)) through
+    // inv_abc (rasterizer.py:247-248, 264-267), which is sigma sqrt(a) up to rounding amplified
+    // by the conditioning: |rx_ref - sigma sqrt(a)| <= 8 eps (kappa + 2) rx, kappa = lmax / lmin
+    // (the cancellations in det and det(inv_abc) are bounded by kappa).  When every bbox and
+    // on-screen decision below is farther than that (plus the rounding of the sum) from its
+    // threshold, it is taken on sigma sqrt(a), else on the reference's own chain (rare: a bbox
+    // edge within ~1e-14 px of an integer).
+    {
+        const double rxf = dmul(P.sigma, __dsqrt_rn(o.a)), ryf = dmul(P.sigma, __dsqrt_rn(o.c));
+        const double kap = (double)((float)o.lmax * __frcp_rn((float)o.lmin));  // inf if lmin underflows
+        const double vx0 = dsub(o.cx, rxf), vx1 = dadd(o.cx, rxf), vy0 = dsub(o.cy, ryf), vy1 = dadd(o.cy, ryf);
+        const double tx = rxf * (4e-15 * (kap + 2.0)), ty = ryf * (4e-15 * (kap + 2.0));
+        auto far_int = [](double v, double t) { return fabs(v - rint(v)) > t + 4.5e-16 * fabs(v) + 1e-300; };
+        auto far_val = [](double v, double c, double t) {
+            return fabs(v - c) > t + 4.5e-16 * (fabs(v) + fabs(c)) + 1e-300;
+        };
+        if (far_int(vx0, tx) && far_int(vx1, tx) && far_int(vy0, ty) && far_int(vy1, ty) && far_val(vx1, 0.0, tx) &&
+            far_val(vx0, P.wm1, tx) && far_val(vy1, 0.0, ty) && far_val(vy0, P.hm1, ty)) {
+            o.rx = rxf;
+            o.ry = ryf;
+            o.x0 = clip_coord(ceil(vx0), P.W - 1);
+            o.x1 = clip_coord(floor(vx1), P.W - 1);
+            o.y0 = clip_coord(ceil(vy0), P.H - 1);
+            o.y1 = clip_coord(floor(vy1), P.H - 1);
+            o.on_screen = vx1 >= 0.0 && vx0 <= P.wm1 && vy1 >= 0.0 && vy0 <= P.hm1;
+            return;
+        }
+    }
     double dinv = dsub(dmul(o.ia, o.ic), dmul(o.ib, o.ib));
     if (!(dinv > 0.0)) dinv = 1.0;
     double qx = ddiv(o.ic, dinv), qy = ddiv(o.ia, dinv);
