@@ -192,8 +192,8 @@ struct s2d_view {
     uint8_t *flags = nullptr;
     uint32_t *keys[2] = {nullptr, nullptr}, *vals[2] = {nullptr, nullptr};
     uint32_t *pkeys[2] = {nullptr, nullptr}, *pvals[2] = {nullptr, nullptr};
-    uint4 *bstream = nullptr;  // [8 pcap] per-warp (surfel, blend mask, clamp mask) streams of blended pairs
-    int *bcount = nullptr;     // [ntiles * 8] stream lengths
+    uint4 *bstream = nullptr;  // [16 pcap] per-(warp, column half) (surfel, blend mask, clamp mask) streams
+    int *bcount = nullptr;     // [ntiles * 16] stream lengths
     float *grad2d = nullptr;
     int2 *aux = nullptr;
     uint8_t *sync = nullptr;
@@ -293,8 +293,8 @@ int ensure_capacity(s2d_view *v, int64_t n, int64_t npx, int ntiles) {
         if ((rc = grow(v->pkeys[b], v->cap_pk[b], v->pcap))) return rc;
         if ((rc = grow(v->pvals[b], v->cap_pv[b], v->pcap))) return rc;
     }
-    if ((rc = grow(v->bstream, v->cap_bs, 8 * v->pcap))) return rc;
-    if ((rc = grow(v->bcount, v->cap_bc, 8 * (int64_t)ntiles))) return rc;
+    if ((rc = grow(v->bstream, v->cap_bs, 16 * v->pcap))) return rc;
+    if ((rc = grow(v->bcount, v->cap_bc, 16 * (int64_t)ntiles))) return rc;
     return layout_sync(v, nn, v->pcap, ntiles);
 }
 

@@ -37,10 +37,10 @@
 #define S2D_FWD_MINB 4
 #endif
 #ifndef S2D_BWD_MINB
-#define S2D_BWD_MINB 3
+#define S2D_BWD_MINB 4
 #endif
-#ifndef S2D_BWD_GROUPS  // lane groups walking the blend stream independently: 1, 2 or 4
-#define S2D_BWD_GROUPS 2
+#ifndef S2D_BWD_UNROLL2
+#define S2D_BWD_UNROLL2 1
 #endif
 
 namespace s2d {
@@ -280,15 +280,15 @@ __device__ __forceinline__ int ring_fill(WarpRing &rg, int buf, ListCursor &c, c
     return n;
 }
 
-// Backward ring fill: entries [e0, e1) of the warp's blend stream, newest first (ring index
-// 31 - j holds entry e1 - 1 - j).  Every entry is work, so this is one coalesced 16-B load per lane; the
-// entry itself is the slot's meta.
-__device__ __forceinline__ int stream_fill(WarpRing &rg, int buf, const uint4 *ws, int e0, int e1,
-                                           const SplatRecord *rec, int lane) {
-    const int n = min(32, e1 - e0);
-    if (lane < n) {
-        const uint4 en = __ldcg(ws + (e1 - 1 - lane));
-        Slot &sl = rg.s[buf][31 - lane];  // entry e1 - 1 - j at ring index 31 - j
+// Backward ring fill, per column half: the newest up to 16 of the entries [0, e1) of the
+// half's blend stream; the j-th newest (entry e1 - 1 - j) at ring index 16 half + j, loaded
+// by the half's lane j (coalesced 16-B loads).  Returns how many.
+__device__ __forceinline__ int stream_fill(WarpRing &rg, int buf, const uint4 *ws, int e1,
+                                           const SplatRecord *rec, int half, int jh) {
+    const int n = min(16, e1);
+    if (jh < n) {
+        const uint4 en = __ldcg(ws + (e1 - 1 - jh));
+        Slot &sl = rg.s[buf][16 * half + jh];
         const float4 *g = reinterpret_cast<const float4 *>(rec + en.x);
         float4 *d = reinterpret_cast<float4 *>(&sl.r);
         cp_async16(d + 0, g + 0);
@@ -329,8 +329,12 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
 
     // this warp's blend stream: one (surfel, lane mask) entry per pair its pixels blended, in
     // list order (the backward's work list)
-    uint4 *wp = a.bstream + 8 * (size_t)rg.x + (size_t)warp * (size_t)max(rg.y - rg.x, 0);
-    int wc = 0;
+    // Two streams per warp, one per column half of its block (lane bit 2 clear / set): an entry
+    // goes to each half whose pixels blended it, so the backward's halves walk them apart.
+    // Segment of (warp w, half h) of tile t: 16 ranges[t].x + (2 w + h) len(t), len = list length.
+    const size_t seg = (size_t)max(rg.y - rg.x, 0);
+    uint4 *wp0 = a.bstream + 16 * (size_t)rg.x + (size_t)(2 * warp) * seg, *wp1 = wp0 + seg;
+    int wc0 = 0, wc1 = 0;
     if (rg.y > rg.x && !__all_sync(kFull, done)) {
         ListCursor cur;
         cursor_init(cur, a, rg.x, rg.y, lane);
@@ -459,10 +463,16 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
             {
                 const uint32_t bm = transpose32(__brev(bl_bits), lane);
                 const uint32_t cm = __any_sync(kFull, cl_bits != 0u) ? transpose32(__brev(cl_bits), lane) : 0u;
-                const uint32_t has = __ballot_sync(kFull, bm != 0u);
-                if (bm != 0u) wp[__popc(has & lanemask_lt())] = make_uint4(ring.s[buf][31 - lane].meta.x, bm, cm, 0u);
-                wp += __popc(has);
-                wc += __popc(has);
+                const bool h0 = (bm & 0x0F0F0F0Fu) != 0u, h1 = (bm & 0xF0F0F0F0u) != 0u;
+                const uint32_t b0 = __ballot_sync(kFull, h0), b1 = __ballot_sync(kFull, h1);
+                const uint4 en = make_uint4(ring.s[buf][31 - lane].meta.x, bm, cm, 0u);
+                const uint32_t lt = lanemask_lt();
+                if (h0) wp0[__popc(b0 & lt)] = en;
+                if (h1) wp1[__popc(b1 & lt)] = en;
+                wp0 += __popc(b0);
+                wp1 += __popc(b1);
+                wc0 += __popc(b0);
+                wc1 += __popc(b1);
             }
             if (__all_sync(kFull, kRay ? done : lxy.x != lxy.x)) break;
             __syncwarp();  // slot `buf` is refilled by the next ring_fill
@@ -472,8 +482,9 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
         cp_wait<0>();
     }
     if (lane == 0) {
-        a.bcount[8 * tile + warp] = wc;
-        if (wc) atomicAdd(&a.stats->blended, wc);
+        a.bcount[16 * tile + 2 * warp] = wc0;
+        a.bcount[16 * tile + 2 * warp + 1] = wc1;
+        if (wc0 + wc1) atomicAdd(&a.stats->blended, wc0 + wc1);
     }
     if (inside) {
         const int p = py * P.W + px;
@@ -665,8 +676,9 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
         for (int w = 0; w < 8; ++w) l += s_loss[w];
         if (l != 0.f) atomicAdd(a.loss_accum, (double)l);
     }
-    const int cnt = a.bcount[8 * tile + warp];
-    if (cnt == 0) return;  // no pixel of this warp's block blended anything (warp-uniform)
+    const int half = (lane >> 2) & 1;  // column half of the block (lane bit 2)
+    const int cnt0 = a.bcount[16 * tile + 2 * warp], cnt1 = a.bcount[16 * tile + 2 * warp + 1];
+    if (cnt0 + cnt1 == 0) return;  // no pixel of this warp's block blended anything (warp-uniform)
 
     // ---- reverse traversal of the pairs this warp's pixels blended ----
     // Per pair, only the lanes in the forward's lane mask work (no cut / guard-band tests);
@@ -676,39 +688,33 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
     // with w = (u, v) = Minv d the whitened pixel offset (dL/dMinv = 2 K M^T and
     // dL/dcentre = -2 Minv^T e are formed in k_project_bwd).
     constexpr int NV = kRay ? (kExt ? 16 : 13) : (kExt ? 13 : 10);
-#if S2D_BWD_GROUPS > 1
-    // the lane groups of the block (4: its rows; 2: its column halves) walk the stream entries
-    // that touch them independently, one entry per group per step; each group reduces its NV
-    // values over its lanes (transposed); lane ownership of the sums is fixed per kernel
-    constexpr int kMode = S2D_BWD_GROUPS == 4 ? 2 : 1, NR = NV;
-#else
-    // two entries per step: their 2 NV values share one transposed reduction (about 2 NV
-    // shuffles instead of 2 x (NV + 2)); lane ownership of the 2 NV sums is fixed per kernel
-    constexpr int kMode = 0, NR = 2 * NV;
-#endif
-    constexpr int RF = red_final(NR, kMode);  // sums held per lane after the reduction
+    // The two column halves of the block (lane bit 2 clear / set) walk their own blend streams
+    // (the entries that touch them, written apart by the forward) in step, one entry per half
+    // per step; each half reduces its NV values over its 16 lanes (transposed, offsets 16, 8,
+    // 2, 1); lane ownership of the sums is fixed per kernel.
+    constexpr int kMode = 1, RF = red_final(NV, kMode);  // sums held per lane after the reduction
     int vi[RF];
     bool own[RF];
-    red_map<NR, kMode>(lane, vi, own);
+    red_map<NV, kMode>(lane, vi, own);
     float *gcol[RF];  // this lane's gradient columns (where it owns a sum)
 #pragma unroll
-    for (int t = 0; t < RF; ++t) gcol[t] = a.grad2d + (vi[t] >= NV ? vi[t] - NV : vi[t]);
-#if S2D_BWD_GROUPS == 1
-    const bool second = vi[0] >= NV;  // this lane's sum belongs to the older entry of the pair
-#endif
+    for (int t = 0; t < RF; ++t) gcol[t] = a.grad2d + vi[t];
     float R = 1.f;     // prod_{j later} (1 - w_j)
     // suffixes (S_r, S_g), (S_b, S_depth) as register pairs for the packed FFMA2
     float2 S01 = make_float2(0.f, 0.f), S2d = make_float2(0.f, 0.f);
     float Sn0 = 0.f, Sn1 = 0.f, Sn2 = 0.f;
     const float2 gc01 = make_float2(gc0, gc1), gc2d = make_float2(gc2, gd);
     WarpRing &ring = s_ring[warp];
-    const uint4 *ws = a.bstream + 8 * (size_t)rg.x + (size_t)warp * (size_t)(rg.y - rg.x);
-    int e1 = cnt;
+    // this lane's half stream; each half stages up to 16 entries per ring buffer, at ring
+    // indices 16 half + j (j-th newest), lane position j in the half = jh
+    const uint4 *ws = a.bstream + 16 * (size_t)rg.x + (size_t)(2 * warp + half) * (size_t)(rg.y - rg.x);
+    const int jh = (lane & 3) | ((lane >> 3) << 2);
+    int e1 = half ? cnt1 : cnt0;
     int buf = 0;
-    int n = stream_fill(ring, 0, ws, max(e1 - 32, 0), e1, a.rec, lane);
+    int n = stream_fill(ring, 0, ws, e1, a.rec, half, jh);
     e1 -= n;
     cp_commit();
-    float v[NR];
+    float v[NV];
     // one entry of the reverse traversal for this lane: updates the pixel state, writes the
     // entry's NV gradient values at v[off ...]
     auto entry = [&](int k, bool act, int off) -> uint32_t {
@@ -812,88 +818,37 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
         S2d = __ffma2_rn(ww, d2d, S2d);
         return meta.x;
     };
-    while (n > 0) {
-        const int nn = stream_fill(ring, buf ^ 1, ws, max(e1 - 32, 0), e1, a.rec, lane);
+    while (true) {
+        const int n0 = __shfl_sync(kFull, n, 0), n1 = __shfl_sync(kFull, n, 4);  // per half
+        if (n0 + n1 == 0) break;
+        const int nn = stream_fill(ring, buf ^ 1, ws, e1, a.rec, half, jh);
         e1 -= nn;
         cp_commit();
         cp_wait<1>();
         __syncwarp();
-        uint32_t lmv = 0u;  // lane j: the blend lane mask of the j-th newest entry
-        if (lane < n) {     // prep: block-relative centre, as the forward computed it
-            Slot &sl = ring.s[buf][31 - lane];
-            lmv = sl.meta.y;
-            if (!kRay) {
-                const BlockCentre bc = block_centre(sl.r.q0, sl.r.q1, (float)wx0, (float)wy0);
-                sl.r.q0.x = bc.f;
-                sl.r.q0.y = bc.g;
-                sl.meta.w = __float_as_uint(sl.r.q0.w);  // opacity
-                sl.r.q0.z = bc.lo.x;
-                sl.r.q0.w = bc.lo.y;
-            }
+        if (!kRay && jh < n) {  // prep: block-relative centre, as the forward computed it
+            Slot &sl = ring.s[buf][16 * half + jh];
+            const BlockCentre bc = block_centre(sl.r.q0, sl.r.q1, (float)wx0, (float)wy0);
+            sl.r.q0.x = bc.f;
+            sl.r.q0.y = bc.g;
+            sl.meta.w = __float_as_uint(sl.r.q0.w);  // opacity
+            sl.r.q0.z = bc.lo.x;
+            sl.r.q0.w = bc.lo.y;
         }
-#if S2D_BWD_GROUPS > 1
-        // per group, the ring indices whose entry's mask touches it (bit 31 - j: j-th newest, so
-        // the highest set bit is the next entry in reverse order)
-#if S2D_BWD_GROUPS == 4
-        const uint32_t p0 = __brev(__ballot_sync(kFull, (lmv & 0x000000FFu) != 0u));
-        const uint32_t p1 = __brev(__ballot_sync(kFull, (lmv & 0x0000FF00u) != 0u));
-        const uint32_t p2 = __brev(__ballot_sync(kFull, (lmv & 0x00FF0000u) != 0u));
-        const uint32_t p3 = __brev(__ballot_sync(kFull, (lmv & 0xFF000000u) != 0u));
-        const int grp = lane >> 3;
-        uint32_t pm = grp < 2 ? (grp ? p1 : p0) : (grp == 2 ? p2 : p3);
-        const int steps = max(max(__popc(p0), __popc(p1)), max(__popc(p2), __popc(p3)));
-#else
-        const uint32_t p0 = __brev(__ballot_sync(kFull, (lmv & 0x0F0F0F0Fu) != 0u));
-        const uint32_t p1 = __brev(__ballot_sync(kFull, (lmv & 0xF0F0F0F0u) != 0u));
-        uint32_t pm = (lane & 4) ? p1 : p0;
-        const int steps = max(__popc(p0), __popc(p1));
-#endif
         __syncwarp();
-#ifdef S2D_DIAG  // step counts of alternative splits (tools/diag_stats.py)
-        {
-            int rq = 0;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) rq = max(rq, __popc(__ballot_sync(kFull, (lmv & (0xFFu << (8 * q))) != 0u)));
-            const int ch = max(__popc(__ballot_sync(kFull, (lmv & 0x0F0F0F0Fu) != 0u)),
-                               __popc(__ballot_sync(kFull, (lmv & 0xF0F0F0F0u) != 0u)));
-            const int rh = max(__popc(__ballot_sync(kFull, (lmv & 0xFFFFu) != 0u)),
-                               __popc(__ballot_sync(kFull, (lmv & 0xFFFF0000u) != 0u)));
-            if (lane == 0) {
-                atomicAdd(&a.stats->guard_hits, ch);
-                atomicAdd(&a.stats->degenerate, rq);
-                atomicAdd(&a.stats->pairs_stored, n);
-                atomicAdd(&a.stats->n_mask, rh);
-            }
-        }
+        const int steps = max(n0, n1);
+        const int kidle = n > 0 ? 16 * half : 16 * (1 - half);  // a staged slot, for idle steps
+#if S2D_BWD_UNROLL2
+#pragma unroll 2  // lets one step's reduction overlap the next step's entry
 #endif
-#pragma unroll 2  // lets one step's reduction overlap the next step's entry (+1.6% backward)
-        for (int it = 0; it < steps; ++it) {
-            // kb = index of pm's highest set bit, 0xffffffff when pm = 0 (an idle group, which
-            // reads the newest entry, always loaded, with w = 0); shl clamps, so pm is unchanged
-            uint32_t kb, bit;
-            asm("bfind.u32 %0, %1;" : "=r"(kb) : "r"(pm));
-            asm("shl.b32 %0, 1, %1;" : "=r"(bit) : "r"(kb));
-            const bool act = pm != 0u;
-            pm ^= bit;
-            const uint32_t id = entry((int)min(kb, 31u), act, 0);
+        for (int st = 0; st < steps; ++st) {
+            const bool act = st < n;  // this half still has an entry in this chunk
+            const uint32_t id = entry(act ? 16 * half + st : kidle, act, 0);
             red_stage<NV, red_first(kMode), kMode>(v, lane);
 #pragma unroll
             for (int t = 0; t < RF; ++t) red_add_if(gcol[t] + (size_t)id * 16, v[t], own[t] && act);
         }
-#else
-        (void)lmv;
-        __syncwarp();
-        for (int s = 0; s < n; s += 2) {
-            const bool two = s + 1 < n;
-#pragma unroll
-            for (int t = 0; t < 2 * NV; ++t) v[t] = 0.f;
-            const uint32_t ida = entry(31 - s, true, 0);
-            const uint32_t idb = two ? entry(30 - s, true, NV) : 0u;
-            red_stage<2 * NV, 16, 0>(v, lane);
-            if (own[0] && v[0] != 0.f && (!second || two)) atomicAdd(gcol[0] + (size_t)(second ? idb : ida) * 16, v[0]);
-        }
-#endif
-        __syncwarp();  // slot `buf` is refilled by the next ring_fill
+        __syncwarp();  // slot `buf` is refilled by the next stream_fill
         buf ^= 1;
         n = nn;
     }

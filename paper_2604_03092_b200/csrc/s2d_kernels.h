@@ -95,7 +95,8 @@ struct RasterArgs {
     // Forward -> backward work lists: warp w of tile t appends, in list order, one (surfel id,
     // lane mask of the block's pixels that blended it, lane mask of those whose weight was
     // clamped, 0) entry per pair its pixels blended, at
-    // bstream[8 ranges[t].x + w (ranges[t].y - ranges[t].x) ...]; bcount[8 t + w] = entries.
+    // bstream[16 ranges[t].x + (2 w + h) (ranges[t].y - ranges[t].x) ...]: the stream of column
+    // half h of warp w's block; bcount[16 t + 2 w + h] = its entries.
     uint4 *bstream;
     int *bcount;
     const SplatRecord *rec;
