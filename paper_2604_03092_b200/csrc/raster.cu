@@ -281,14 +281,15 @@ __device__ __forceinline__ int ring_fill(WarpRing &rg, int buf, ListCursor &c, c
 }
 
 // Backward ring fill, per column half: the newest up to 16 of the entries [0, e1) of the
-// half's blend stream; the j-th newest (entry e1 - 1 - j) at ring index 16 half + j, loaded
-// by the half's lane j (coalesced 16-B loads).  Returns how many.
+// half's blend stream; the j-th newest (entry e1 - 1 - j) at ring index 2 j + half (the two
+// halves' slots of a step interleave, so their 16-B reads hit disjoint banks), loaded by the
+// half's lane j (coalesced 16-B loads).  Returns how many.
 __device__ __forceinline__ int stream_fill(WarpRing &rg, int buf, const uint4 *ws, int e1,
                                            const SplatRecord *rec, int half, int jh) {
     const int n = min(16, e1);
     if (jh < n) {
         const uint4 en = __ldcg(ws + (e1 - 1 - jh));
-        Slot &sl = rg.s[buf][16 * half + jh];
+        Slot &sl = rg.s[buf][2 * jh + half];
         const float4 *g = reinterpret_cast<const float4 *>(rec + en.x);
         float4 *d = reinterpret_cast<float4 *>(&sl.r);
         cp_async16(d + 0, g + 0);
@@ -706,7 +707,7 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
     const float2 gc01 = make_float2(gc0, gc1), gc2d = make_float2(gc2, gd);
     WarpRing &ring = s_ring[warp];
     // this lane's half stream; each half stages up to 16 entries per ring buffer, at ring
-    // indices 16 half + j (j-th newest), lane position j in the half = jh
+    // indices 2 j + half (j-th newest), lane position j in the half = jh
     const uint4 *ws = a.bstream + 16 * (size_t)rg.x + (size_t)(2 * warp + half) * (size_t)(rg.y - rg.x);
     const int jh = (lane & 3) | ((lane >> 3) << 2);
     int e1 = half ? cnt1 : cnt0;
@@ -827,7 +828,7 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
         cp_wait<1>();
         __syncwarp();
         if (!kRay && jh < n) {  // prep: block-relative centre, as the forward computed it
-            Slot &sl = ring.s[buf][16 * half + jh];
+            Slot &sl = ring.s[buf][2 * jh + half];
             const BlockCentre bc = block_centre(sl.r.q0, sl.r.q1, (float)wx0, (float)wy0);
             sl.r.q0.x = bc.f;
             sl.r.q0.y = bc.g;
@@ -837,13 +838,13 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
         }
         __syncwarp();
         const int steps = max(n0, n1);
-        const int kidle = n > 0 ? 16 * half : 16 * (1 - half);  // a staged slot, for idle steps
+        const int kidle = n > 0 ? half : 1 - half;  // a staged slot, for idle steps
 #if S2D_BWD_UNROLL2
 #pragma unroll 2  // lets one step's reduction overlap the next step's entry
 #endif
         for (int st = 0; st < steps; ++st) {
             const bool act = st < n;  // this half still has an entry in this chunk
-            const uint32_t id = entry(act ? 16 * half + st : kidle, act, 0);
+            const uint32_t id = entry(act ? 2 * st + half : kidle, act, 0);
             red_stage<NV, red_first(kMode), kMode>(v, lane);
 #pragma unroll
             for (int t = 0; t < RF; ++t) red_add_if(gcol[t] + (size_t)id * 16, v[t], own[t] && act);
