@@ -325,27 +325,29 @@ __device__ __forceinline__ double exact_maha(double cx, double cy, double ia, do
 
 // Conservative minimum over the continuous rectangle [x0,x1]x[y0,y1] (pixel coordinates,
 // relative to the splat centre) of m(d) = |Minv d|^2: 0 if the centre is inside, else the
-// smallest of the four edge minima (1-D convex quadratics, minimiser clamped to the edge).
+// smaller of the minima over the (at most two) edges visible from the centre (the closest
+// point of a convex polygon to an outside point, in the whitened metric, lies on a visible
+// edge; affine maps keep visibility).  Each edge minimum is a 1-D convex quadratic with the
+// minimiser clamped to the edge.
 __device__ __forceinline__ float rect_min_maha(float dx0, float dx1, float dy0, float dy1, float A, float B,
                                               float C, float D) {
-    if (dx0 <= 0.f && dx1 >= 0.f && dy0 <= 0.f && dy1 >= 0.f) return 0.f;
+    const bool vx = dx0 > 0.f || dx1 < 0.f, vy = dy0 > 0.f || dy1 < 0.f;
+    if (!vx && !vy) return 0.f;
     const float ac = A * A + C * C, bd = B * B + D * D, x = A * B + C * D;
     // approximate reciprocals are fine: the edge minimiser only needs to be close (the value
     // at a nearby t exceeds the minimum by O(dt^2), far inside the 1e-3 culling slack)
-    const float iac = ac > 0.f ? __frcp_rn(ac) : 0.f, ibd = bd > 0.f ? __frcp_rn(bd) : 0.f;
+    float iac, ibd;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(iac) : "f"(ac));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ibd) : "f"(bd));
     float best = 3.0e38f;
-    // horizontal edges y = dy0, dy1: minimise over d.x in [dx0, dx1]
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-        const float y = e ? dy1 : dy0;
+    if (vy) {  // horizontal edge y = dy0 (centre below) or dy1 (above): minimise over d.x
+        const float y = dy0 > 0.f ? dy0 : dy1;
         const float t = fminf(fmaxf(-x * y * iac, dx0), dx1);
         const float u = A * t + B * y, v = C * t + D * y;
-        best = fminf(best, u * u + v * v);
+        best = u * u + v * v;
     }
-    // vertical edges x = dx0, dx1: minimise over d.y in [dy0, dy1]
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-        const float xx = e ? dx1 : dx0;
+    if (vx) {  // vertical edge x = dx0 (centre left) or dx1 (right): minimise over d.y
+        const float xx = dx0 > 0.f ? dx0 : dx1;
         const float t = fminf(fmaxf(-x * xx * ibd, dy0), dy1);
         const float u = A * xx + B * t, v = C * xx + D * t;
         best = fminf(best, u * u + v * v);
