@@ -42,6 +42,9 @@
 #ifndef S2D_BWD_UNROLL2
 #define S2D_BWD_UNROLL2 1
 #endif
+#ifndef S2D_FWD_BRANCHFREE
+#define S2D_FWD_BRANCHFREE 1
+#endif
 
 namespace s2d {
 
@@ -428,6 +431,43 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
                     const uint4 mt = sl.meta;
                     const float m = slot_maha(make_float2(q0.x, q0.y),
                                               make_float2(__uint_as_float(mt.z), __uint_as_float(mt.w)), q1, lxy, u, v);
+#if S2D_FWD_BRANCHFREE
+                    // Branch-free: every lane runs the blend with w = 0 where the pair does not
+                    // blend (m above cut + gb, or NaN for a terminated lane), which leaves its
+                    // state unchanged; only a warp with a lane inside a guard band (or a flagged
+                    // slot) takes the uniform slow-path branch.
+                    const bool pass = m <= q0.z;
+                    float w = __fmul_rn(q0.w, fast_exp2(__fmul_rn(m, -0.72134752044448170368f)));
+                    w = pass ? w : 0.f;
+                    const float tlo = __uint_as_float(mt.y);
+                    const bool slow = pass && m >= tlo;
+                    if (__any_sync(kFull, slow)) {
+                        if (slow) {
+                            bool clamped = false;
+                            w = slow_weight(P, a, mt.x, q0.w, m, w, tlo, px, py, clamped, guard);
+                            if (clamped) cl_bits |= bit;
+                        }
+                    }
+                    {  // blend (blend_forward, _raster_kernels.py:47-55), a no-op where w = 0
+                        bl_bits |= w > 0.f ? bit : 0u;
+                        contrib = w * T;
+                        const float4 q2 = sl.r.q2;
+                        const float2 cc = make_float2(contrib, contrib);
+                        c01 = __ffma2_rn(cc, make_float2(q2.x, q2.y), c01);
+                        c2d = __ffma2_rn(cc, make_float2(q2.z, q2.w), c2d);
+                        if (kNormal) {
+                            const float4 q3 = sl.r.q3;
+                            n01 = __ffma2_rn(cc, make_float2(q3.x, q3.y), n01);
+                            n2 = fmaf(contrib, q3.z, n2);
+                        }
+                        if (kArg && contrib > maxw) {
+                            maxw = contrib;
+                            argw = (int)mt.x;
+                        }
+                        T -= contrib;
+                        lxy.x = T < term_t ? kNaN : lxy.x;
+                    }
+#else
                     if (m <= q0.z) {  // else certainly outside the reference's cut
                         float w = __fmul_rn(q0.w, fast_exp2(__fmul_rn(m, -0.72134752044448170368f)));
                         const float tlo = __uint_as_float(mt.y);
@@ -441,6 +481,7 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
                         }
                         if (ok) blend(w, sl.r.q2.w);
                     }
+#endif
                 }
                 if (kMaxW) {
                     const uint32_t id = sl.meta.x;
