@@ -245,6 +245,7 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = ref.kernel_launches
+    regrows0 = ref.regrows
     clocks.start()
     time.sleep(0.2)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -256,6 +257,7 @@ def main():
         dist.barrier()
     clk = clocks.stop()
     launches = ref.kernel_launches - launches0
+    regrows = ref.regrows - regrows0  # timed steps re-run after a pair-capacity overflow
     ms = e0.elapsed_time(e1)
     t = torch.tensor([ms], device=dev, dtype=torch.float64)
     if world > 1:
@@ -373,6 +375,7 @@ def main():
             "e2e": {"value": round(e2e_value, 3), "unit": "Mpix/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": 8 + 32, "ms_per_step": round(e2e_ms_step, 4)},
             "gpu_launches": int(launches),
+            "capacity_regrows_timed": int(regrows),
             "clocks": clk,
             "cpu_baseline": cpu,
         }

@@ -435,6 +435,7 @@ class AdamRefiner:
         self._graph = None
         self._graph_launches = 0
         self.kernel_launches = 0  # library kernels launched by step() (graph replays included)
+        self.regrows = 0  # steps re-run after a view overflowed the pair capacity
         self.h2d_bytes_per_step = (sum(self.rgb[v].numel() + self.depth[v].numel() for v in self.my_views) * 4
                                    if host_targets else 0)
         self._size_pairs()
@@ -518,6 +519,7 @@ class AdamRefiner:
                 return
             self._reserve(int(self.host_stats[1]) * 5 // 4 + 4096)
             self._graph = None  # buffers may have moved: capture again
+            self.regrows += 1
 
     def step(self) -> float:
         """One refine iteration; returns the total loss over ALL views (all ranks)."""

@@ -8,7 +8,8 @@ import bench
 
 nviews = int(os.environ.get("PROFILE_VIEWS", "4"))
 sc = scenes.config5(0) if os.environ.get("PROFILE_CONFIG", "4") == "5" else scenes.config4(0)
-sc.poses = sc.poses[12:12 + nviews]
+first = int(os.environ.get("PROFILE_FIRST", "12"))
+sc.poses = sc.poses[first:first + nviews]
 rgbs, deps = bench.render_targets(sc, torch.device("cuda", 0))
 ref = AdamRefiner(sc.extra["perturbed"], sc.intr, sc.poses, rgbs, deps, ViewLoss(), AdamConfig())
 for _ in range(2):
