@@ -39,12 +39,6 @@
 #ifndef S2D_BWD_MINB
 #define S2D_BWD_MINB 4
 #endif
-#ifndef S2D_BWD_UNROLL2
-#define S2D_BWD_UNROLL2 1
-#endif
-#ifndef S2D_FWD_BRANCHFREE
-#define S2D_FWD_BRANCHFREE 1
-#endif
 
 namespace s2d {
 
@@ -431,7 +425,6 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
                     const uint4 mt = sl.meta;
                     const float m = slot_maha(make_float2(q0.x, q0.y),
                                               make_float2(__uint_as_float(mt.z), __uint_as_float(mt.w)), q1, lxy, u, v);
-#if S2D_FWD_BRANCHFREE
                     // Branch-free: every lane runs the blend with w = 0 where the pair does not
                     // blend (m above cut + gb, or NaN for a terminated lane), which leaves its
                     // state unchanged; only a warp with a lane inside a guard band (or a flagged
@@ -442,11 +435,12 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
                     const float tlo = __uint_as_float(mt.y);
                     const bool slow = pass && m >= tlo;
                     if (__any_sync(kFull, slow)) {
-                        if (slow) {
-                            bool clamped = false;
-                            w = slow_weight(P, a, mt.x, q0.w, m, w, tlo, px, py, clamped, guard);
-                            if (clamped) cl_bits |= bit;
-                        }
+                        // every lane calls (a warp-uniform branch): a lane that is not slow passes
+                        // m = 0, which is below the band and cannot clamp its w (< clamp or 0),
+                        // so slow_weight returns its w unchanged
+                        bool clamped = false;
+                        w = slow_weight(P, a, mt.x, q0.w, slow ? m : 0.f, w, tlo, px, py, clamped, guard);
+                        if (clamped) cl_bits |= bit;
                     }
                     {  // blend (blend_forward, _raster_kernels.py:47-55), a no-op where w = 0
                         bl_bits |= w > 0.f ? bit : 0u;
@@ -467,21 +461,6 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(con
                         T -= contrib;
                         lxy.x = T < term_t ? kNaN : lxy.x;
                     }
-#else
-                    if (m <= q0.z) {  // else certainly outside the reference's cut
-                        float w = __fmul_rn(q0.w, fast_exp2(__fmul_rn(m, -0.72134752044448170368f)));
-                        const float tlo = __uint_as_float(mt.y);
-                        bool ok = true;
-                        // fast path (m < cut - gb, unflagged slot): 0 < w < clamp, blends
-                        if (m >= tlo) {
-                            bool clamped = false;
-                            w = slow_weight(P, a, sl.meta.x, q0.w, m, w, tlo, px, py, clamped, guard);
-                            ok = w > 0.f;
-                            if (clamped) cl_bits |= bit;
-                        }
-                        if (ok) blend(w, sl.r.q2.w);
-                    }
-#endif
                 }
                 if (kMaxW) {
                     const uint32_t id = sl.meta.x;
@@ -880,9 +859,7 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
         __syncwarp();
         const int steps = max(n0, n1);
         const int kidle = n > 0 ? half : 1 - half;  // a staged slot, for idle steps
-#if S2D_BWD_UNROLL2
 #pragma unroll 2  // lets one step's reduction overlap the next step's entry
-#endif
         for (int st = 0; st < steps; ++st) {
             const bool act = st < n;  // this half still has an entry in this chunk
             const uint32_t id = entry(act ? 2 * st + half : kidle, act, 0);
