@@ -34,7 +34,7 @@
 #include "s2d_kernels.h"
 
 #ifndef S2D_FWD_MINB
-#define S2D_FWD_MINB 4
+#define S2D_FWD_MINB 5
 #endif
 #ifndef S2D_BWD_MINB
 #define S2D_BWD_MINB 4
@@ -298,8 +298,11 @@ __device__ __forceinline__ int stream_fill(WarpRing &rg, int buf, const uint4 *w
     return n;
 }
 
+// The plain variant (the refine path) fits 48 registers, 5 CTAs/SM: besides its own latency
+// hiding, a smaller footprint lets it share SMs with the other views' kernels in flight.
 template <bool kArg, bool kMaxW, bool kNormal, bool kRay>
-__global__ void __launch_bounds__(kRasterThreads, S2D_FWD_MINB) k_raster_fwd(const RasterArgs a) {
+__global__ void __launch_bounds__(kRasterThreads, (kArg || kMaxW || kNormal) ? 4 : S2D_FWD_MINB)
+    k_raster_fwd(const RasterArgs a) {
     __shared__ WarpRing s_ring[kRasterThreads / 32];
     const ViewParams &P = a.P;
     const int tile = blockIdx.x;
