@@ -24,6 +24,16 @@
 #ifndef S2D_PROJ_MINB
 #define S2D_PROJ_MINB 3
 #endif
+#ifdef S2D_SORT_MINB
+#define S2D_SORT_BOUNDS __launch_bounds__(kSortThreads, S2D_SORT_MINB)
+#else
+#define S2D_SORT_BOUNDS __launch_bounds__(kSortThreads)
+#endif
+#ifdef S2D_EMIT_MINB
+#define S2D_EMIT_BOUNDS __launch_bounds__(256, S2D_EMIT_MINB)
+#else
+#define S2D_EMIT_BOUNDS __launch_bounds__(256)
+#endif
 
 namespace s2d {
 
@@ -215,7 +225,7 @@ __global__ void __launch_bounds__(256) k_radix_hist(uint32_t *__restrict__ keys,
         if (sh[k]) atomicAdd(&hist[k], sh[k]);
 }
 
-__global__ void __launch_bounds__(kSortThreads) k_onesweep(
+__global__ void S2D_SORT_BOUNDS k_onesweep(
     const uint32_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint32_t *__restrict__ kout,
     uint32_t *__restrict__ vout, const int *__restrict__ d_n, int n_host, int shift,
     const uint32_t *__restrict__ hist, uint32_t *status, int *ticket) {
@@ -319,7 +329,7 @@ __global__ void __launch_bounds__(256) k_tie_fix(const uint32_t *__restrict__ ke
 
 // ----------------------------------------------------------- scan + emission
 
-__global__ void __launch_bounds__(256) k_scan_emit(const EmitArgs a) {
+__global__ void S2D_EMIT_BOUNDS k_scan_emit(const EmitArgs a) {
     __shared__ int s_tile;
     __shared__ uint32_t s_w[8];
     __shared__ uint32_t s_base;

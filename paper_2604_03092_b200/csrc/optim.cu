@@ -14,6 +14,12 @@
 // local), followed by the post-step projection of DESIGN.md.
 #include "s2d_kernels.h"
 
+#ifdef S2D_PBWD_MINB
+#define S2D_PBWD_BOUNDS __launch_bounds__(128, S2D_PBWD_MINB)
+#else
+#define S2D_PBWD_BOUNDS __launch_bounds__(128)
+#endif
+
 namespace s2d {
 
 namespace {
@@ -39,7 +45,7 @@ __device__ __forceinline__ void dR_dq(const double q[4], const double G[9], doub
 }
 
 template <bool kRay>
-__global__ void __launch_bounds__(128) k_project_bwd(const ProjectBwdArgs a) {
+__global__ void S2D_PBWD_BOUNDS k_project_bwd(const ProjectBwdArgs a) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const ViewParams &P = a.P;
     if (i >= P.n) return;
