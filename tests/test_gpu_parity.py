@@ -300,3 +300,65 @@ def test_stationary_point():
     assert loss == 0.0
     for f in g:
         assert np.abs(g[f]).max() == 0.0, f
+
+
+@pytest.mark.parametrize("kind", ["mse", "l1"])
+def test_tiny_splats_on_pixel_centres(kind):
+    """Splats far below a pixel whose centres project exactly onto pixel centres (x = y = 0 maps
+    to the integer principal point): the reference blends each at that one pixel with m = 0.
+    Exercises the block-relative offsets at an exact integer centre, near-singular Minv (up to
+    ~1e7 per pixel) on the lanes around it, and the branch-free backward's masking of those
+    lanes (finite values only), beside a normal scene; images and all gradients vs the oracle."""
+    sc = scenes.config2(3)
+    rng = np.random.default_rng(23)
+    rows = []
+    for k in range(40):
+        z = 1.0 + 0.11 * k
+        sc_ = 10.0 ** rng.uniform(-9, -5)
+        q = rng.normal(size=4)
+        rows.append(([0.0, 0.0, z], q / np.linalg.norm(q), [sc_, sc_ * rng.uniform(0.5, 2.0)],
+                     rng.uniform(0.3, 0.95), rng.uniform(0, 1, 3)))
+    t = _arr(rows)  # float32-representable inputs, as the device sees them
+    f32 = lambda a: np.asarray(a, np.float32).astype(np.float64)  # noqa: E731
+    t = SurfelArrays(f32(t.means), f32(t.quats), f32(t.scales), f32(t.opacities), f32(t.colors))
+    s = SurfelArrays.concatenate([sc.surfels, t])
+    pose = SE3Pose.identity()
+    intr = R.CameraIntrinsics(250.0, 250.0, 160.0, 120.0, 320, 240)
+    run = Run(s, pose, intr, normal=True, argmax=False)
+    proj = O.project(s, pose, intr)
+    check_binning(run, proj, O.depth_order(proj), intr)
+    ref = O.render(s, pose, intr)
+    im = run.images()
+    for key in ("color", "depth", "accumulation", "normal"):
+        ok, mx, l2 = gate(im[key], getattr(ref, key))
+        assert ok, (key, mx, l2)
+    trgb, tdep = far_targets(ref.color, ref.depth, np.random.default_rng(29))
+    mask = kind == "mse"
+    g, loss = run.backward(kind, trgb, tdep, 1.0, 0.1, mask)
+    for f, v in g.items():
+        assert np.isfinite(v).all(), f
+    oloss, og, _ = O.loss_and_grads(s, pose, intr, trgb, tdep, kind, 1.0, 0.1, mask_depth=mask)
+    assert abs(loss - oloss) <= 1e-5 * abs(oloss)
+    for f in ("colors", "opacities", "means", "quats", "scales"):
+        ok, mx, l2 = gate(g[f], getattr(og, f))
+        assert ok, (f, mx, l2)
+
+
+def test_needle_splat_geometry_gradients():
+    """config2(4) seen head-on holds a needle-like splat (surfel 273: cov2 eigenvalues 6.2 and
+    1.6e-5 px^2, kappa(M) ~ 620).  Its whitened offsets u = A ex + (B ey + lo) cancel ~1e3
+    down to O(1) in float32, so its geometry gradients carry ~kappa eps ~ 1e-4 relative error:
+    this test records that bound (3e-4 of the tensor max for means / quats / scales, 1e-4 for
+    opacities and colours, whose chain does not go through the whitening)."""
+    sc = scenes.config2(4)
+    pose = SE3Pose.identity()
+    intr = R.CameraIntrinsics(250.0, 250.0, 160.0, 120.0, 320, 240)
+    run = Run(sc.surfels, pose, intr, normal=True, argmax=False)
+    ref = O.render(sc.surfels, pose, intr)
+    trgb, tdep = far_targets(ref.color, ref.depth, np.random.default_rng(29))
+    g, loss = run.backward("mse", trgb, tdep, 1.0, 0.1, True)
+    oloss, og, _ = O.loss_and_grads(sc.surfels, pose, intr, trgb, tdep, "mse", 1.0, 0.1, mask_depth=True)
+    assert abs(loss - oloss) <= 1e-5 * abs(oloss)
+    for f, tol in (("colors", 1e-4), ("opacities", 1e-4), ("means", 3e-4), ("quats", 3e-4), ("scales", 3e-4)):
+        ok, mx, l2 = gate(g[f], getattr(og, f), tol)
+        assert ok, (f, mx, l2)
