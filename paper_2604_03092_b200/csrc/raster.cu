@@ -406,7 +406,7 @@ __global__ void __launch_bounds__(kRasterThreads, (kArg || kMaxW || kNormal) ? 4
                         maxw = contrib;
                         argw = (int)sl.meta.x;
                     }
-                    T -= contrib;  // T (1 - w)
+                    T = fmaf(-w, T, T);  // T (1 - w), one rounding (T - w T loses bits for w near 1)
                     if (kRay) done = T < term_t;
                     else lxy.x = T < term_t ? kNaN : lxy.x;
                 };
@@ -461,7 +461,7 @@ __global__ void __launch_bounds__(kRasterThreads, (kArg || kMaxW || kNormal) ? 4
                             maxw = contrib;
                             argw = (int)mt.x;
                         }
-                        T -= contrib;
+                        T = fmaf(-w, T, T);  // T (1 - w), one rounding (T - w T loses bits for w near 1)
                         lxy.x = T < term_t ? kNaN : lxy.x;
                     }
                 }
