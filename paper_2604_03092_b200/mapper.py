@@ -350,15 +350,12 @@ class ViewLoss:
 
 
 class _Lane:
-    """One stream's worth of view state: workspace, render targets, host-target staging."""
+    """One stream's worth of view state: workspace and render buffers."""
 
-    def __init__(self, ctx, h, w, dev, host_targets):
+    def __init__(self, ctx, h, w, dev):
         self.stream = torch.cuda.Stream(dev)
         self.view = View(ctx)
         self.img = ImageBuffers.allocate(h, w, dev, normal=False)
-        if host_targets:
-            self.rgb = torch.empty((h, w, 3), device=dev)
-            self.depth = torch.empty((h, w), device=dev)
 
 
 class AdamRefiner:
@@ -370,7 +367,8 @@ class AdamRefiner:
 
     ``targets_rgb[v]`` (H,W,3) / ``targets_depth[v]`` (H,W) may be numpy arrays, device
     tensors, or (``host_targets=True``) host tensors that are pinned and copied in every
-    step on the view's stream, overlapping the other streams' compute (the end-to-end path).
+    step on a copy stream, each view's backward waiting for its own copy (the end-to-end
+    path: the transfers overlap the forwards and the other views' compute).
     ``inflight`` views run concurrently on separate streams.
     """
 
@@ -422,7 +420,14 @@ class AdamRefiner:
                 self.depth[v] = torch.as_tensor(np.asarray(d, dtype=np.float32) if not isinstance(d, torch.Tensor) else d).to(self.dev, torch.float32)
         self.inflight = max(1, int(inflight))
         self.active_lanes = self.inflight
-        self.lanes = [_Lane(self.ctx, h, w, self.dev, host_targets) for _ in range(self.inflight)]
+        self.lanes = [_Lane(self.ctx, h, w, self.dev) for _ in range(self.inflight)]
+        if host_targets:
+            # end-to-end path: every view's targets go up on a copy stream at the start of the
+            # step, into per-view device buffers; a view's backward (the only reader) waits
+            # for its own copy, so the transfers overlap the forwards and the other views
+            self.copy_stream = torch.cuda.Stream(self.dev)
+            self.dev_rgb = {v: torch.empty((h, w, 3), device=self.dev) for v in self.my_views}
+            self.dev_depth = {v: torch.empty((h, w), device=self.dev) for v in self.my_views}
         self.view = self.lanes[0].view  # the first lane (phase timing / inspection)
         self.loss_acc = torch.zeros(1, dtype=torch.float64, device=self.dev)
         self.stats_acc = torch.zeros(8, dtype=torch.int32, device=self.dev)
@@ -469,24 +474,34 @@ class AdamRefiner:
         start.record(main)
         for lane in lanes:
             lane.stream.wait_stream(main)
+        copied = {}
+        if self.host_targets:
+            cs = self.copy_stream
+            cs.wait_stream(main)
+            with torch.cuda.stream(cs):
+                for v in self.my_views:
+                    self.dev_rgb[v].copy_(self.rgb[v], non_blocking=True)
+                    self.dev_depth[v].copy_(self.depth[v], non_blocking=True)
+                    copied[v] = torch.cuda.Event()
+                    copied[v].record(cs)
         lc = self.loss_cfg
         for j, v in enumerate(self.my_views):
             lane = lanes[j % len(lanes)]
             s = lane.stream
-            if self.host_targets:
-                with torch.cuda.stream(s):
-                    lane.rgb.copy_(self.rgb[v], non_blocking=True)
-                    lane.depth.copy_(self.depth[v], non_blocking=True)
-                trgb, tdep = lane.rgb, lane.depth
-            else:
-                trgb, tdep = self.rgb[v], self.depth[v]
             lane.view.forward(self.params, self.n, self.all_poses[v], self.cam, self.cfg, lane.img, stream=s)
             lane.view.accumulate_stats(self.stats_acc, stream=s)
+            if self.host_targets:
+                s.wait_event(copied[v])
+                trgb, tdep = self.dev_rgb[v], self.dev_depth[v]
+            else:
+                trgb, tdep = self.rgb[v], self.depth[v]
             lane.view.backward(self.params, self.n, lane.img,
                                loss_struct(lc.code(), lc.w_rgb, lc.w_depth, lc.depth_mask, trgb, tdep),
                                self.grads, self.loss_acc, stream=s)
         for lane in lanes:
             main.wait_stream(lane.stream)
+        if self.host_targets:
+            main.wait_stream(self.copy_stream)
 
     def _capture(self):
         """Capture compute_grads (+ the stats read-back) into a CUDA graph.  The pair
