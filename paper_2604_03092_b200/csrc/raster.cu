@@ -33,6 +33,12 @@
 
 #include "s2d_kernels.h"
 
+#ifndef S2D_FWD_WARPS  // warp blocks (8x4 pixels) per raster CTA: 8 = the whole 16x16 tile
+#define S2D_FWD_WARPS 4
+#endif
+#ifndef S2D_BWD_WARPS
+#define S2D_BWD_WARPS 4
+#endif
 #ifndef S2D_FWD_MINB
 #define S2D_FWD_MINB 5
 #endif
@@ -45,6 +51,7 @@ namespace s2d {
 namespace {
 
 constexpr uint32_t kFull = 0xffffffffu;
+constexpr int kFwdWarps = S2D_FWD_WARPS, kBwdWarps = S2D_BWD_WARPS;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -301,13 +308,15 @@ __device__ __forceinline__ int stream_fill(WarpRing &rg, int buf, const uint4 *w
 // The plain variant (the refine path) fits 48 registers, 5 CTAs/SM: besides its own latency
 // hiding, a smaller footprint lets it share SMs with the other views' kernels in flight.
 template <bool kArg, bool kMaxW, bool kNormal, bool kRay>
-__global__ void __launch_bounds__(kRasterThreads, (kArg || kMaxW || kNormal) ? 4 : S2D_FWD_MINB)
+__global__ void __launch_bounds__(kFwdWarps * 32, ((kArg || kMaxW || kNormal) ? 4 : S2D_FWD_MINB) * 8 / kFwdWarps)
     k_raster_fwd(const RasterArgs a) {
-    __shared__ WarpRing s_ring[kRasterThreads / 32];
+    __shared__ WarpRing s_ring[kFwdWarps];
     const ViewParams &P = a.P;
-    const int tile = blockIdx.x;
+    const int tile = blockIdx.x / (8 / kFwdWarps);
     const int tx = tile % P.ntx, ty = tile / P.ntx;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    // a CTA holds kFwdWarps of the tile's 8 warp blocks; warp = the block's index in the tile
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int warp = (blockIdx.x % (8 / kFwdWarps)) * kFwdWarps + (tid >> 5);
     const int wx0 = tx * kTile + (warp & 1) * 8, wy0 = ty * kTile + (warp >> 1) * 4;
     const int px = wx0 + (lane & 7), py = wy0 + (lane >> 3);
     const bool inside = px < P.W && py < P.H;
@@ -326,7 +335,7 @@ __global__ void __launch_bounds__(kRasterThreads, (kArg || kMaxW || kNormal) ? 4
     int argw = -1, nblend = 0, guard = 0;
     bool done = !inside;  // ray mode
     const float term_t = P.term_t_f;
-    WarpRing &ring = s_ring[warp];
+    WarpRing &ring = s_ring[tid >> 5];
 
     // this warp's blend stream: one (surfel, lane mask) entry per pair its pixels blended, in
     // list order (the backward's work list)
@@ -618,13 +627,14 @@ __device__ __forceinline__ void red_map(int lane, int (&vi)[RF], bool (&own)[RF]
 __device__ __forceinline__ float sgnf(float x) { return x > 0.f ? 1.f : (x < 0.f ? -1.f : 0.f); }
 
 template <bool kExt, bool kRay>  // kExt: normal / accumulation seeds present (external loss)
-__global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(const RasterArgs a) {
-    __shared__ WarpRing s_ring[kRasterThreads / 32];
-    __shared__ float s_loss[8];
+__global__ void __launch_bounds__(kBwdWarps * 32, S2D_BWD_MINB * 8 / kBwdWarps) k_raster_bwd(const RasterArgs a) {
+    __shared__ WarpRing s_ring[kBwdWarps];
+    __shared__ float s_loss[kBwdWarps];
     const ViewParams &P = a.P;
-    const int tile = blockIdx.x;
+    const int tile = blockIdx.x / (8 / kBwdWarps);
     const int tx = tile % P.ntx, ty = tile / P.ntx;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int warp = (blockIdx.x % (8 / kBwdWarps)) * kBwdWarps + (tid >> 5);  // block index in the tile
     const int wx0 = tx * kTile + (warp & 1) * 8, wy0 = ty * kTile + (warp >> 1) * 4;
     const int px = wx0 + (lane & 7), py = wy0 + (lane >> 3);
     const bool inside = px < P.W && py < P.H;
@@ -692,12 +702,12 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
         float l = lpx;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(kFull, l, o);
-        if (lane == 0) s_loss[warp] = l;
+        if (lane == 0) s_loss[tid >> 5] = l;
     }
     __syncthreads();
     if (tid == 0 && a.loss_accum) {
         float l = 0.f;
-        for (int w = 0; w < 8; ++w) l += s_loss[w];
+        for (int w = 0; w < kBwdWarps; ++w) l += s_loss[w];
         if (l != 0.f) atomicAdd(a.loss_accum, (double)l);
     }
     const int half = (lane >> 2) & 1;  // column half of the block (lane bit 2)
@@ -728,7 +738,7 @@ __global__ void __launch_bounds__(kRasterThreads, S2D_BWD_MINB) k_raster_bwd(con
     float2 S01 = make_float2(0.f, 0.f), S2d = make_float2(0.f, 0.f);
     float Sn0 = 0.f, Sn1 = 0.f, Sn2 = 0.f;
     const float2 gc01 = make_float2(gc0, gc1), gc2d = make_float2(gc2, gd);
-    WarpRing &ring = s_ring[warp];
+    WarpRing &ring = s_ring[tid >> 5];
     // this lane's half stream; each half stages up to 16 entries per ring buffer, at ring
     // indices 2 j + half (j-th newest), lane position j in the half = jh
     const uint4 *ws = a.bstream + 16 * (size_t)rg.x + (size_t)(2 * warp + half) * (size_t)(rg.y - rg.x);
@@ -890,8 +900,9 @@ static void ensure_smem(int bytes) {
 
 template <bool kArg, bool kMaxW, bool kRay>
 static void fwd_dispatch(const RasterArgs &a, int tiles, cudaStream_t s) {
-    if (a.normal) k_raster_fwd<kArg, kMaxW, true, kRay><<<tiles, kRasterThreads, 0, s>>>(a);
-    else k_raster_fwd<kArg, kMaxW, false, kRay><<<tiles, kRasterThreads, 0, s>>>(a);
+    const int grid = tiles * (8 / kFwdWarps);
+    if (a.normal) k_raster_fwd<kArg, kMaxW, true, kRay><<<grid, kFwdWarps * 32, 0, s>>>(a);
+    else k_raster_fwd<kArg, kMaxW, false, kRay><<<grid, kFwdWarps * 32, 0, s>>>(a);
 }
 
 template <bool kRay>
@@ -913,7 +924,7 @@ void launch_raster_forward(const RasterArgs &a, cudaStream_t s) {
 
 template <bool kExt, bool kRay>
 static void bwd_launch(const RasterArgs &a, int tiles, cudaStream_t s) {
-    k_raster_bwd<kExt, kRay><<<tiles, kRasterThreads, 0, s>>>(a);
+    k_raster_bwd<kExt, kRay><<<tiles * (8 / kBwdWarps), kBwdWarps * 32, 0, s>>>(a);
 }
 
 void launch_raster_backward(const RasterArgs &a, cudaStream_t s) {
