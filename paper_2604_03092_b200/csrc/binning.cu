@@ -99,7 +99,7 @@ __device__ __forceinline__ bool clearly_out(const ViewParams &P, const ParamView
 }
 
 template <bool kRay>
-__global__ void __launch_bounds__(kProjThreads, S2D_PROJ_MINB) k_project(const ProjectArgs a) {
+__global__ void __launch_bounds__(kProjThreads, S2D_PROJ_MINB * 256 / kProjThreads) k_project(const ProjectArgs a) {
     const int64_t i = (int64_t)blockIdx.x * kProjThreads + threadIdx.x;
     const ViewParams &P = a.P;
     bool on = false, degen = false;

@@ -14,10 +14,13 @@
 // local), followed by the post-step projection of DESIGN.md.
 #include "s2d_kernels.h"
 
+#ifndef S2D_PBWD_THREADS
+#define S2D_PBWD_THREADS 64
+#endif
 #ifdef S2D_PBWD_MINB
-#define S2D_PBWD_BOUNDS __launch_bounds__(128, S2D_PBWD_MINB)
+#define S2D_PBWD_BOUNDS __launch_bounds__(S2D_PBWD_THREADS, S2D_PBWD_MINB)
 #else
-#define S2D_PBWD_BOUNDS __launch_bounds__(128)
+#define S2D_PBWD_BOUNDS __launch_bounds__(S2D_PBWD_THREADS)
 #endif
 
 namespace s2d {
@@ -312,11 +315,11 @@ __global__ void __launch_bounds__(256) k_adam(float *__restrict__ params, const 
 }  // namespace
 
 void launch_project_backward(const ProjectBwdArgs &a, cudaStream_t s) {
-    const int64_t blocks = (a.P.n + 127) / 128;
+    const int64_t blocks = (a.P.n + S2D_PBWD_THREADS - 1) / S2D_PBWD_THREADS;
     if (blocks > 0) {
         count_launch();
-        if (a.P.mode == S2D_SPLAT_RAY) k_project_bwd<true><<<(unsigned)blocks, 128, 0, s>>>(a);
-        else k_project_bwd<false><<<(unsigned)blocks, 128, 0, s>>>(a);
+        if (a.P.mode == S2D_SPLAT_RAY) k_project_bwd<true><<<(unsigned)blocks, S2D_PBWD_THREADS, 0, s>>>(a);
+        else k_project_bwd<false><<<(unsigned)blocks, S2D_PBWD_THREADS, 0, s>>>(a);
     }
 }
 

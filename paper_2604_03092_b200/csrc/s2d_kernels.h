@@ -22,7 +22,10 @@ constexpr int kSortItems = S2D_SORT_ITEMS;
 constexpr int kSortTile = kSortThreads * kSortItems;  // keys per onesweep CTA
 constexpr int kRadixBits = 8;
 constexpr int kRadix = 1 << kRadixBits;
-constexpr int kProjThreads = 256;   // surfels per projection CTA (one per thread)
+#ifndef S2D_PROJ_THREADS
+#define S2D_PROJ_THREADS 128
+#endif
+constexpr int kProjThreads = S2D_PROJ_THREADS;  // surfels per projection CTA (one per thread)
 constexpr int kEmitItems = 8;
 constexpr int kEmitTile = 256 * kEmitItems;
 
