@@ -1,8 +1,9 @@
 // raster.cu — per-tile front-to-back compositing and its reverse-order backward
 // (SURVEY.md §8(a) A7-A9, N1-N3).
 //
-// One 256-thread CTA per 16x16 tile.  Warp w owns an 8x4 pixel block (2 columns x 4 rows
-// of warps); lane l owns pixel (l & 7, l >> 3) of it.
+// A 16x16 tile is split into 8 warp blocks of 8x4 pixels (2 columns x 4 rows); a CTA holds
+// kFwdWarps / kBwdWarps of them (4: half a tile).  Lane l owns pixel (l & 7, l >> 3) of its
+// warp's block.
 //
 // Forward (k_raster_fwd): each warp streams its own candidates from the tile's depth-ordered
 // list (entries whose bbox bit for its block is set, k_scan_emit) into a warp-private
