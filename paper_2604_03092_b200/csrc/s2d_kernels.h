@@ -26,7 +26,10 @@ constexpr int kRadix = 1 << kRadixBits;
 #define S2D_PROJ_THREADS 128
 #endif
 constexpr int kProjThreads = S2D_PROJ_THREADS;  // surfels per projection CTA (one per thread)
-constexpr int kEmitItems = 8;
+#ifndef S2D_EMIT_ITEMS
+#define S2D_EMIT_ITEMS 8
+#endif
+constexpr int kEmitItems = S2D_EMIT_ITEMS;
 constexpr int kEmitTile = 256 * kEmitItems;
 
 // Zeroed-per-view scratch ("sync region"): look-back status words, tickets,
