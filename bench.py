@@ -234,7 +234,7 @@ def main():
     loss = ViewLoss("l1", 1.0, 0.1, False)
 
     # ---- device-resident run (value) ----
-    inflight = int(os.environ.get("S2D_INFLIGHT", "8"))
+    inflight = int(os.environ.get("S2D_INFLIGHT", "16"))
     graph = os.environ.get("S2D_GRAPH", "1") == "1"
     ref = AdamRefiner(sc.extra["perturbed"], sc.intr, sc.poses, rgbs, deps, loss, AdamConfig(), device=dev,
                       inflight=inflight, cuda_graph=graph)

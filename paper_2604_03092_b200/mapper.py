@@ -375,7 +375,7 @@ class AdamRefiner:
     def __init__(self, surfels, intr: CameraIntrinsics, poses, targets_rgb, targets_depth,
                  loss: ViewLoss = ViewLoss(), adam: AdamConfig = AdamConfig(),
                  raster_cfg: RasterConfig = DEFAULT_RASTER_CONFIG, mask=None, group=None, device=None,
-                 host_targets: bool = False, inflight: int = 8, shard_optimizer: bool | None = None,
+                 host_targets: bool = False, inflight: int = 16, shard_optimizer: bool | None = None,
                  cuda_graph: bool = False):
         self.ctx = DeviceContext.get(device)
         self.dev = self.ctx.device
