@@ -145,8 +145,11 @@ __global__ void __launch_bounds__(kProjThreads, S2D_PROJ_MINB * 256 / kProjThrea
                 const float cxh = (float)e.cx, cyh = (float)e.cy;
                 const __half2 lo = __floats2half2_rn((float)(e.cx - (double)cxh), (float)(e.cy - (double)cyh));
                 r.q0 = make_float4(cxh, cyh, __uint_as_float(*reinterpret_cast<const uint32_t *>(&lo)), pv.opac[i]);
-                // Minv = (A B; C D) stored by columns: (A, C, B, D)
-                r.q1 = make_float4((float)(M11 * id), (float)(-M10 * id), (float)(-M01 * id), (float)(M00 * id));
+                // Minv = (A B; C D) stored by columns: (A, C, B, D), clamped to the float32 range
+                // (a splat below ~1e-38 px would overflow to inf, and inf * 0 at its centre pixel
+                // would give NaN where the reference has m = 0; FLT_MAX * 0 = 0)
+                auto f32c = [](double x) { return (float)fmin(fmax(x, -3.4028234663852886e38), 3.4028234663852886e38); };
+                r.q1 = make_float4(f32c(M11 * id), f32c(-M10 * id), f32c(-M01 * id), f32c(M00 * id));
                 r.q2 = make_float4(pv.colors[3 * i], pv.colors[3 * i + 1], pv.colors[3 * i + 2], (float)e.p[2]);
                 // guard band of the float32 Mahalanobis distance (covers float32 rounding of Minv,
                 // of the pixel offset and of u, v, m)

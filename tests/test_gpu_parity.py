@@ -304,8 +304,9 @@ def test_stationary_point():
 
 @pytest.mark.parametrize("kind", ["mse", "l1"])
 def test_tiny_splats_on_pixel_centres(kind):
-    """Splats far below a pixel whose centres project exactly onto pixel centres (x = y = 0 maps
-    to the integer principal point): the reference blends each at that one pixel with m = 0.
+    """Splats far below a pixel (scales 1e-9 .. 1e-5, and some near 1e-40) whose centres project
+    exactly onto pixel centres (x = y = 0 maps to the integer principal point): the reference
+    blends each at that one pixel with m = 0.
     Exercises the block-relative offsets at an exact integer centre, near-singular Minv (up to
     ~1e7 per pixel) on the lanes around it, and the branch-free backward's masking of those
     lanes (finite values only), beside a normal scene; images and all gradients vs the oracle."""
@@ -314,7 +315,8 @@ def test_tiny_splats_on_pixel_centres(kind):
     rows = []
     for k in range(40):
         z = 1.0 + 0.11 * k
-        sc_ = 10.0 ** rng.uniform(-9, -5)
+        # down to 1e-40 (a float32 subnormal): Minv beyond the float32 range, clamped
+        sc_ = 10.0 ** (rng.uniform(-9, -5) if k % 8 else -40.0 + 0.1 * k)
         q = rng.normal(size=4)
         rows.append(([0.0, 0.0, z], q / np.linalg.norm(q), [sc_, sc_ * rng.uniform(0.5, 2.0)],
                      rng.uniform(0.3, 0.95), rng.uniform(0, 1, 3)))
