@@ -252,8 +252,13 @@ __device__ __forceinline__ float adam_one(float p, float g, float &m, float &v, 
                                           const AdamK &k) {
     m = k.b1 * m + (1.f - k.b1) * g;
     v = k.b2 * v + (1.f - k.b2) * g * g;
-    const float denom = sqrtf(v) * k.inv_sqrt_bc2 + k.eps;
-    return p - step_size * (m / denom);
+    // approximate sqrt / reciprocal (~1e-7 relative on a step of ~lr): the IEEE forms cost
+    // ~3x the instructions in this instruction-bound kernel, which runs alone at the step's end
+    float sv, r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sv) : "f"(v));
+    const float denom = sv * k.inv_sqrt_bc2 + k.eps;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(denom));
+    return p - step_size * (m * r);
 }
 
 __global__ void __launch_bounds__(256) k_adam(float *__restrict__ params, const float *__restrict__ grads,
@@ -323,6 +328,58 @@ void launch_project_backward(const ProjectBwdArgs &a, cudaStream_t s) {
     }
 }
 
+// The same update over float4 chunks of the packed block (n % 4 == 0, so no chunk straddles a
+// segment and every quaternion is one aligned chunk): coalesced 16-B accesses to the four
+// arrays instead of one thread per surfel walking strided elements.  Chunk c covers elements
+// 4c .. 4c + 3 of segment means [0, 3n) | quats [3n, 7n) | scales [7n, 9n) | opacity [9n, 10n) |
+// colours [10n, 13n); an element of a segment with d values per surfel belongs to surfel
+// (e - start) / d (the mask).
+__global__ void __launch_bounds__(256) k_adam_vec(float4 *__restrict__ params, const float4 *__restrict__ grads,
+                                                  float4 *__restrict__ m1, float4 *__restrict__ m2, int64_t n,
+                                                  const AdamK k, const uint8_t *__restrict__ mask) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= 13 * n / 4) return;
+    const int64_t e0 = 4 * c;
+    int seg;
+    int64_t start;
+    int dim;
+    if (e0 < 3 * n) { seg = 0; start = 0; dim = 3; }
+    else if (e0 < 7 * n) { seg = 1; start = 3 * n; dim = 4; }
+    else if (e0 < 9 * n) { seg = 2; start = 7 * n; dim = 2; }
+    else if (e0 < 10 * n) { seg = 3; start = 9 * n; dim = 1; }
+    else { seg = 4; start = 10 * n; dim = 3; }
+    float4 pp = params[c], mm = m1[c], vv = m2[c];
+    const float4 g = grads[c];
+    float *pv = &pp.x, *mv = &mm.x, *vvv = &vv.x;
+    const float *gv = &g.x;
+    const float step = seg == 0 ? k.step_means : k.step_rest;
+    bool on[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        on[j] = !mask || mask[(e0 + j - start) / dim];
+        if (on[j]) pv[j] = adam_one(pv[j], gv[j], mv[j], vvv[j], step, k);
+    }
+    if (seg == 1) {  // quaternion: renormalised after the step (all four share the surfel's mask)
+        if (on[0]) {
+            const float nq = sqrtf(pp.x * pp.x + pp.y * pp.y + pp.z * pp.z + pp.w * pp.w);
+            const float inq = nq > 0.f ? 1.f / nq : 1.f;
+            pp.x *= inq;
+            pp.y *= inq;
+            pp.z *= inq;
+            pp.w *= inq;
+        }
+    } else if (seg == 2) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) pv[j] = on[j] ? fmaxf(pv[j], k.scale_min) : pv[j];
+    } else if (seg >= 3) {  // opacity, colours: clip to [0, 1] (mapper.py:334-335)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) pv[j] = on[j] ? fminf(fmaxf(pv[j], 0.f), 1.f) : pv[j];
+    }
+    params[c] = pp;
+    m1[c] = mm;
+    m2[c] = vv;
+}
+
 void launch_adam(float *params, const float *grads, float *m1, float *m2, int64_t n, int64_t step,
                  const s2d_adam_config &cfg, const uint8_t *mask, cudaStream_t s) {
     AdamK k;
@@ -337,6 +394,14 @@ void launch_adam(float *params, const float *grads, float *m1, float *m2, int64_
     k.step_means = (float)(cfg.lr_means / bc1);
     k.step_rest = (float)(cfg.lr_rest / bc1);
     k.inv_sqrt_bc2 = (float)(1.0 / sqrt(bc2));
+    if (n > 0 && n % 4 == 0 && ((uintptr_t)params | (uintptr_t)grads | (uintptr_t)m1 | (uintptr_t)m2) % 16 == 0) {
+        count_launch();
+        const int64_t chunks = 13 * n / 4;
+        k_adam_vec<<<(unsigned)((chunks + 255) / 256), 256, 0, s>>>(
+            reinterpret_cast<float4 *>(params), reinterpret_cast<const float4 *>(grads), reinterpret_cast<float4 *>(m1),
+            reinterpret_cast<float4 *>(m2), n, k, mask);
+        return;
+    }
     const int64_t blocks = (n + 255) / 256;
     if (blocks > 0) {
         count_launch();
