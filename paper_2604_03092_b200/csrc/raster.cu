@@ -628,7 +628,10 @@ __device__ __forceinline__ void red_map(int lane, int (&vi)[RF], bool (&own)[RF]
 __device__ __forceinline__ float sgnf(float x) { return x > 0.f ? 1.f : (x < 0.f ? -1.f : 0.f); }
 
 template <bool kExt, bool kRay>  // kExt: normal / accumulation seeds present (external loss)
-__global__ void __launch_bounds__(kBwdWarps * 32, S2D_BWD_MINB * 8 / kBwdWarps) k_raster_bwd(const RasterArgs a) {
+#ifndef S2D_BWD_CTAS_PER_SM
+#define S2D_BWD_CTAS_PER_SM (S2D_BWD_MINB * 8 / kBwdWarps)
+#endif
+__global__ void __launch_bounds__(kBwdWarps * 32, S2D_BWD_CTAS_PER_SM) k_raster_bwd(const RasterArgs a) {
     __shared__ WarpRing s_ring[kBwdWarps];
     __shared__ float s_loss[kBwdWarps];
     const ViewParams &P = a.P;
