@@ -255,6 +255,8 @@ __device__ __forceinline__ int ring_fill(WarpRing &rg, int buf, ListCursor &c, c
                                          int lane) {
     const uint32_t lt = lanemask_lt();
     int n = 0;
+    // 1. walk the list: each hit's surfel id goes to its slot's meta.x (list position j at ring
+    //    index 31 - j)
     while (n < 32) {
         if (c.pend == 0) {
             if (c.cb + 32 >= c.hi) break;  // no chunk beyond the current one
@@ -269,18 +271,20 @@ __device__ __forceinline__ int ring_fill(WarpRing &rg, int buf, ListCursor &c, c
         const int take = min(__popc(c.pend), 32 - n);
         const int rank = __popc(c.pend & lt);
         const bool mine = ((c.pend >> lane) & 1u) && rank < take;
-        if (mine) {
-            Slot &sl = rg.s[buf][31 - (n + rank)];  // forward ring: list position j at index 31 - j
-            const float4 *g = reinterpret_cast<const float4 *>(a.rec + c.kid);
-            float4 *d = reinterpret_cast<float4 *>(&sl.r);
-            cp_async16(d + 0, g + 0);
-            cp_async16(d + 1, g + 1);
-            cp_async16(d + 2, g + 2);
-            cp_async16(d + 3, g + 3);
-            sl.meta.x = c.kid;
-        }
+        if (mine) rg.s[buf][31 - (n + rank)].meta.x = c.kid;
         c.pend &= ~__ballot_sync(kFull, mine);
         n += take;
+    }
+    // 2. stage the records, one slot per lane (one cp.async round for the whole fill)
+    __syncwarp();
+    if (lane < n) {
+        Slot &sl = rg.s[buf][31 - lane];
+        const float4 *g = reinterpret_cast<const float4 *>(a.rec + sl.meta.x);
+        float4 *d = reinterpret_cast<float4 *>(&sl.r);
+        cp_async16(d + 0, g + 0);
+        cp_async16(d + 1, g + 1);
+        cp_async16(d + 2, g + 2);
+        cp_async16(d + 3, g + 3);
     }
     return n;
 }
