@@ -27,7 +27,7 @@ constexpr int kRadix = 1 << kRadixBits;
 #endif
 constexpr int kProjThreads = S2D_PROJ_THREADS;  // surfels per projection CTA (one per thread)
 #ifndef S2D_EMIT_ITEMS
-#define S2D_EMIT_ITEMS 8
+#define S2D_EMIT_ITEMS 4
 #endif
 constexpr int kEmitItems = S2D_EMIT_ITEMS;
 constexpr int kEmitTile = 256 * kEmitItems;
