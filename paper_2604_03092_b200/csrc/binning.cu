@@ -107,8 +107,6 @@ __global__ void __launch_bounds__(kProjThreads, S2D_PROJ_MINB * 256 / kProjThrea
     const ParamView pv(a.params, P.n);
     if (i < P.n && clearly_out(P, pv, i)) {
         a.flags[i] = 0;
-        a.keys[i] = key;
-        a.vals[i] = (uint32_t)i;
     } else if (i < P.n) {
         ExactProj e;
         project_exact(P, pv, i, e);
@@ -178,8 +176,6 @@ __global__ void __launch_bounds__(kProjThreads, S2D_PROJ_MINB * 256 / kProjThrea
             a.z64[i] = e.p[2];
             if (drawn_b) key = (uint32_t)((uint64_t)__double_as_longlong(e.p[2]) >> 32);  // z > 0: monotone
         }
-        a.keys[i] = key;
-        a.vals[i] = (uint32_t)i;
     }
     // per-view counters: visible, drawn, degenerate (rasterizer.py:244), key range
     const bool drawn = key != 0xffffffffu;
@@ -191,14 +187,24 @@ __global__ void __launch_bounds__(kProjThreads, S2D_PROJ_MINB * 256 / kProjThrea
         kmin = min(kmin, __shfl_xor_sync(kFull, kmin, o));
         kmax = max(kmax, __shfl_xor_sync(kFull, kmax, o));
     }
+    uint32_t base = 0;
     if ((threadIdx.x & 31) == 0) {
         if (vm) atomicAdd(&a.stats->visible, __popc(vm));
         if (wm) {
-            atomicAdd(a.n_drawn, __popc(wm));
+            base = (uint32_t)atomicAdd(a.n_drawn, __popc(wm));
             atomicMax(a.key_range, ~kmin);  // the sync region starts zeroed: store ~min
             atomicMax(a.key_range + 1, kmax);
         }
         if (dm) atomicAdd(&a.stats->degenerate, __popc(dm));
+    }
+    // the drawn surfels' (depth key, index) pairs, appended warp by warp: the compaction is not
+    // order-preserving, but k_tie_fix orders every run of equal keys by (z64, index), so the
+    // final order is the reference's lexsort((index, z)) regardless
+    base = __shfl_sync(kFull, base, 0);
+    if (drawn) {
+        const uint32_t o = base + __popc(wm & lanemask_lt());
+        a.keys[o] = key;
+        a.vals[o] = (uint32_t)i;
     }
 }
 
@@ -206,9 +212,10 @@ __global__ void __launch_bounds__(kProjThreads, S2D_PROJ_MINB * 256 / kProjThrea
 
 // Depth keys: rebase to [0, 2^24) (shift only if the key range needs more bits; ties are
 // resolved by k_tie_fix) and histogram the three 8-bit digits.  Sentinels stay sentinels.
-__global__ void __launch_bounds__(256) k_radix_hist(uint32_t *__restrict__ keys, int n,
+__global__ void __launch_bounds__(256) k_radix_hist(uint32_t *__restrict__ keys, const int *__restrict__ d_n,
                                                     const uint32_t *__restrict__ key_range,
                                                     uint32_t *__restrict__ hist) {
+    const int n = *d_n;
     __shared__ uint32_t sh[3 * kRadix];
     for (int k = threadIdx.x; k < 3 * kRadix; k += blockDim.x) sh[k] = 0;
     __syncthreads();
@@ -428,12 +435,13 @@ void launch_project(const ProjectArgs &a, cudaStream_t s) {
     }
 }
 
-void launch_radix_hist(uint32_t *keys, int n, const uint32_t *key_range, uint32_t *hist, cudaStream_t s) {
+void launch_radix_hist(uint32_t *keys, const int *d_n, int n, const uint32_t *key_range, uint32_t *hist,
+                       cudaStream_t s) {
     int blocks = (n + 255) / 256;
     if (blocks > 592) blocks = 592;
     if (blocks < 1) blocks = 1;
     count_launch();
-    k_radix_hist<<<blocks, 256, 0, s>>>(keys, n, key_range, hist);
+    k_radix_hist<<<blocks, 256, 0, s>>>(keys, d_n, key_range, hist);
 }
 
 void launch_onesweep(const uint32_t *kin, const uint32_t *vin, uint32_t *kout, uint32_t *vout,

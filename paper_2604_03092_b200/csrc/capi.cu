@@ -347,14 +347,14 @@ int view_forward(s2d_view *v, cudaStream_t s, const float *params, int64_t n, co
         pa.n_drawn = sr.n_drawn;
         launch_project(pa, s);
         mark();
-        // depth order: keys rebased to 24 bits, 3 stable 8-bit passes; the first pass reads all
-        // n surfels in index order and drops the off-screen ones (order-preserving compaction)
-        launch_radix_hist(v->keys[0], (int)n, sr.key_range, sr.depth_hist, s);
+        // depth order: the drawn surfels' keys (appended by k_project), rebased to 24 bits, 3
+        // stable 8-bit passes, then k_tie_fix orders equal keys by (z64, index)
+        launch_radix_hist(v->keys[0], d_v, (int)n, sr.key_range, sr.depth_hist, s);
         const int64_t sort_tiles = (n + kSortTile - 1) / kSortTile + 1;
         int cur = 0;
         for (int p = 0; p < 3; ++p) {
             launch_onesweep(v->keys[cur], v->vals[cur], v->keys[cur ^ 1], v->vals[cur ^ 1], d_v, (int)n,
-                            p == 0 ? (int)n : -1, kRadixBits * p, sr.depth_hist + p * kRadix,
+                            -1, kRadixBits * p, sr.depth_hist + p * kRadix,
                             sr.depth_status + (size_t)p * sort_tiles * kRadix, sr.tickets + 1 + p, s);
             cur ^= 1;
         }

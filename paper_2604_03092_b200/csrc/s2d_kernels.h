@@ -65,7 +65,8 @@ struct ProjectArgs {
 };
 void launch_project(const ProjectArgs &a, cudaStream_t s);
 
-void launch_radix_hist(uint32_t *keys, int n, const uint32_t *key_range, uint32_t *hist, cudaStream_t s);
+void launch_radix_hist(uint32_t *keys, const int *d_n, int n, const uint32_t *key_range, uint32_t *hist,
+                       cudaStream_t s);
 // n_host >= 0: pass over n_host entries that drops sentinel keys (0xffffffff); else *d_n entries
 void launch_onesweep(const uint32_t *kin, const uint32_t *vin, uint32_t *kout, uint32_t *vout,
                      const int *d_n, int cap, int n_host, int shift, const uint32_t *hist_pass,
