@@ -137,8 +137,8 @@ def render_targets(sc, device):
 # pairs, e blend-stream entries ((pair, 8x4 block) with >= 1 blended pixel), x pixels.
 def phase_bytes(n, v, p, x, e):
     return {
-        "project": 52 * n + n + 8 * n + 120 * v,   # params in; flags, keys/vals out; record 64, exact 40, rect 8, z64 8
-        "depth_sort": 12 * n + 52 * v,              # hist over n keys, 3 stable passes (first one compacts), tie fix
+        "project": 52 * n + n + 128 * v,           # params in; flags out; drawn keys/vals 8, record 64, exact 40, rect 8, z64 8
+        "depth_sort": 60 * v,                       # hist (rebase in place) + 3 stable passes over the drawn keys/vals, tie fix
         "tile_bin": 12 * v + 44 * p,                # order+rect in; pairs out; 2 stable passes; tile ranges
         "raster_fwd": 72 * p + 16 * e + 28 * x,     # key+id+record per pair; blend stream out; rgb, depth, acc, aux out
         "raster_bwd": 16 * e + 64 * p + 40 * x + 40 * v,  # stream + records; aux, render, targets; 2D gradients
