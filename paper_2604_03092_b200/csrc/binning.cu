@@ -240,8 +240,9 @@ __global__ void S2D_SORT_BOUNDS k_onesweep(
     uint32_t *__restrict__ vout, const int *__restrict__ d_n, int n_host, int shift,
     const uint32_t *__restrict__ hist, uint32_t *status, int *ticket) {
     __shared__ uint32_t s_wh[8][kRadix];
-    __shared__ uint32_t s_base[kRadix];
-    __shared__ uint32_t s_w[8];
+    __shared__ uint32_t s_base[kRadix], s_lstart[kRadix];
+    __shared__ uint32_t s_w[8], s_w2[8];
+    __shared__ uint32_t s_key[kSortTile], s_val[kSortTile];  // the tile regrouped by digit
     __shared__ int s_tile;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) s_tile = atomicAdd(ticket, 1);
@@ -287,18 +288,30 @@ __global__ void S2D_SORT_BOUNDS k_onesweep(
     // global start of each digit (exclusive scan of the pass histogram)
     uint32_t htot;
     const uint32_t dstart = block_exclusive_scan_256(hist[tid], s_w, &htot);
+    // block-local start of each digit: the tile is regrouped by digit in shared memory, so the
+    // global writes go out as contiguous runs per digit instead of a 256-way scatter
+    uint32_t btot;
+    const uint32_t lstart = block_exclusive_scan_256(run, s_w2, &btot);
+    s_lstart[tid] = lstart;
     const uint32_t prefix = lookback_batched(status + tid, kRadix, tile, run);
-    s_base[tid] = dstart + prefix;
+    s_base[tid] = dstart + prefix - lstart;
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < kSortItems; ++r) {
         const int idx = wbase + r * 32 + lane;
         if (idx < n && !(drop && key[r] == 0xffffffffu)) {
             const uint32_t d = (key[r] >> shift) & (kRadix - 1);
-            const uint32_t o = s_base[d] + s_wh[warp][d] + pos[r];
-            kout[o] = key[r];
-            vout[o] = vin[idx];
+            const uint32_t l = s_lstart[d] + s_wh[warp][d] + pos[r];
+            s_key[l] = key[r];
+            s_val[l] = vin[idx];
         }
+    }
+    __syncthreads();
+    for (uint32_t l = tid; l < btot; l += kSortThreads) {
+        const uint32_t k = s_key[l];
+        const uint32_t o = s_base[(k >> shift) & (kRadix - 1)] + l;
+        kout[o] = k;
+        vout[o] = s_val[l];
     }
 }
 
