@@ -1,14 +1,14 @@
 // binning.cu — projection, depth order and tile binning.
 //
 //   k_project     per-surfel float64 projection (bit-exact with rasterizer.py:201-281),
-//                 64-B splat record, bbox; writes (depth key, index) for every surfel in
-//                 index order, off-screen surfels keyed by a sentinel; per-view min/max key.
+//                 64-B splat record, bbox; appends (depth key, index) of the drawn surfels
+//                 warp by warp (one atomic per warp); per-view min/max key.
 //   k_radix_hist  rebases the keys to 24 bits (key - min, shifted right only if the
 //                 depth range spans more than 2^24 key steps) and builds the digit
 //                 histograms of all 3 passes in one read.
-//   k_onesweep    one stable LSD radix pass (8-bit digits) with decoupled look-back; the
-//                 first depth pass drops sentinel keys, i.e. it also compacts the
-//                 on-screen surfels (order-preserving, so ties stay in index order).
+//   k_onesweep    one stable LSD radix pass (8-bit digits) with decoupled look-back; each
+//                 tile is regrouped by digit in shared memory, then written out as
+//                 contiguous per-digit runs (with n_host >= 0 it also drops sentinel keys).
 //   k_tie_fix     the depth key is the (rebased) upper 32 bits of the float64 z; runs of
 //                 equal keys whose z differ in the low bits are re-sorted by (z64, index),
 //                 giving exactly the reference order lexsort((index, z))
