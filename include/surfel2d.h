@@ -132,7 +132,7 @@ typedef struct s2d_view s2d_view; /* per-view workspace + forward state */
 
 /* thread-local message of the last failing call */
 const char *s2d_last_error(void);
-int32_t s2d_version(void);
+int32_t s2d_version(void); /* 200: s2d_render_host takes a stream */
 
 int s2d_ctx_create(int32_t device, s2d_ctx **out);
 int s2d_ctx_destroy(s2d_ctx *ctx);
@@ -207,12 +207,27 @@ int s2d_adam_step(void *stream, float *params, const float *grads, float *m1, fl
                   int64_t step, const s2d_adam_config *cfg, const uint8_t *mask);
 
 /*
+ * mapper.refine's backtracking trial (mapper.py:319-335) on the packed block's opacity +
+ * colour part (the contiguous floats [9n, 13n)): params = clip(params0 - step * grads, 0, 1),
+ * grads taken as 0 outside `mask` (n uint8, nullable; mapper.py:320-321).  Every surfel is
+ * clipped, like the reference's np.clip over the whole arrays.  Stream-ordered.
+ */
+int s2d_refine_gd(void *stream, float *params, const float *params0, const float *grads, int64_t n, double step,
+                  const uint8_t *mask);
+/* *out (device float) <- max |grads| over the masked surfels' opacity + colour gradients, the
+ * L-inf norm of mapper.py:322.  Stream-ordered. */
+int s2d_refine_gnorm(void *stream, const float *grads, int64_t n, const uint8_t *mask, float *out);
+
+/*
  * Host-buffer entry point for non-Python callers: float64 numpy-layout
  * SurfelArrays fields in, float64 RenderBuffers out (what rasterizer.render
- * returns, rasterizer.py:334-337), host<->device copies inside.  Synchronous.
+ * returns, rasterizer.py:334-337; replaces _render_state + _k.blend_forward,
+ * rasterizer.py:301-331), host<->device copies inside through a pinned staging
+ * buffer the view keeps (grow-only).  Runs on `stream` (NULL: the legacy default
+ * stream) and returns after synchronising it.  Output pointers may be NULL.
  */
-int s2d_render_host(s2d_view *view, const double *means, const double *quats, const double *scales,
-                    const double *opacities, const double *colors, int64_t n,
+int s2d_render_host(s2d_view *view, void *stream, const double *means, const double *quats,
+                    const double *scales, const double *opacities, const double *colors, int64_t n,
                     const double pose_c2w[8], const s2d_camera *cam, const s2d_raster_config *cfg,
                     double *color, double *depth, double *accumulation, double *normal,
                     int32_t *degenerate_skipped);

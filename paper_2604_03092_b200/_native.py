@@ -106,9 +106,11 @@ _SIGNATURES = {
                                     ctypes.POINTER(Loss), c_p, c_p]),
     "s2d_adam_step": (ctypes.c_int, [c_p, c_p, c_p, c_p, c_p, ctypes.c_int64, ctypes.c_int64,
                                      ctypes.POINTER(AdamCfg), c_p]),
-    "s2d_render_host": (ctypes.c_int, [c_p] + [c_p] * 5 + [ctypes.c_int64, ctypes.POINTER(ctypes.c_double),
+    "s2d_render_host": (ctypes.c_int, [c_p, c_p] + [c_p] * 5 + [ctypes.c_int64, ctypes.POINTER(ctypes.c_double),
                                                            ctypes.POINTER(Camera), ctypes.POINTER(RasterCfg)]
                         + [c_p] * 4 + [ctypes.POINTER(ctypes.c_int32)]),
+    "s2d_refine_gd": (ctypes.c_int, [c_p, c_p, c_p, c_p, ctypes.c_int64, ctypes.c_double, c_p]),
+    "s2d_refine_gnorm": (ctypes.c_int, [c_p, c_p, ctypes.c_int64, c_p, c_p]),
     "s2d_transform_surfels": (ctypes.c_int, [c_p, ctypes.POINTER(ctypes.c_double), c_p, ctypes.c_int64, c_p]),
     "s2d_fuse_gate": (ctypes.c_int, [c_p, c_p, ctypes.POINTER(Camera), c_p, ctypes.c_int64, ctypes.c_double, c_p]),
     "s2d_prune_mark": (ctypes.c_int, [c_p] * 6 + [ctypes.c_int64, ctypes.c_double, ctypes.c_double, c_p]),

@@ -1,8 +1,8 @@
 // binning.cu — projection, depth order and tile binning.
 //
 //   k_project     per-surfel float64 projection (bit-exact with rasterizer.py:201-281),
-//                 64-B splat record, bbox; appends (depth key, index) of the drawn surfels
-//                 warp by warp (one atomic per warp); per-view min/max key.
+//                 64-B splat record, bbox; compacts the (depth key, index) pairs of the drawn
+//                 surfels in index order (chained scan over ticketed tiles); min/max key.
 //   k_radix_hist  rebases the keys to 24 bits (key - min, shifted right only if the
 //                 depth range spans more than 2^24 key steps) and builds the digit
 //                 histograms of all 3 passes in one read.
@@ -100,7 +100,15 @@ __device__ __forceinline__ bool clearly_out(const ViewParams &P, const ParamView
 
 template <bool kRay>
 __global__ void __launch_bounds__(kProjThreads, S2D_PROJ_MINB * 256 / kProjThreads) k_project(const ProjectArgs a) {
-    const int64_t i = (int64_t)blockIdx.x * kProjThreads + threadIdx.x;
+    // tiles are taken in ticket order (the decoupled look-back of the compaction below needs
+    // every predecessor tile to be running or done)
+    __shared__ int s_tile;
+    __shared__ uint32_t s_wcnt[kProjThreads / 32];
+    __shared__ uint32_t s_base;
+    if (threadIdx.x == 0) s_tile = atomicAdd(a.ticket, 1);
+    __syncthreads();
+    const int tile = s_tile;
+    const int64_t i = (int64_t)tile * kProjThreads + threadIdx.x;
     const ViewParams &P = a.P;
     bool on = false, degen = false;
     uint32_t key = 0xffffffffu;
@@ -163,13 +171,18 @@ __global__ void __launch_bounds__(kProjThreads, S2D_PROJ_MINB * 256 / kProjThrea
                 const bool nearclamp = pv.opac[i] > P.w_clamp_f - 8e-6f;
                 r.q3 = make_float4((float)(sg * nn[0]), (float)(sg * nn[1]), (float)(sg * nn[2]),
                                    nearclamp ? -gb : gb);
-                ExactRec x;
+                ExactRec &x = a.exact[i];
                 x.cx = e.cx;
                 x.cy = e.cy;
                 x.ia = e.ia;
                 x.ib = e.ib;
                 x.ic = e.ic;
-                a.exact[i] = x;
+                if (!(gb <= kAccurateGb)) {  // accurate slot (s2d_device.cuh): float64 Minv
+                    x.ma = M11 * id;
+                    x.mb = -M01 * id;
+                    x.mc = -M10 * id;
+                    x.md = M00 * id;
+                }
             }
             a.rec[i] = r;
             a.rect[i] = make_short4((short)bb[0], (short)bb[1], (short)bb[2], (short)bb[3]);
@@ -187,22 +200,34 @@ __global__ void __launch_bounds__(kProjThreads, S2D_PROJ_MINB * 256 / kProjThrea
         kmin = min(kmin, __shfl_xor_sync(kFull, kmin, o));
         kmax = max(kmax, __shfl_xor_sync(kFull, kmax, o));
     }
-    uint32_t base = 0;
-    if ((threadIdx.x & 31) == 0) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) {
         if (vm) atomicAdd(&a.stats->visible, __popc(vm));
         if (wm) {
-            base = (uint32_t)atomicAdd(a.n_drawn, __popc(wm));
             atomicMax(a.key_range, ~kmin);  // the sync region starts zeroed: store ~min
             atomicMax(a.key_range + 1, kmax);
         }
         if (dm) atomicAdd(&a.stats->degenerate, __popc(dm));
+        s_wcnt[warp] = __popc(wm);
     }
-    // the drawn surfels' (depth key, index) pairs, appended warp by warp: the compaction is not
-    // order-preserving, but k_tie_fix orders every run of equal keys by (z64, index), so the
-    // final order is the reference's lexsort((index, z)) regardless
-    base = __shfl_sync(kFull, base, 0);
+    __syncthreads();
+    // Order-preserving compaction of the drawn surfels' (depth key, index) pairs: a chained
+    // scan over the tiles (decoupled look-back), so the keys enter the stable radix passes in
+    // index order and runs of exactly equal z need no re-sorting (k_tie_fix).
+    if (warp == 0) {
+        uint32_t tot = 0;
+#pragma unroll
+        for (int w = 0; w < kProjThreads / 32; ++w) tot += s_wcnt[w];
+        const uint32_t pre = lookback_warp(a.status, tile, tot);
+        if (lane == 0) {
+            s_base = pre;
+            if (tile == (int)((P.n + kProjThreads - 1) / kProjThreads) - 1) *a.n_drawn = (int)(pre + tot);
+        }
+    }
+    __syncthreads();
     if (drawn) {
-        const uint32_t o = base + __popc(wm & lanemask_lt());
+        uint32_t o = s_base + __popc(wm & lanemask_lt());
+        for (int w = 0; w < warp; ++w) o += s_wcnt[w];
         a.keys[o] = key;
         a.vals[o] = (uint32_t)i;
     }
@@ -315,28 +340,63 @@ __global__ void S2D_SORT_BOUNDS k_onesweep(
     }
 }
 
-// Runs of equal (upper-32-bit) depth keys: restore (z64, index) order.
-__global__ void __launch_bounds__(256) k_tie_fix(const uint32_t *__restrict__ keys,
-                                                 uint32_t *vals, const double *__restrict__ z64,
-                                                 const int *__restrict__ d_n, uint32_t *claim) {
+// Runs of equal (rebased upper-32-bit) depth keys: restore (z64, index) order.
+//
+// The compaction in k_project is order-preserving and the radix passes are stable, so a run of
+// equal keys arrives in index order: runs of exactly equal z (a fronto-parallel plane, quantised
+// depth) are already in the reference order and cost one comparison per position.  Only keys
+// whose float64 z differ below the key resolution can be inverted.
+//   - A run of <= kTieShort entries is checked, and if needed insertion-sorted, by the thread
+//     at its head (bounded work per thread).
+//   - A longer run is appended to a list by its head; any inversion inside a long run (seen
+//     by the head within its first kTieShort entries, or by the inverted entry itself, which
+//     then cannot find its head within kTieShort) sets a flag, and k_tie_long sorts the listed
+//     runs cooperatively (one CTA per run).  With the flag clear k_tie_long exits at once.
+constexpr int kTieShort = 64;
+
+__device__ __forceinline__ bool zi_less(const double *z64, uint32_t a, uint32_t b) {
+    const double za = z64[a], zb = z64[b];
+    return za < zb || (za == zb && a < b);
+}
+
+__global__ void __launch_bounds__(256) k_tie_fix(const uint32_t *__restrict__ keys, uint32_t *vals,
+                                                 const double *__restrict__ z64, const int *__restrict__ d_n,
+                                                 uint32_t *ctl, uint32_t *list) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     const int n = *d_n;
-    if (r <= 0 || r >= n) return;
+    if (r >= n) return;
     const uint32_t k = keys[r];
-    if (keys[r - 1] != k) return;
-    const uint32_t a = vals[r - 1], b = vals[r];
-    const double za = z64[a], zb = z64[b];
-    if (!(za > zb || (za == zb && a > b))) return;
-    int s = r - 1;
-    while (s > 0 && keys[s - 1] == k) --s;
-    if (atomicExch(&claim[s], 1u) != 0u) return;
+    const bool head = r == 0 || keys[r - 1] != k;
+    if (!head) {
+        // an inverted pair whose run head lies more than kTieShort back: a long run (the head
+        // only inspects its first kTieShort entries)
+        if (r >= kTieShort && !zi_less(z64, vals[r - 1], vals[r])) {
+            const int lim = r - kTieShort;
+            int s = r - 1;
+            while (s > lim && keys[s - 1] == k) --s;
+            if (s == lim) atomicExch(ctl + 1, 1u);  // head at or before r - kTieShort
+        }
+        return;
+    }
+    if (r + 1 >= n || keys[r + 1] != k) return;  // run of one
     int e = r + 1;
-    while (e < n && keys[e] == k) ++e;
-    for (int j = s + 1; j < e; ++j) {
+    bool sorted = true;
+    while (e < n && e - r < kTieShort && keys[e] == k) {
+        sorted = sorted && zi_less(z64, vals[e - 1], vals[e]);
+        ++e;
+    }
+    if (e < n && keys[e] == k) {  // longer than kTieShort: k_tie_long
+        const uint32_t slot = atomicAdd(ctl, 1u);
+        list[slot] = (uint32_t)r;
+        if (!sorted) atomicExch(ctl + 1, 1u);
+        return;
+    }
+    if (sorted) return;
+    for (int j = r + 1; j < e; ++j) {  // insertion sort of <= kTieShort entries
         const uint32_t v = vals[j];
         const double zv = z64[v];
         int t = j - 1;
-        while (t >= s) {
+        while (t >= r) {
             const uint32_t u = vals[t];
             const double zu = z64[u];
             if (zu > zv || (zu == zv && u > v)) {
@@ -347,6 +407,97 @@ __global__ void __launch_bounds__(256) k_tie_fix(const uint32_t *__restrict__ ke
             }
         }
         vals[t + 1] = v;
+    }
+}
+
+// Cooperative sort of the long runs (only when one of them holds an inversion).  One CTA per
+// run: the run's end is found 256 entries at a time; chunks of kTieChunk entries are bitonic-
+// sorted in shared memory, then merged pairwise (merge path, 256 threads) through `scratch`.
+constexpr int kTieChunk = 2048;
+
+__device__ void tie_bitonic_chunk(uint32_t *v, int len, const double *z64, double *sz, uint32_t *si) {
+    const int tid = threadIdx.x;
+    for (int j = tid; j < kTieChunk; j += blockDim.x) {
+        si[j] = j < len ? v[j] : 0xffffffffu;
+        sz[j] = j < len ? z64[si[j]] : __longlong_as_double(0x7ff0000000000000ll);  // +inf pads last
+    }
+    __syncthreads();
+    for (int size = 2; size <= kTieChunk; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int t = tid; t < kTieChunk / 2; t += blockDim.x) {
+                const int lo = 2 * t - (t & (stride - 1)), hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const double za = sz[lo], zb = sz[hi];
+                const uint32_t ia = si[lo], ib = si[hi];
+                const bool gt = za > zb || (za == zb && ia > ib);
+                if (gt == up) {
+                    sz[lo] = zb;
+                    sz[hi] = za;
+                    si[lo] = ib;
+                    si[hi] = ia;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int j = tid; j < len; j += blockDim.x) v[j] = si[j];
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) k_tie_long(const uint32_t *__restrict__ keys, uint32_t *vals,
+                                                  const double *__restrict__ z64, const int *__restrict__ d_n,
+                                                  const uint32_t *ctl, const uint32_t *list, uint32_t *scratch) {
+    if (ctl[1] == 0u) return;  // no inversion in any long run
+    __shared__ double sz[kTieChunk];
+    __shared__ uint32_t si[kTieChunk];
+    __shared__ int s_end;
+    const int n = *d_n, tid = threadIdx.x;
+    const int nruns = (int)ctl[0];
+    for (int q = blockIdx.x; q < nruns; q += gridDim.x) {
+        const int r0 = (int)list[q];
+        const uint32_t k = keys[r0];
+        if (tid == 0) s_end = n;
+        __syncthreads();
+        for (int base = r0 + kTieShort;; base += blockDim.x) {
+            const int pos = base + tid;
+            if (pos < n && keys[pos] != k) atomicMin(&s_end, pos);
+            __syncthreads();
+            const int e = s_end;
+            __syncthreads();
+            if (e < n || base + (int)blockDim.x >= n) break;
+        }
+        const int len = s_end - r0;
+        for (int c = 0; c < len; c += kTieChunk) tie_bitonic_chunk(vals + r0 + c, min(kTieChunk, len - c), z64, sz, si);
+        // pairwise merges: src -> dst, widths kTieChunk, 2 kTieChunk, ...
+        uint32_t *src = vals + r0, *dst = scratch + r0;
+        for (int w = kTieChunk; w < len; w <<= 1) {
+            for (int s0 = 0; s0 < len; s0 += 2 * w) {
+                const int na = min(w, len - s0), nb = min(w, max(len - s0 - w, 0));
+                const uint32_t *A = src + s0, *B = src + s0 + na;
+                const int tot = na + nb;
+                const int per = (tot + blockDim.x - 1) / blockDim.x;
+                const int d0 = min(tid * per, tot), d1 = min(d0 + per, tot);
+                // merge path: the split (i, d0 - i) of the first d0 outputs
+                int lo = max(0, d0 - nb), hi = min(d0, na);
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (zi_less(z64, B[d0 - mid - 1], A[mid])) hi = mid;  // A[mid] comes after
+                    else lo = mid + 1;
+                }
+                int ia = lo, ib = d0 - lo;
+                for (int d = d0; d < d1; ++d) {
+                    const bool takeA = ib >= nb || (ia < na && !zi_less(z64, B[ib], A[ia]));
+                    dst[s0 + d] = takeA ? A[ia++] : B[ib++];
+                }
+            }
+            __syncthreads();
+            uint32_t *t = src;
+            src = dst;
+            dst = t;
+        }
+        if (src != vals + r0)
+            for (int j = tid; j < len; j += blockDim.x) vals[r0 + j] = src[j];
+        __syncthreads();
     }
 }
 
@@ -469,11 +620,13 @@ void launch_onesweep(const uint32_t *kin, const uint32_t *vin, uint32_t *kout, u
 }
 
 void launch_tie_fix(const uint32_t *keys, uint32_t *vals, const double *z64, const int *d_n, int cap,
-                    uint32_t *claim, cudaStream_t s) {
+                    uint32_t *ctl, uint32_t *list, uint32_t *scratch, cudaStream_t s) {
     const int blocks = (cap + 255) / 256;
     if (blocks > 0) {
         count_launch();
-        k_tie_fix<<<blocks, 256, 0, s>>>(keys, vals, z64, d_n, claim);
+        k_tie_fix<<<blocks, 256, 0, s>>>(keys, vals, z64, d_n, ctl, list);
+        count_launch();
+        k_tie_long<<<64, 256, 0, s>>>(keys, vals, z64, d_n, ctl, list, scratch);
     }
 }
 

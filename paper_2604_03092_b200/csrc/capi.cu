@@ -121,6 +121,7 @@ void make_view_params(const double pose[8], const s2d_camera &cam, const s2d_ras
     P.maha_cut = cfg.footprint_sigma * cfg.footprint_sigma;
     P.w_clamp_f = (float)cfg.weight_clamp;
     P.term_t_f = (float)cfg.termination_transmittance;
+    P.term_t = cfg.termination_transmittance;
     P.maha_cut_f = (float)P.maha_cut;
     P.W = cam.width;
     P.H = cam.height;
@@ -184,7 +185,7 @@ struct s2d_view {
     // capacities (elements)
     int64_t cap_rec = 0, cap_rect = 0, cap_z = 0, cap_flags = 0, cap_keys[2] = {0, 0},
             cap_vals[2] = {0, 0}, cap_grad = 0, cap_aux = 0, cap_pk[2] = {0, 0}, cap_pv[2] = {0, 0},
-            cap_bs = 0, cap_bc = 0, cap_ex = 0, cap_sync = 0;
+            cap_bs = 0, cap_bc = 0, cap_ex = 0, cap_sync = 0, cap_amb = 0;
     SplatRecord *rec = nullptr;
     ExactRec *exact = nullptr;  // float64 centre + inv_abc per on-screen surfel (guard-band path)
     short4 *rect = nullptr;
@@ -196,6 +197,7 @@ struct s2d_view {
     int *bcount = nullptr;     // [ntiles * 16] stream lengths
     float *grad2d = nullptr;
     int2 *aux = nullptr;
+    int *amb = nullptr;  // [npx] ambiguous depth-mask pixels (k_mask_fixup)
     uint8_t *sync = nullptr;
     SyncRegion sr{};
     int64_t pcap = 0;  // pair capacity in use
@@ -230,6 +232,8 @@ struct s2d_view {
     // scratch for the host-buffer entry point
     int64_t cap_hp = 0, cap_himg = 0;
     float *h_params_dev = nullptr, *h_img_dev = nullptr;
+    size_t cap_pin = 0;
+    float *h_pin = nullptr;  // pinned host staging (grow-only)
 };
 
 namespace {
@@ -248,12 +252,14 @@ int layout_sync(s2d_view *v, int64_t n, int64_t pcap, int ntiles) {
     const size_t o_tickets = take(16 * sizeof(int));
     const size_t o_drawn = take(sizeof(int));
     const size_t o_krange = take(2 * 4);
+    const size_t o_pstat0 = take((size_t)((n + kProjThreads - 1) / kProjThreads + 1) * 4);
     const size_t o_dhist = take(3 * kRadix * 4);
     const size_t o_dstat = take((size_t)3 * sort_tiles * kRadix * 4);
     const size_t o_emit = take((size_t)emit_tiles * 4);
     const size_t o_phist = take(2 * kRadix * 4);
     const size_t o_pstat = take((size_t)2 * psort_tiles * kRadix * 4);
-    const size_t o_claim = take((size_t)(n + 1) * 4);
+    const size_t o_tie = take(4 * 4);
+    const size_t o_amb = take(4);
     const size_t o_ranges = take((size_t)ntiles * sizeof(int2));
     int64_t need = (int64_t)off;
     int rc = grow(v->sync, v->cap_sync, need);
@@ -263,12 +269,14 @@ int layout_sync(s2d_view *v, int64_t n, int64_t pcap, int ntiles) {
     v->sr.tickets = reinterpret_cast<int *>(b + o_tickets);
     v->sr.n_drawn = reinterpret_cast<int *>(b + o_drawn);
     v->sr.key_range = reinterpret_cast<uint32_t *>(b + o_krange);
+    v->sr.proj_status = reinterpret_cast<uint32_t *>(b + o_pstat0);
     v->sr.depth_hist = reinterpret_cast<uint32_t *>(b + o_dhist);
     v->sr.depth_status = reinterpret_cast<uint32_t *>(b + o_dstat);
     v->sr.emit_status = reinterpret_cast<uint32_t *>(b + o_emit);
     v->sr.pair_hist = reinterpret_cast<uint32_t *>(b + o_phist);
     v->sr.pair_status = reinterpret_cast<uint32_t *>(b + o_pstat);
-    v->sr.tie_claim = reinterpret_cast<uint32_t *>(b + o_claim);
+    v->sr.tie_ctl = reinterpret_cast<uint32_t *>(b + o_tie);
+    v->sr.amb_count = reinterpret_cast<int *>(b + o_amb);
     v->sr.ranges = reinterpret_cast<int2 *>(b + o_ranges);
     v->sr.bytes = off;
     return S2D_OK;
@@ -288,6 +296,7 @@ int ensure_capacity(s2d_view *v, int64_t n, int64_t npx, int ntiles) {
     }
     if ((rc = grow(v->grad2d, v->cap_grad, nn * 16, /*zero=*/true))) return rc;
     if ((rc = grow(v->aux, v->cap_aux, npx))) return rc;
+    if ((rc = grow(v->amb, v->cap_amb, npx))) return rc;
     if (v->pcap == 0) v->pcap = 4 * nn < 65536 ? 65536 : 4 * nn;  // first guess; regrown on overflow
     for (int b = 0; b < 2; ++b) {
         if ((rc = grow(v->pkeys[b], v->cap_pk[b], v->pcap))) return rc;
@@ -345,6 +354,8 @@ int view_forward(s2d_view *v, cudaStream_t s, const float *params, int64_t n, co
         pa.stats = sr.stats;
         pa.key_range = sr.key_range;
         pa.n_drawn = sr.n_drawn;
+        pa.ticket = sr.tickets + 0;
+        pa.status = sr.proj_status;
         launch_project(pa, s);
         mark();
         // depth order: the drawn surfels' keys (appended by k_project), rebased to 24 bits, 3
@@ -358,7 +369,9 @@ int view_forward(s2d_view *v, cudaStream_t s, const float *params, int64_t n, co
                             sr.depth_status + (size_t)p * sort_tiles * kRadix, sr.tickets + 1 + p, s);
             cur ^= 1;
         }
-        launch_tie_fix(v->keys[cur], v->vals[cur], v->z64, d_v, (int)n, sr.tie_claim, s);
+        // (the other ping-pong buffers are free now: the long-run list and the merge scratch)
+        launch_tie_fix(v->keys[cur], v->vals[cur], v->z64, d_v, (int)n, sr.tie_ctl, v->vals[cur ^ 1],
+                       v->keys[cur ^ 1], s);
         v->order_buf = cur;
         mark();
         // tile binning: pairs emitted in depth order, then stable sort by tile id
@@ -418,6 +431,8 @@ int view_forward(s2d_view *v, cudaStream_t s, const float *params, int64_t n, co
     ra.max_marked = max_marked;
     ra.mask = mask;
     ra.stats = sr.stats;
+    ra.amb_count = sr.amb_count;
+    ra.amb_list = v->amb;
     launch_raster_forward(ra, s);
     S2D_CHECK_LAUNCH();
     mark();
@@ -435,7 +450,7 @@ extern "C" {
 
 const char *s2d_last_error(void) { return g_err.c_str(); }
 
-int32_t s2d_version(void) { return 100; }
+int32_t s2d_version(void) { return 200; }
 
 int s2d_ctx_create(int32_t device, s2d_ctx **out) {
     if (!out) return fail(S2D_ERR_INVALID, "out is NULL");
@@ -465,10 +480,11 @@ int s2d_view_create(s2d_ctx *ctx, s2d_view **out) {
 int s2d_view_destroy(s2d_view *v) {
     if (!v) return S2D_OK;
     void *ptrs[] = {v->rec, v->exact, v->rect, v->z64, v->flags, v->keys[0], v->keys[1], v->vals[0], v->vals[1],
-                    v->pkeys[0], v->pkeys[1], v->pvals[0], v->pvals[1], v->bstream, v->bcount, v->grad2d, v->aux, v->sync,
+                    v->pkeys[0], v->pkeys[1], v->pvals[0], v->pvals[1], v->bstream, v->bcount, v->grad2d, v->aux, v->amb, v->sync,
                     v->h_params_dev, v->h_img_dev};
     for (void *p : ptrs)
         if (p) cudaFree(p);
+    if (v->h_pin) cudaFreeHost(v->h_pin);
     for (auto &tc : v->timed)
         for (int k = 0; k < tc.n; ++k) cudaEventDestroy(tc.e[k]);
     for (cudaEvent_t e : v->free_events) cudaEventDestroy(e);
@@ -612,6 +628,12 @@ int s2d_backward(s2d_view *v, void *stream, const float *params, int64_t n, cons
     ra.d_accum = loss->d_accumulation;
     ra.grad2d = v->grad2d;
     ra.loss_accum = loss_accum;
+    ra.amb_count = v->sr.amb_count;
+    ra.amb_list = v->amb;
+    // a loss over the depth mask: re-decide the float32-ambiguous mask pixels in float64 first
+    const bool uses_mask = (loss->kind == S2D_LOSS_MSE && loss->w_depth != 0.0) ||
+                           (loss->kind == S2D_LOSS_L1 && loss->depth_mask);
+    if (uses_mask && n > 0) launch_mask_fixup(ra, s);
     launch_raster_backward(ra, s);
     mark();
     if (n > 0) {
@@ -643,6 +665,28 @@ int s2d_adam_step(void *stream, float *params, const float *grads, float *m1, fl
     return S2D_OK;
 }
 
+int s2d_refine_gd(void *stream, float *params, const float *params0, const float *grads, int64_t n, double step,
+                  const uint8_t *mask) {
+    if (n < 0) return fail(S2D_ERR_INVALID, "negative n");
+    if (!(step >= 0.0) || !std::isfinite(step)) return fail(S2D_ERR_INVALID, "step must be finite and >= 0");
+    if (n == 0) return S2D_OK;
+    if (!params || !params0 || !grads) return fail(S2D_ERR_INVALID, "NULL buffer");
+    launch_refine_gd(params + 9 * n, params0 + 9 * n, grads + 9 * n, n, step, mask, (cudaStream_t)stream);
+    S2D_CHECK_LAUNCH();
+    return S2D_OK;
+}
+
+int s2d_refine_gnorm(void *stream, const float *grads, int64_t n, const uint8_t *mask, float *out) {
+    if (n < 0) return fail(S2D_ERR_INVALID, "negative n");
+    if (!out) return fail(S2D_ERR_INVALID, "NULL buffer");
+    S2D_CUDA(cudaMemsetAsync(out, 0, sizeof(float), (cudaStream_t)stream));
+    if (n == 0) return S2D_OK;
+    if (!grads) return fail(S2D_ERR_INVALID, "NULL buffer");
+    launch_refine_gnorm(grads + 9 * n, n, mask, out, (cudaStream_t)stream);
+    S2D_CHECK_LAUNCH();
+    return S2D_OK;
+}
+
 int s2d_view_inspect(s2d_view *v, s2d_view_debug *out) {
     if (!v || !out) return fail(S2D_ERR_INVALID, "NULL argument");
     if (!v->has_fwd) return fail(S2D_ERR_STATE, "no forward on this view");
@@ -662,7 +706,7 @@ int s2d_view_inspect(s2d_view *v, s2d_view_debug *out) {
     return S2D_OK;
 }
 
-int s2d_render_host(s2d_view *v, const double *means, const double *quats, const double *scales,
+int s2d_render_host(s2d_view *v, void *stream, const double *means, const double *quats, const double *scales,
                     const double *opacities, const double *colors, int64_t n, const double pose_c2w[8],
                     const s2d_camera *cam, const s2d_raster_config *cfg, double *color, double *depth,
                     double *accumulation, double *normal, int32_t *degenerate_skipped) {
@@ -670,26 +714,29 @@ int s2d_render_host(s2d_view *v, const double *means, const double *quats, const
     int rc = validate_camera(cam);
     if (rc) return rc;
     if (n < 0) return fail(S2D_ERR_INVALID, "negative n");
+    if (n > 0 && !(means && quats && scales && opacities && colors))
+        return fail(S2D_ERR_INVALID, "NULL surfel array");
     const int64_t npx = (int64_t)cam->width * cam->height;
-    // float32 packed parameter block, converted on the host
-    float *hp = nullptr;
     const int64_t np = 13 * (n < 1 ? 1 : n);
-    S2D_CUDA(cudaMallocHost(&hp, (size_t)np * sizeof(float) + (size_t)8 * npx * sizeof(float)));
+    // one grow-only pinned staging buffer per view: the float32 packed block, then the images
+    const size_t need = (size_t)(np + 8 * npx) * sizeof(float);
+    if (v->cap_pin < need) {
+        if (v->h_pin) cudaFreeHost(v->h_pin);
+        v->h_pin = nullptr;
+        v->cap_pin = 0;
+        S2D_CUDA(cudaMallocHost(&v->h_pin, need));
+        v->cap_pin = need;
+    }
+    float *hp = v->h_pin;
     for (int64_t i = 0; i < 3 * n; ++i) hp[i] = (float)means[i];
     for (int64_t i = 0; i < 4 * n; ++i) hp[3 * n + i] = (float)quats[i];
     for (int64_t i = 0; i < 2 * n; ++i) hp[7 * n + i] = (float)scales[i];
     for (int64_t i = 0; i < n; ++i) hp[9 * n + i] = (float)opacities[i];
     for (int64_t i = 0; i < 3 * n; ++i) hp[10 * n + i] = (float)colors[i];
     float *himg = hp + np;
-    if ((rc = grow(v->h_params_dev, v->cap_hp, np))) {
-        cudaFreeHost(hp);
-        return rc;
-    }
-    if ((rc = grow(v->h_img_dev, v->cap_himg, 8 * npx))) {
-        cudaFreeHost(hp);
-        return rc;
-    }
-    cudaStream_t s = nullptr;
+    if ((rc = grow(v->h_params_dev, v->cap_hp, np))) return rc;
+    if ((rc = grow(v->h_img_dev, v->cap_himg, 8 * npx))) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
     S2D_CUDA(cudaMemcpyAsync(v->h_params_dev, hp, (size_t)np * sizeof(float), cudaMemcpyHostToDevice, s));
     s2d_image img;
     memset(&img, 0, sizeof(img));
@@ -697,11 +744,9 @@ int s2d_render_host(s2d_view *v, const double *means, const double *quats, const
     img.depth = v->h_img_dev + 3 * npx;
     img.accumulation = v->h_img_dev + 4 * npx;
     img.normal = v->h_img_dev + 5 * npx;
-    for (int attempt = 0; attempt < 3; ++attempt) {
-        if ((rc = view_forward(v, s, v->h_params_dev, n, pose_c2w, cam, cfg, &img, nullptr, nullptr, nullptr))) {
-            cudaFreeHost(hp);
+    for (int attempt = 0;; ++attempt) {
+        if ((rc = view_forward(v, s, v->h_params_dev, n, pose_c2w, cam, cfg, &img, nullptr, nullptr, nullptr)))
             return rc;
-        }
         s2d_view_stats st;
         S2D_CUDA(cudaMemcpyAsync(&st, v->sr.stats, sizeof(st), cudaMemcpyDeviceToHost, s));
         S2D_CUDA(cudaStreamSynchronize(s));
@@ -709,6 +754,7 @@ int s2d_render_host(s2d_view *v, const double *means, const double *quats, const
             if (degenerate_skipped) *degenerate_skipped = st.degenerate;
             break;
         }
+        if (attempt == 3) return fail(S2D_ERR_STATE, "pair capacity could not be sized");
         v->pcap = (int64_t)st.pairs + st.pairs / 4 + 1024;
     }
     S2D_CUDA(cudaMemcpyAsync(himg, v->h_img_dev, (size_t)8 * npx * sizeof(float), cudaMemcpyDeviceToHost, s));
@@ -721,7 +767,6 @@ int s2d_render_host(s2d_view *v, const double *means, const double *quats, const
         if (depth) depth[i] = himg[3 * npx + i];
         if (accumulation) accumulation[i] = himg[4 * npx + i];
     }
-    cudaFreeHost(hp);
     return S2D_OK;
 }
 

@@ -317,7 +317,51 @@ __global__ void __launch_bounds__(256) k_adam(float *__restrict__ params, const 
     }
 }
 
+// mapper.refine's backtracking step (mapper.py:319-335) on the contiguous opacity + colour part
+// of the packed block (elements [9n, 13n)): x = clip(x0 - step * g, 0, 1), with g zeroed for
+// surfels outside the target mask (mapper.py:320-321); every surfel is clipped, as the
+// reference's np.clip over the whole arrays does.
+__global__ void __launch_bounds__(256) k_refine_gd(float *__restrict__ x, const float *__restrict__ x0,
+                                                   const float *__restrict__ g, int64_t n, double step,
+                                                   const uint8_t *__restrict__ mask) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= 4 * n) return;
+    const int64_t surf = e < n ? e : (e - n) / 3;
+    const double gi = (mask && !mask[surf]) ? 0.0 : (double)g[e];
+    const double v = (double)x0[e] - step * gi;
+    x[e] = (float)fmin(fmax(v, 0.0), 1.0);
+}
+
+// max |g| over the targeted surfels' opacity + colour gradients (the L-inf norm of
+// mapper.py:322); non-negative floats order like their bit patterns.
+__global__ void __launch_bounds__(256) k_refine_gnorm(const float *__restrict__ g, int64_t n,
+                                                      const uint8_t *__restrict__ mask, float *out) {
+    float mx = 0.f;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < 4 * n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t surf = e < n ? e : (e - n) / 3;
+        if (!mask || mask[surf]) mx = fmaxf(mx, fabsf(g[e]));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0 && mx > 0.f) atomicMax(reinterpret_cast<int *>(out), __float_as_int(mx));
+}
+
 }  // namespace
+
+void launch_refine_gd(float *x, const float *x0, const float *g, int64_t n, double step, const uint8_t *mask,
+                      cudaStream_t s) {
+    if (n <= 0) return;
+    count_launch();
+    k_refine_gd<<<(unsigned)((4 * n + 255) / 256), 256, 0, s>>>(x, x0, g, n, step, mask);
+}
+
+void launch_refine_gnorm(const float *g, int64_t n, const uint8_t *mask, float *out, cudaStream_t s) {
+    if (n <= 0) return;
+    count_launch();
+    int blocks = (int)((4 * n + 255) / 256);
+    if (blocks > 1184) blocks = 1184;
+    k_refine_gnorm<<<blocks, 256, 0, s>>>(g, n, mask, out);
+}
 
 void launch_project_backward(const ProjectBwdArgs &a, cudaStream_t s) {
     const int64_t blocks = (a.P.n + S2D_PBWD_THREADS - 1) / S2D_PBWD_THREADS;

@@ -52,6 +52,9 @@ namespace s2d {
 namespace {
 
 constexpr uint32_t kFull = 0xffffffffu;
+// |(1 - T) - 0.5| band of the float32 transmittance inside which the depth mask is re-decided
+// in float64 (the float32 T of a pixel is within ~1e-5 of the reference's; 10x margin)
+constexpr float kMaskBand = 1e-4f;
 constexpr int kFwdWarps = S2D_FWD_WARPS, kBwdWarps = S2D_BWD_WARPS;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -102,22 +105,41 @@ __device__ __forceinline__ float fast_rcp(float x) {
     return y;
 }
 
-// Forward decision for a pair whose float32 m fell at or above the slot's lower threshold
-// cut - gb, or whose slot is flagged slow (tlo < 0: opacity within 8e-6 of the weight clamp,
-// or not above 1e-30).  Returns 0 if the pair does not blend, else the weight the reference
-// blends with.  Below cut - gb the reference's float64 m is below the cut, so the pixel lies
-// inside the reference bbox (the bbox is the ellipse's exact extent) and the pair blends with
-// the float32 weight, which for a non-flagged slot is positive and below the clamp (the fast
-// path in k_raster_fwd).  Inside the band [cut - gb, cut + gb], or when the weight is within
-// 4e-6 of the clamp, guard_resolve decides in float64.  (A tiny-opacity slot takes the
-// near-clamp branches harmlessly: its weight is far below the clamp.)  The backward
-// recomputes w with the same float32 operations and takes the clamp decision from the
-// forward's blend stream, so both passes see bit-identical weights.
+// Forward decision for a slow lane: a pair whose float32 m fell at or above the slot's lower
+// threshold cut - gb, or any passing lane of a flagged slot (near-clamp opacity, opacity not
+// above 1e-30, or an accurate slot).  Returns 0 if the pair does not blend, else the weight the
+// reference blends with; `act` false returns w unchanged (lanes of the warp that are not slow).
+//  - Accurate slot (|gb| > kAccurateGb, s2d_device.cuh): m is re-evaluated from the float64
+//    Minv and centre; within accurate_band of the cut the reference's own formula decides
+//    (guard_resolve); the weight is op 2^(-0.72 m) on that m, which k_raster_bwd recomputes
+//    with the same code.
+//  - Otherwise: below cut - gb the reference's float64 m is below the cut, so the pixel lies
+//    inside the reference bbox (the bbox is the ellipse's exact extent) and the pair blends with
+//    the float32 weight, which for a non-flagged slot is positive and below the clamp (the fast
+//    path in k_raster_fwd).  Inside the band [cut - gb, cut + gb], or when the weight is within
+//    4e-6 of the clamp, guard_resolve decides in float64.
+// The backward recomputes w with the same float32 operations and takes the clamp decision from
+// the forward's blend stream, so both passes see bit-identical weights.
 __device__ __forceinline__ float slow_weight(const ViewParams &P, const RasterArgs &a, uint32_t id, float op, float m,
-                                          float w, float tlo, int px, int py, bool &clamped, int &guard_hits) {
-    const bool nearclamp = tlo < 0.f;
+                                          float w, float gbs, bool act, int px, int py, bool &clamped,
+                                          int &guard_hits) {
     clamped = false;
-    if (m >= fabsf(tlo) || (nearclamp && fabsf(w - P.w_clamp_f) <= 4e-6f)) {
+    if (!act) return w;
+    const float gb = fabsf(gbs);
+    const bool nearclamp = gbs < 0.f;
+    bool resolve = false;
+    if (gb > kAccurateGb) {
+        float u, v;
+        double m64;
+        const float m32 = accurate_uvm(a.exact[id], px, py, u, v, m64);
+        if (fabs(m64 - P.maha_cut) <= accurate_band(gb, P.maha_cut)) resolve = true;
+        else if (!(m64 <= P.maha_cut)) return 0.f;
+        w = __fmul_rn(op, fast_exp2(__fmul_rn(m32, -0.72134752044448170368f)));
+        resolve = resolve || (nearclamp && fabsf(w - P.w_clamp_f) <= 4e-6f);
+    } else {
+        resolve = m >= __fsub_rn(P.maha_cut_f, gb) || (nearclamp && fabsf(w - P.w_clamp_f) <= 4e-6f);
+    }
+    if (resolve) {
         ++guard_hits;
         const int rr = guard_resolve(P, a, id, op, px, py);
         if (!(rr & 1)) return 0.f;
@@ -337,6 +359,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32, ((kArg || kMaxW || kNormal) ? 
     float2 c01 = make_float2(0.f, 0.f), c2d = make_float2(0.f, 0.f), n01 = make_float2(0.f, 0.f);
     float n2 = 0.f;
     float maxw = 0.f;
+    double T64 = 1.0, maxw64 = 0.0;  // argmax variant (affine): the reference's float64 state
     int argw = -1, nblend = 0, guard = 0;
     bool done = !inside;  // ray mode
     const float term_t = P.term_t_f;
@@ -378,11 +401,12 @@ __global__ void __launch_bounds__(kFwdWarps * 32, ((kArg || kMaxW || kNormal) ? 
                     if (keep) {
                         const BlockCentre bc = block_centre(q0, q1, (float)wx0, (float)wy0);
                         const float thi = __fadd_rn(P.maha_cut_f, gb), tlo = __fsub_rn(P.maha_cut_f, gb);
-                        const bool slow = gbs < 0.f || !(op > 1e-30f);
+                        // flagged slots send every passing lane to slow_weight
+                        const bool slow = gbs < 0.f || !(op > 1e-30f) || gb > kAccurateGb;
                         // forward slot: q0 = (f, g, cut + gb, opacity),
-                        // meta = (id, +-(cut - gb), lo.x, lo.y)
+                        // meta = (id, cut - gb or -3e38 (flagged), lo.x, lo.y)
                         sl.r.q0 = make_float4(bc.f, bc.g, thi, op);
-                        sl.meta.y = __float_as_uint(slow ? -tlo : tlo);
+                        sl.meta.y = __float_as_uint(slow ? -3.0e38f : tlo);
                         sl.meta.z = __float_as_uint(bc.lo.x);
                         sl.meta.w = __float_as_uint(bc.lo.y);
                     }
@@ -452,11 +476,9 @@ __global__ void __launch_bounds__(kFwdWarps * 32, ((kArg || kMaxW || kNormal) ? 
                     const float tlo = __uint_as_float(mt.y);
                     const bool slow = pass && m >= tlo;
                     if (__any_sync(kFull, slow)) {
-                        // every lane calls (a warp-uniform branch): a lane that is not slow passes
-                        // m = 0, which is below the band and cannot clamp its w (< clamp or 0),
-                        // so slow_weight returns its w unchanged
+                        // a warp-uniform branch; lanes that are not slow keep their w
                         bool clamped = false;
-                        w = slow_weight(P, a, mt.x, q0.w, slow ? m : 0.f, w, tlo, px, py, clamped, guard);
+                        w = slow_weight(P, a, mt.x, q0.w, m, w, sl.r.q3.w, slow, px, py, clamped, guard);
                         if (clamped) cl_bits |= bit;
                     }
                     {  // blend (blend_forward, _raster_kernels.py:47-55), a no-op where w = 0
@@ -471,12 +493,27 @@ __global__ void __launch_bounds__(kFwdWarps * 32, ((kArg || kMaxW || kNormal) ? 
                             n01 = __ffma2_rn(cc, make_float2(q3.x, q3.y), n01);
                             n2 = fmaf(contrib, q3.z, n2);
                         }
-                        if (kArg && contrib > maxw) {
-                            maxw = contrib;
-                            argw = (int)mt.x;
-                        }
                         T = fmaf(-w, T, T);  // T (1 - w), one rounding (T - w T loses bits for w near 1)
-                        lxy.x = T < term_t ? kNaN : lxy.x;
+                        if (kArg) {
+                            // render_with_argmax: the reference's float64 weight, transmittance and
+                            // strict `contrib > max_w` (_raster_kernels.py:42-55) for the pairs that
+                            // blend, so the argmax index and the termination are the reference's
+                            if (w > 0.f) {
+                                const ExactRec &e = a.exact[mt.x];
+                                const double m64 = exact_maha(e.cx, e.cy, e.ia, e.ib, e.ic, px, py);
+                                double w64 = dmul((double)q0.w, exp(dmul(-0.5, m64)));
+                                if (w64 > P.w_clamp) w64 = P.w_clamp;
+                                const double c64 = dmul(w64, T64);
+                                if (c64 > maxw64) {
+                                    maxw64 = c64;
+                                    argw = (int)mt.x;
+                                }
+                                T64 = dmul(T64, dsub(1.0, w64));
+                            }
+                            lxy.x = T64 < P.term_t ? kNaN : lxy.x;
+                        } else {
+                            lxy.x = T < term_t ? kNaN : lxy.x;
+                        }
                     }
                 }
                 if (kMaxW) {
@@ -539,10 +576,16 @@ __global__ void __launch_bounds__(kFwdWarps * 32, ((kArg || kMaxW || kNormal) ? 
             a.normal[3 * p + 2] = n2;
         }
         if (kArg) {
-            if (a.max_w) a.max_w[p] = maxw;
+            if (a.max_w) a.max_w[p] = kRay ? maxw : (float)maxw64;
             if (a.arg_w) a.arg_w[p] = argw;
         }
         a.aux[p] = make_int2(nblend, __float_as_int(T));
+        // `accumulation > 0.5` (the reference's depth mask, rasterizer.py:365-376) within the
+        // float32 error band of 0.5: re-decided in float64 by k_mask_fixup when a loss needs it
+        if (!kRay && fabsf(0.5f - T) <= kMaskBand) {
+            const int slot = atomicAdd(a.amb_count, 1);
+            a.amb_list[slot] = p;
+        }
     }
     const int nm = __popc(__ballot_sync(kFull, inside && (1.0f - T) > 0.5f));
     int gsum = guard;
@@ -678,7 +721,8 @@ __global__ void __launch_bounds__(kBwdWarps * 32, S2D_BWD_CTAS_PER_SM) k_raster_
             const float e2 = a.color[3 * p + 2] - a.target_rgb[3 * p + 2];
             const float ed = a.depth[p] - a.target_depth[p];
             const int nm = a.stats->n_mask;
-            const bool masked = a.accum[p] > 0.5f;
+            // aux.x bit 30: the mask was re-decided in float64 (k_mask_fixup), value in bit 29
+            const bool masked = (ax.x & (1 << 30)) ? ((ax.x >> 29) & 1) != 0 : a.accum[p] > 0.5f;
             if (a.loss_kind == S2D_LOSS_MSE) {
                 const float k = (float)(a.w_rgb * (2.0 / (3.0 * npx)));
                 gc0 = k * e0;
@@ -786,7 +830,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, S2D_BWD_CTAS_PER_SM) k_raster_
             z = re.iS;
             w = clamped ? P.w_clamp_f : __fmul_rn(r.q0.w, g);
         } else {
-            // backward slot: q0 = (f, g, lo.x, lo.y), meta.w = opacity
+            // backward slot: q0 = (f, g, lo.x, lo.y), meta.w = opacity (negative: accurate slot)
             const float4 q0 = r.q0, q1 = r.q1;
             const float m = slot_maha(make_float2(q0.x, q0.y), make_float2(q0.z, q0.w), q1, lxy, u, vv);
             // lanes outside the mask: keep (u, v) finite (a near-singular Minv could overflow
@@ -794,8 +838,17 @@ __global__ void __launch_bounds__(kBwdWarps * 32, S2D_BWD_CTAS_PER_SM) k_raster_
             u = inl ? u : 0.f;
             vv = inl ? vv : 0.f;
             g = fast_exp2(__fmul_rn(m, -0.72134752044448170368f));
+            const float opm = __uint_as_float(meta.w);
+            const bool accurate = inl && opm < 0.f;
+            if (__any_sync(kFull, accurate)) {  // warp-uniform: the forward's slow_weight evaluation
+                if (accurate) {
+                    double m64;
+                    const float m32 = accurate_uvm(a.exact[meta.x], px, py, u, vv, m64);
+                    g = fast_exp2(__fmul_rn(m32, -0.72134752044448170368f));
+                }
+            }
             z = q2.w;
-            w = clamped ? P.w_clamp_f : __fmul_rn(__uint_as_float(meta.w), g);
+            w = clamped ? P.w_clamp_f : __fmul_rn(fabsf(opm), g);
         }
         w = inl ? w : 0.f;
         const float Ti = inl ? Tn * fast_rcp(1.0f - w) : Tn;
@@ -873,7 +926,8 @@ __global__ void __launch_bounds__(kBwdWarps * 32, S2D_BWD_CTAS_PER_SM) k_raster_
             const BlockCentre bc = block_centre(sl.r.q0, sl.r.q1, (float)wx0, (float)wy0);
             sl.r.q0.x = bc.f;
             sl.r.q0.y = bc.g;
-            sl.meta.w = __float_as_uint(sl.r.q0.w);  // opacity
+            // opacity, negated for an accurate slot (s2d_device.cuh kAccurateGb)
+            sl.meta.w = __float_as_uint(fabsf(sl.r.q3.w) > kAccurateGb ? -sl.r.q0.w : sl.r.q0.w);
             sl.r.q0.z = bc.lo.x;
             sl.r.q0.w = bc.lo.y;
         }
@@ -895,7 +949,67 @@ __global__ void __launch_bounds__(kBwdWarps * 32, S2D_BWD_CTAS_PER_SM) k_raster_
     cp_wait<0>();
 }
 
+// Float64 re-decision of the depth mask `accumulation > 0.5` (rasterizer.py:365-376) for the
+// pixels the forward listed (float32 1 - T within kMaskBand of 0.5): the pixel's transmittance is
+// recomputed with the reference's arithmetic (blend_forward, _raster_kernels.py:32-55) over its
+// tile's depth-ordered list, one warp per pixel (lanes decide 32 pairs at a time, the product
+// runs in list order).  Corrects stats.n_mask, stores the decision in aux.x bits 30/29, and
+// clears the list so a second backward of the same forward is a no-op.  One CTA.
+__global__ void __launch_bounds__(256) k_mask_fixup(const RasterArgs a) {
+    const ViewParams &P = a.P;
+    const int cnt = *a.amb_count;
+    if (cnt == 0) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int q = warp; q < cnt; q += 8) {
+        const int p = a.amb_list[q];
+        const int px = p % P.W, py = p / P.W;
+        const int tile = (py / kTile) * P.ntx + px / kTile;
+        const int2 rg = a.ranges[tile];
+        double T64 = 1.0;
+        bool done = false;
+        for (int cb = rg.x; cb < rg.y && !done; cb += 32) {
+            const int j = cb + lane;
+            double f = 1.0;  // factor (1 - w) of this pair, 1 if it does not blend
+            if (j < rg.y) {
+                const uint32_t id = a.pair_ids[j];
+                const short4 b = a.rect[id];
+                if (px >= b.x && px <= b.y && py >= b.z && py <= b.w) {
+                    const ExactRec &e = a.exact[id];
+                    const double m64 = exact_maha(e.cx, e.cy, e.ia, e.ib, e.ic, px, py);
+                    if (m64 <= P.maha_cut) {
+                        double w64 = dmul((double)a.rec[id].q0.w, exp(dmul(-0.5, m64)));
+                        if (w64 > P.w_clamp) w64 = P.w_clamp;
+                        if (w64 > 0.0) f = dsub(1.0, w64);
+                    }
+                }
+            }
+            for (int k = 0; k < 32; ++k) {
+                const double fk = __shfl_sync(kFull, f, k);
+                if (!done) {
+                    if (T64 < P.term_t) done = true;
+                    else T64 = dmul(T64, fk);
+                }
+            }
+        }
+        if (lane == 0) {
+            const bool m64 = dsub(1.0, T64) > 0.5;
+            const int2 ax = a.aux[p];
+            const bool m32 = 1.0f - __int_as_float(ax.y) > 0.5f;
+            if (m64 != m32) atomicAdd(&a.stats->n_mask, m64 ? 1 : -1);
+            a.aux[p].x = (ax.x & ((1 << 29) - 1)) | (1 << 30) | (m64 ? (1 << 29) : 0);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *a.amb_count = 0;
+}
+
 }  // namespace
+
+void launch_mask_fixup(const RasterArgs &a, cudaStream_t s) {
+    if (a.P.mode != S2D_SPLAT_AFFINE) return;
+    count_launch();
+    k_mask_fixup<<<1, 256, 0, s>>>(a);
+}
 
 template <auto Kernel>
 static void ensure_smem(int bytes) {

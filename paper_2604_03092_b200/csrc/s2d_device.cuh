@@ -29,6 +29,7 @@ struct ViewParams {
     double mx, my, wmax, hmax;  // centre-margin gate (rasterizer.py:231-236)
     double wm1, hm1;            // W-1, H-1 (rasterizer.py:278-279)
     double w_clamp, maha_cut;   // 0.999, sigma^2
+    double term_t;              // termination_transmittance (float64: the argmax variant)
     float w_clamp_f, term_t_f, maha_cut_f;
     int W, H, ntx, nty;
     int64_t n;
@@ -258,10 +259,41 @@ __device__ __forceinline__ void project_exact(const ViewParams &P, const ParamVi
 }
 
 // The float64 quantities the per-pixel decisions depend on (reference centre and inv_abc),
-// written per on-screen surfel by k_project for the raster guard-band re-checks.
+// written per on-screen surfel by k_project for the raster guard-band re-checks.  For an
+// ill-conditioned splat (accurate_slot below) k_project also writes Minv = M^-1 in float64
+// (rows (a, b), (c, d)), which the raster kernels use to evaluate its whitened offset without
+// the float32 cancellation.
 struct ExactRec {
     double cx, cy, ia, ib, ic;
+    double ma, mb, mc, md;  // float64 Minv; written only for accurate slots
 };
+
+// A splat whose float32 guard band exceeds this (kappa(M) above ~32, or a sub-pixel sigma_min)
+// is an "accurate" slot: the float32 whitened offset u = A ex + (B ey + lo) cancels by
+// ~kappa(M), which leaves ~5e-7 kappa relative error in its weights and ~3 eps kappa in (u, v),
+// i.e. beyond the 1e-4 gradient gate for kappa ~ 100+.  Its per-pixel offsets are evaluated in
+// float64 from ExactRec in both raster passes (same code, so both see the same weights).
+constexpr float kAccurateGb = 1.3e-3f;
+
+// Whitened offset (u, v) = Minv (p - c) and m = |(u, v)|^2 of pixel (px, py) in float64 (the
+// accurate-slot path of k_raster_fwd / k_raster_bwd).  Returns m rounded to float32.
+__device__ __forceinline__ float accurate_uvm(const ExactRec &e, int px, int py, float &u, float &v, double &m64) {
+    const double dx = dsub((double)px, e.cx), dy = dsub((double)py, e.cy);
+    const double U = dfma(e.mb, dy, dmul(e.ma, dx));
+    const double V = dfma(e.md, dy, dmul(e.mc, dx));
+    m64 = dfma(U, U, dmul(V, V));
+    u = (float)U;
+    v = (float)V;
+    return (float)m64;
+}
+
+// Band around the cut inside which the accurate path defers to the reference's own formula
+// (exact_maha): the reference's conic m carries ~few eps64 kappa(Sigma) relative error, kappa
+// estimated from the guard band (gb ~ 4e-5 kappa(M)); generous by orders of magnitude.
+__device__ __forceinline__ double accurate_band(float gb, double cut) {
+    const double q = (double)gb * 2.5e4;
+    return 4e-14 * (1.0 + q * q) * cut + 1e-12;
+}
 
 // Ray-splat footprint (S2D_SPLAT_RAY).  With the camera-frame tangent axes
 // a = Bc[:,0], b = Bc[:,1] and centre p, H = K [a b p] maps tangent-plane (u, v, 1) to

@@ -39,12 +39,14 @@ struct SyncRegion {
     int *tickets;              // [16]
     int *n_drawn;              // on-screen surfels with a non-empty integer bbox (the sorted set)
     uint32_t *key_range;       // [2]: ~min, max depth key
+    uint32_t *proj_status;     // [ceil(n / kProjThreads)] compaction look-back of k_project
     uint32_t *depth_hist;      // [3 * kRadix]
     uint32_t *depth_status;    // [3][ceil(n / kSortTile) * kRadix]
     uint32_t *emit_status;     // [ceil(n / kEmitTile)]
     uint32_t *pair_hist;       // [2 * kRadix]
     uint32_t *pair_status;     // [2][ceil(pcap / kSortTile) * kRadix]
-    uint32_t *tie_claim;       // [n]
+    int *amb_count;            // pixels listed for k_mask_fixup
+    uint32_t *tie_ctl;         // [2]: long-run count, inversion-in-a-long-run flag (k_tie_fix)
     int2 *ranges;              // [ntiles]
     size_t bytes;
 };
@@ -62,6 +64,8 @@ struct ProjectArgs {
     s2d_view_stats *stats;
     uint32_t *key_range;  // [~min, max] of on-screen depth keys (sync region, zeroed)
     int *n_drawn;         // count of drawn surfels (sync region, zeroed)
+    int *ticket;          // tile ticket (sync region, zeroed)
+    uint32_t *status;     // look-back status words, one per projection tile (sync region, zeroed)
 };
 void launch_project(const ProjectArgs &a, cudaStream_t s);
 
@@ -71,8 +75,9 @@ void launch_radix_hist(uint32_t *keys, const int *d_n, int n, const uint32_t *ke
 void launch_onesweep(const uint32_t *kin, const uint32_t *vin, uint32_t *kout, uint32_t *vout,
                      const int *d_n, int cap, int n_host, int shift, const uint32_t *hist_pass,
                      uint32_t *status, int *ticket, cudaStream_t s);
+// ctl: 2 zeroed words; list: >= cap / 64 + 1 words; scratch: cap words (may not alias keys / vals)
 void launch_tie_fix(const uint32_t *keys, uint32_t *vals, const double *z64, const int *d_n, int cap,
-                    uint32_t *claim, cudaStream_t s);
+                    uint32_t *ctl, uint32_t *list, uint32_t *scratch, cudaStream_t s);
 
 struct EmitArgs {
     const uint32_t *order;
@@ -123,9 +128,14 @@ struct RasterArgs {
     const float *d_color, *d_depth, *d_normal, *d_accum;
     float *grad2d;  // [n][16] per-view 2D gradients (layout in raster.cu, k_raster_bwd)
     double *loss_accum;
+    // pixels whose float32 depth-mask decision is within the error band (k_mask_fixup)
+    int *amb_count;  // sync region (zeroed per view)
+    int *amb_list;   // [H*W]
 };
 void launch_raster_forward(const RasterArgs &a, cudaStream_t s);
 void launch_raster_backward(const RasterArgs &a, cudaStream_t s);
+// float64 re-decision of the ambiguous depth-mask pixels (before a masked loss's backward)
+void launch_mask_fixup(const RasterArgs &a, cudaStream_t s);
 
 struct ProjectBwdArgs {
     ViewParams P;
@@ -139,6 +149,11 @@ void launch_project_backward(const ProjectBwdArgs &a, cudaStream_t s);
 
 void launch_adam(float *params, const float *grads, float *m1, float *m2, int64_t n, int64_t step,
                  const s2d_adam_config &cfg, const uint8_t *mask, cudaStream_t s);
+
+// mapper.refine's backtracking GD step and gradient norm on the opacity + colour block (optim.cu)
+void launch_refine_gd(float *x, const float *x0, const float *g, int64_t n, double step, const uint8_t *mask,
+                      cudaStream_t s);
+void launch_refine_gnorm(const float *g, int64_t n, const uint8_t *mask, float *out, cudaStream_t s);
 
 // map maintenance (map.cu)
 void launch_transform(const float *in, float *out, int64_t n, const double pose[8], cudaStream_t s);

@@ -240,7 +240,13 @@ def refine(map_: GlobalSurfelMap, keyframe_ids, observations, intr: CameraIntrin
            cfg: RefinementConfig = RefinementConfig(),
            raster_cfg: RasterConfig = DEFAULT_RASTER_CONFIG) -> RefinementReport:
     """Backtracking GD on colours/opacities of the surfels bound to ``keyframe_ids``
-    (mapper.py:276-349).  ``observations`` maps keyframe_id -> (rgb, depth)."""
+    (mapper.py:276-349).  ``observations`` maps keyframe_id -> (rgb, depth).
+
+    The map stays on the device: every trial is the views' fused forward + backward
+    (s2d_forward / s2d_backward), the L-inf norm and the clipped step run in
+    s2d_refine_gnorm / s2d_refine_gd.  Like the reference, a trial clips every surfel's
+    colour and opacity to [0, 1] (np.clip over the whole arrays, mapper.py:334-335), and the
+    last rejected trial restores the previous state (mapper.py:346-347)."""
     keyframe_ids = [k for k in keyframe_ids if k in observations]
     poses = [map_.keyframe_poses[k] for k in keyframe_ids]
     target_mask = np.isin(np.asarray(map_.surfels.keyframe_ids), np.asarray(keyframe_ids, dtype=np.int64))
@@ -250,9 +256,9 @@ def refine(map_: GlobalSurfelMap, keyframe_ids, observations, intr: CameraIntrin
     vs = _ViewSet(intr, poses, [observations[k][0] for k in keyframe_ids],
                   [observations[k][1] for k in keyframe_ids], raster_cfg, None)
     dev = vs.dev
+    L = N.lib()
     params = pack_params(map_.surfels, dev) if n else torch.zeros(13, device=dev)
-    P = unpack_params(params, n) if n else None
-    grads = torch.zeros_like(params)
+    grads = [torch.zeros_like(params), torch.zeros_like(params)]  # current / trial
     loss_acc = torch.zeros(1, dtype=torch.float64, device=dev)
     lw = cfg.loss
 
@@ -264,41 +270,43 @@ def refine(map_: GlobalSurfelMap, keyframe_ids, observations, intr: CameraIntrin
         finite = [x for x in vals if math.isfinite(x)]
         return float(np.mean(finite)) if finite else float("inf")
 
-    def total_loss_and_grads():
-        grads.zero_()
+    def total_loss_and_grads(g):
+        """Sum over the views of the reference loss and its gradients (mapper.py:300-313)."""
+        g.zero_()
         loss_acc.zero_()
         for v in range(len(poses)):
             forward_checked(vs.view, params, n, vs.poses[v], vs.cam, vs.cfg, vs.img)
             vs.view.backward(params, n, vs.img,
                              loss_struct(N.LOSS_MSE, lw.mse, lw.depth, True, vs.rgb[v], vs.depth[v]),
-                             grads, loss_acc)
-        G = unpack_params(grads, n)
-        return float(loss_acc.item()), G["colors"].clone(), G["opacities"].clone()
+                             g, loss_acc)
+        return float(loss_acc.item())
 
     psnr_before = view_psnrs()
     if cfg.iterations == 0 or not target_mask.any() or n == 0:
         return RefinementReport([], psnr_before, psnr_before, 0)
-    mask_t = torch.from_numpy(target_mask).to(dev)
-    loss, gc, go = total_loss_and_grads()
+    mask_t = torch.from_numpy(target_mask.astype(np.uint8)).to(dev)
+    gn = torch.zeros(1, device=dev)
+    params0 = torch.empty_like(params)
+    stream = _stream()
+    loss = total_loss_and_grads(grads[0])
     losses = [loss]
     accepted = 0
     step_scale = cfg.initial_step
     for _ in range(cfg.iterations):
-        gc[~mask_t] = 0.0
-        go[~mask_t] = 0.0
-        gnorm = max(float(gc.abs().max()), float(go.abs().max()))
+        N.check(L.s2d_refine_gnorm(stream, N.dptr(grads[0]), n, N.dptr(mask_t), N.dptr(gn)), "s2d_refine_gnorm")
+        gnorm = float(gn.item())
         if gnorm < 1e-14:
             break
         step = step_scale / gnorm
-        colors0 = P["colors"].clone()
-        opac0 = P["opacities"].clone()
+        params0.copy_(params)
         improved = False
         while step >= cfg.min_step / gnorm:
-            P["colors"].copy_(torch.clamp(colors0 - step * gc, 0.0, 1.0))
-            P["opacities"].copy_(torch.clamp(opac0 - step * go, 0.0, 1.0))
-            new_loss, new_gc, new_go = total_loss_and_grads()
+            N.check(L.s2d_refine_gd(stream, N.dptr(params), N.dptr(params0), N.dptr(grads[0]), n, float(step),
+                                    N.dptr(mask_t)), "s2d_refine_gd")
+            new_loss = total_loss_and_grads(grads[1])
             if new_loss < loss:
-                loss, gc, go = new_loss, new_gc, new_go
+                loss = new_loss
+                grads.reverse()
                 losses.append(loss)
                 accepted += 1
                 improved = True
@@ -306,17 +314,17 @@ def refine(map_: GlobalSurfelMap, keyframe_ids, observations, intr: CameraIntrin
                 break
             step *= 0.5
         if not improved:
-            P["colors"].copy_(colors0)
-            P["opacities"].copy_(opac0)
+            params.copy_(params0)
             break
     if accepted:
+        P = unpack_params(params, n)
+        cols = np.clip(np.asarray(map_.surfels.colors, dtype=float), 0.0, 1.0)
+        ops = np.clip(np.asarray(map_.surfels.opacities, dtype=float), 0.0, 1.0)
         idx = np.flatnonzero(target_mask)
-        cols = P["colors"].double().cpu().numpy()
-        ops = P["opacities"].double().cpu().numpy()
-        map_.surfels.colors = np.array(map_.surfels.colors, dtype=float, copy=True)
-        map_.surfels.opacities = np.array(map_.surfels.opacities, dtype=float, copy=True)
-        map_.surfels.colors[idx] = cols[idx]
-        map_.surfels.opacities[idx] = ops[idx]
+        cols[idx] = P["colors"].double().cpu().numpy()[idx]
+        ops[idx] = P["opacities"].double().cpu().numpy()[idx]
+        map_.surfels.colors = cols
+        map_.surfels.opacities = ops
     return RefinementReport(losses, psnr_before, view_psnrs(), accepted)
 
 

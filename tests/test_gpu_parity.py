@@ -65,8 +65,9 @@ def test_images_vs_reference(goldens, name):
     for key in ("color", "depth", "accumulation", "max_w"):
         ok, mx, l2 = gate(im[key], g[key])
         assert ok, (key, mx, l2)
-    agree = np.mean(im["arg_w"] == g["arg_w"])
-    assert agree >= 0.999, agree
+    # render_with_argmax: the index output is bit-exact (float64 weights/transmittance in the
+    # argmax variant of the forward, _raster_kernels.py:52-54, rasterizer.py:327-328)
+    assert np.array_equal(im["arg_w"], g["arg_w"]), int((im["arg_w"] != g["arg_w"]).sum())
 
 
 @pytest.mark.parametrize("name", ["kat_random40", "c1", "c1_posed"])
@@ -170,7 +171,7 @@ def test_external_seeds_normal_and_accumulation_grads():
     ref = O.render(sc.surfels, pose, sc.intr)
     og = O.backward(sc.surfels, pose, sc.intr, ref, *seeds)
     for f in ("colors", "opacities", "means", "quats", "scales"):
-        ok, mx, l2 = gate(g[f], getattr(og, f), tol=2e-4)
+        ok, mx, l2 = gate(g[f], getattr(og, f))
         assert ok, (f, mx, l2)
 
 
@@ -348,19 +349,44 @@ def test_tiny_splats_on_pixel_centres(kind):
 
 def test_needle_splat_geometry_gradients():
     """config2(4) seen head-on holds a needle-like splat (surfel 273: cov2 eigenvalues 6.2 and
-    1.6e-5 px^2, kappa(M) ~ 620).  Its whitened offsets u = A ex + (B ey + lo) cancel ~1e3
-    down to O(1) in float32, so its geometry gradients carry ~kappa eps ~ 1e-4 relative error:
-    this test records that bound (3e-4 of the tensor max for means / quats / scales, 1e-4 for
-    opacities and colours, whose chain does not go through the whitening)."""
+    1.6e-5 px^2, kappa(M) ~ 620).  In float32 its whitened offsets u = A ex + (B ey + lo) would
+    cancel ~1e3 down to O(1); as an accurate slot (kappa(M) > ~32) both raster passes evaluate
+    them from the float64 Minv, so all five gradient groups meet the 1e-4 gate."""
     sc = scenes.config2(4)
     pose = SE3Pose.identity()
     intr = R.CameraIntrinsics(250.0, 250.0, 160.0, 120.0, 320, 240)
     run = Run(sc.surfels, pose, intr, normal=True, argmax=False)
     ref = O.render(sc.surfels, pose, intr)
     trgb, tdep = far_targets(ref.color, ref.depth, np.random.default_rng(29))
-    g, loss = run.backward("mse", trgb, tdep, 1.0, 0.1, True)
-    oloss, og, _ = O.loss_and_grads(sc.surfels, pose, intr, trgb, tdep, "mse", 1.0, 0.1, mask_depth=True)
-    assert abs(loss - oloss) <= 1e-5 * abs(oloss)
-    for f, tol in (("colors", 1e-4), ("opacities", 1e-4), ("means", 3e-4), ("quats", 3e-4), ("scales", 3e-4)):
-        ok, mx, l2 = gate(g[f], getattr(og, f), tol)
-        assert ok, (f, mx, l2)
+    for kind in ("mse", "l1"):
+        mask = kind == "mse"
+        g, loss = run.backward(kind, trgb, tdep, 1.0, 0.1, mask)
+        oloss, og, _ = O.loss_and_grads(sc.surfels, pose, intr, trgb, tdep, kind, 1.0, 0.1, mask_depth=mask)
+        assert abs(loss - oloss) <= 1e-5 * abs(oloss)
+        for f in ("colors", "opacities", "means", "quats", "scales"):
+            ok, mx, l2 = gate(g[f], getattr(og, f))
+            assert ok, (kind, f, mx, l2)
+
+
+@pytest.mark.parametrize("seed", range(32))
+def test_config2_seed_sweep_all_groups(seed):
+    """BASELINE config 2 scenes, seeds 0-31 (each holds a few ill-conditioned splats): images and
+    all five parameter groups within the 1e-4 gate, MSE (reference depth mask) and L1."""
+    sc = scenes.config2(seed)
+    pose = sc.poses[0]
+    run = Run(sc.surfels, pose, sc.intr, normal=True, argmax=True)
+    ref = O.render(sc.surfels, pose, sc.intr)
+    im = run.images()
+    for key in ("color", "depth", "accumulation", "normal", "max_w"):
+        ok, mx, l2 = gate(im[key], getattr(ref, key))
+        assert ok, (key, mx, l2)
+    assert np.array_equal(im["arg_w"], ref.arg_w)
+    trgb, tdep = far_targets(ref.color, ref.depth, np.random.default_rng(100 + seed))
+    for kind in ("mse", "l1"):
+        mask = kind == "mse"
+        g, loss = run.backward(kind, trgb, tdep, 1.0, 0.1, mask)
+        oloss, og, _ = O.loss_and_grads(sc.surfels, pose, sc.intr, trgb, tdep, kind, 1.0, 0.1, mask_depth=mask)
+        assert abs(loss - oloss) <= 1e-5 * abs(oloss)
+        for f in ("colors", "opacities", "means", "quats", "scales"):
+            ok, mx, l2 = gate(g[f], getattr(og, f))
+            assert ok, (seed, kind, f, mx, l2)
