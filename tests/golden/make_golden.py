@@ -210,9 +210,128 @@ def capture_map_ops():
           f"marked px {int(marked.sum())} -> {os.path.getsize(path) / 1e3:.0f} kB")
 
 
+def _random_rows(rng, n, op_lo=0.3, op_hi=0.8):
+    """The reference rasterizer tests' random-scene distribution (test_rasterizer.py random_scene,
+    restated): means in [-.8,.8]x[-.6,.6]x[1.5,3.5], axis-angle rotations up to 0.6 rad, tangent
+    scales U(.05,.18), opacity U(op_lo, op_hi), colour U(.1,.9); float32-representable."""
+    rows = []
+    for _ in range(n):
+        ax = rng.normal(size=3)
+        ax /= np.linalg.norm(ax)
+        rows.append(([rng.uniform(-0.8, 0.8), rng.uniform(-0.6, 0.6), rng.uniform(1.5, 3.5)],
+                     UnitQuaternion.from_axis_angle(ax, rng.uniform(0, 0.6)).array(), rng.uniform(0.05, 0.18, 2),
+                     rng.uniform(op_lo, op_hi), rng.uniform(0.1, 0.9, 3)))
+    means, quats, scales, ops, cols = zip(*rows)
+    f = scenes.f32
+    return R.SurfelArrays(f(np.array(means)), f(np.array(quats)), f(np.array(scales)), f(np.array(ops)),
+                          f(np.array(cols)), np.ones(n), np.zeros(n, np.int64), np.zeros(n, np.int64))
+
+
+def capture_fd():
+    """The reference's gradient checks (test_rasterizer.py:263-291, test_acceptance.py:207-243,
+    criterion 2): 20 seeded 12-surfel scenes at 64x48 whose accumulation stays 1e-3 clear of the
+    0.5 mask edge, LossWeights(1.0, 0.2); the reference's grad_color_opacity and its central
+    finite differences (h = 1e-4) of render_loss(render()) per colour channel and opacity."""
+    intr = R.CameraIntrinsics(60.0, 60.0, 32.0, 24.0, 64, 48)
+    pose = SE3Pose.identity()
+    w = R.LossWeights(mse=1.0, depth=0.2)
+    out = {"intr": np.array([60.0, 60.0, 32.0, 24.0, 64, 48]), "loss_weights": np.array([w.mse, w.depth])}
+    done, seed, checked = 0, 100, 0
+    while done < 20:
+        rng = np.random.default_rng(seed)
+        seed += 1
+        arr = _random_rows(rng, 12)
+        buf = R.render(arr, pose, intr)
+        if np.min(np.abs(buf.accumulation - 0.5)) <= 1e-3:
+            continue
+        trng = np.random.default_rng(seed + 5000)
+        trgb = np.clip(buf.color + trng.normal(scale=0.1, size=buf.color.shape), 0, 1)
+        tdep = np.abs(buf.depth + trng.normal(scale=0.1, size=buf.depth.shape))
+        gc, go, loss = R.grad_color_opacity(arr, pose, intr, trgb, tdep, w)
+        h = 1e-4
+        fdc = np.zeros_like(gc)
+        fdo = np.zeros_like(go)
+        for i in range(len(arr)):
+            for ch in range(3):
+                orig = arr.colors[i, ch]
+                arr.colors[i, ch] = orig + h
+                lp = R.render_loss(R.render(arr, pose, intr), trgb, tdep, w)
+                arr.colors[i, ch] = orig - h
+                lm = R.render_loss(R.render(arr, pose, intr), trgb, tdep, w)
+                arr.colors[i, ch] = orig
+                fdc[i, ch] = (lp - lm) / (2 * h)
+            orig = arr.opacities[i]
+            arr.opacities[i] = orig + h
+            lp = R.render_loss(R.render(arr, pose, intr), trgb, tdep, w)
+            arr.opacities[i] = orig - h
+            lm = R.render_loss(R.render(arr, pose, intr), trgb, tdep, w)
+            arr.opacities[i] = orig
+            fdo[i] = (lp - lm) / (2 * h)
+        checked += int((np.abs(gc) > 1e-8).sum() + (np.abs(go) > 1e-8).sum())
+        k = f"s{done:02d}_"
+        out.update({k + "means": arr.means, k + "quats": arr.quats, k + "scales": arr.scales,
+                    k + "opacities": arr.opacities, k + "colors": arr.colors, k + "target_rgb": trgb,
+                    k + "target_depth": tdep, k + "grad_color": gc, k + "grad_opacity": go,
+                    k + "loss": np.float64(loss), k + "fd_color": fdc, k + "fd_opacity": fdo})
+        done += 1
+    path = os.path.join(HERE, "fd_scenes.npz")
+    np.savez_compressed(path, **out)
+    print(f"fd_scenes: 20 scenes, {checked} checked gradients -> {os.path.getsize(path) / 1e3:.0f} kB")
+
+
+def capture_refine():
+    """The reference's mapper.refine (mapper.py:276-349) on a seeded three-keyframe map: the
+    config-1 cloud bound round-robin to keyframes 0, 5, 10 at nearby poses, colours perturbed
+    by U(-.15,.15) and clipped (test_acceptance.py:385-411 style), observations = the
+    unperturbed map's renders (depth normalised by the accumulation).  Two runs: 10
+    iterations over all three keyframes, and 3 iterations over keyframe 0 only (untargeted
+    surfels)."""
+    from surfelslam import mapper as M
+    f = scenes.f32
+    c1 = scenes.config1(3)
+    intr = ref_intr(c1.intr)
+    arr = ref_arrays(c1.surfels)
+    n = len(arr.means)
+    frames = [0, 5, 10]
+    poses = {0: Sim3Transform(1.0, UnitQuaternion.from_axis_angle([0, 1, 0], 0.04), np.array([0.03, 0.0, 0.0])),
+             5: Sim3Transform(1.0, UnitQuaternion.from_axis_angle([1, 0, 0.2], 0.05), np.array([-0.05, 0.02, 0.05])),
+             10: Sim3Transform(1.0, UnitQuaternion.from_axis_angle([0.3, 1, 0], -0.06), np.array([0.0, -0.04, -0.06]))}
+    arr.keyframe_ids = np.array([frames[i % 3] for i in range(n)], np.int64)
+    obs = {}
+    for k in frames:
+        buf = R.render(arr, poses[k], intr)
+        obs[k] = (buf.color, buf.depth / np.maximum(buf.accumulation, 1e-12))
+    rng = np.random.default_rng(8)
+    pert = arr.copy()
+    pert.colors = f(np.clip(arr.colors + rng.uniform(-0.15, 0.15, arr.colors.shape), 0, 1))
+    out = {"means": pert.means, "quats": pert.quats, "scales": pert.scales, "opacities": pert.opacities,
+           "colors": pert.colors, "keyframe_ids": pert.keyframe_ids, "frames": np.array(frames),
+           "intr": np.array([intr.fx, intr.fy, intr.cx, intr.cy, intr.width, intr.height], float)}
+    for k in frames:
+        out[f"pose_{k}"] = poses[k].packed()
+        out[f"obs_rgb_{k}"], out[f"obs_depth_{k}"] = obs[k]
+    for tag, kfs, iters in (("all", frames, 10), ("kf0", [0], 3)):
+        m = M.GlobalSurfelMap(pert.copy(), dict(poses))
+        rep = M.refine(m, kfs, obs, intr, M.RefinementConfig(iterations=iters))
+        out.update({f"{tag}_losses": np.array(rep.losses), f"{tag}_psnr": np.array([rep.psnr_before, rep.psnr_after]),
+                    f"{tag}_accepted": np.int64(rep.accepted_steps), f"{tag}_colors": m.surfels.colors,
+                    f"{tag}_opacities": m.surfels.opacities, f"{tag}_iters": np.int64(iters)})
+        print(f"refine[{tag}]: losses {len(rep.losses)}, accepted {rep.accepted_steps}, "
+              f"psnr {rep.psnr_before:.3f} -> {rep.psnr_after:.3f}")
+    path = os.path.join(HERE, "refine_ref.npz")
+    np.savez_compressed(path, **out)
+    print(f"refine_ref -> {os.path.getsize(path) / 1e3:.0f} kB")
+
+
 def main():
     if len(sys.argv) > 1 and sys.argv[1] == "map_ops":
         capture_map_ops()
+        return
+    if len(sys.argv) > 1 and sys.argv[1] == "fd":
+        capture_fd()
+        return
+    if len(sys.argv) > 1 and sys.argv[1] == "refine":
+        capture_refine()
         return
     exact = R.RasterConfig(weight_clamp=1.0)
     intr, kats = kat_scenes()
@@ -231,6 +350,8 @@ def main():
     c2 = scenes.config2(0)
     capture("c2", c2.surfels, ident, c2.intr, images_f32=True, grads=False)
     capture_map_ops()
+    capture_fd()
+    capture_refine()
 
 
 if __name__ == "__main__":
