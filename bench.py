@@ -177,41 +177,140 @@ def run_cpu_port(sc, targets, views, threads):
     return time.perf_counter() - t0
 
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def _ref_worker(job):
+    """One view of the reference's own fwd + colour/opacity bwd (surfelslam.rasterizer.
+    grad_color_opacity: numba, single-threaded kernels) in a fresh process: returns seconds."""
+    path, v, pose8 = job
+    import numpy as np
+    os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join(REF_DIR, ".numba_cache"))
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    from surfelslam import rasterizer as RR
+    from surfelslam.geometry import Sim3Transform, UnitQuaternion
+    d = np.load(path, mmap_mode="r")
+    n = len(d["means"])
+    arr = RR.SurfelArrays(np.array(d["means"]), np.array(d["quats"]), np.array(d["scales"]), np.array(d["opacities"]),
+                          np.array(d["colors"]), np.ones(n), np.zeros(n, np.int64), np.zeros(n, np.int64))
+    fx, fy, cx, cy, w, h = d["intr"]
+    intr = RR.CameraIntrinsics(float(fx), float(fy), float(cx), float(cy), int(w), int(h))
+    pose = Sim3Transform(float(pose8[0]), UnitQuaternion.from_array(np.array(pose8[4:8])), np.array(pose8[1:4]))
+    trgb, tdep = np.array(d[f"rgb{v}"]), np.array(d[f"dep{v}"])
+    t0 = time.perf_counter()
+    RR.grad_color_opacity(arr, pose, intr, trgb, tdep, RR.LossWeights(1.0, 0.1))
+    return time.perf_counter() - t0
+
+
+class RefPool:
+    """The reference's own CPU path (baseline/_ref: /root/reference installed with pip) timed on
+    config-4 views, one view per process, `procs` processes (views are independent,
+    mapper.py:300-307; its numba kernels are single-threaded, _raster_kernels.py:16)."""
+
+    def __init__(self, surf, intr, poses, targets, views, procs):
+        import multiprocessing as mp
+        import tempfile
+        import numpy as np
+        from paper_2604_03092_b200.geometry import as_packed_pose
+        tmp = tempfile.NamedTemporaryFile(suffix=".npz", delete=False)
+        data = {k: np.asarray(getattr(surf, k), np.float64) for k in ("means", "quats", "scales", "opacities", "colors")}
+        data["intr"] = np.array([intr.fx, intr.fy, intr.cx, intr.cy, intr.width, intr.height], float)
+        for v in views:
+            data[f"rgb{v}"], data[f"dep{v}"] = targets[v]
+        np.savez(tmp, **data)
+        tmp.close()
+        self.path = tmp.name
+        self.jobs = {v: (tmp.name, v, [float(x) for x in as_packed_pose(poses[v])]) for v in views}
+        self.procs = procs
+        self.pool = mp.get_context("spawn").Pool(procs)
+        self.pool.map(_ref_worker, [self.jobs[v] for v in views[:procs]])  # numba JIT / cache load per worker
+
+    def time(self, views):
+        t0 = time.perf_counter()
+        per = self.pool.map(_ref_worker, [self.jobs[v] for v in views])
+        return time.perf_counter() - t0, per
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+        os.unlink(self.path)
+
+
+def reference_available():
+    return os.path.isdir(os.path.join(REF_DIR, "surfelslam"))
+
+
 def reference_arm(args):
-    """--impl reference: the CPU port of the reference path on all host threads."""
+    """--impl reference: the reference's own CPU implementation of the path (surfelslam's numba
+    grad_color_opacity from baseline/_ref, one view per process on the host cores) when it is
+    installed, else the float64 C port of it (oracle/); rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     import numpy as np
-    from paper_2604_03092_b200 import scenes
     import oracle as O
     sc = make_workload(args.seed, args.small)
-    # targets: CPU port render of the unperturbed map (no GPU on this arm)
     threads = len(os.sched_getaffinity(0))
-    nv = min(threads, len(sc.poses))
+    px = sc.intr.width * sc.intr.height
+    use_ref = reference_available()
+    nv = min(threads, len(sc.poses), 16 if use_ref else 64)
+    # targets: CPU render of the unperturbed map (no GPU on this arm)
     targets = {}
     for v in range(nv):
         b = O.render(sc.surfels, sc.poses[v], sc.intr, with_normal=False)
         targets[v] = (b.color, b.depth)
-    px = sc.intr.width * sc.intr.height
-    for _ in range(args.warmup):
-        run_cpu_port(sc, targets, list(range(nv)), threads)
-    times = [run_cpu_port(sc, targets, list(range(nv)), threads) for _ in range(args.steps)]
+    views = list(range(nv))
+    if use_ref:
+        rp = RefPool(sc.extra["perturbed"], sc.intr, sc.poses, targets, views, nv)
+        run = lambda: rp.time(views)[0]  # noqa: E731
+        kind = "reference"
+        sample = (f"{nv} config-4 views per step, the reference's grad_color_opacity (numba; fwd + colour/opacity "
+                  f"backward, no geometry gradients), one view per process")
+    else:
+        run = lambda: run_cpu_port(sc, targets, views, threads)  # noqa: E731
+        kind = "port"
+        sample = f"{nv} config-4 views fwd+bwd per step (float64 C port of the reference path, oracle/), one per thread"
+    warm = min(args.warmup, 1)  # the pool start already JIT-compiled / cache-loaded every worker
+    for _ in range(warm):
+        run()
+    times = [run() for _ in range(args.steps)]
+    if use_ref:
+        rp.close()
     tot = sum(times)
     val = nv * px * args.steps / tot / 1e6
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "Mpix/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "steps": args.steps, "warmup": warm, "ms_per_step": 1e3 * tot / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded config-4 generator)",
-            "config": {"workload": WORKLOAD, "sample": f"{nv} views fwd+bwd per step, one per thread"},
-            "cpu_baseline": {"value": val, "unit": "Mpix/s", "cores": threads, "kind": "port",
-                             "sample": f"{nv} config-4 views fwd+bwd (float64 C port of the reference path, oracle/)"},
+            "config": {"workload": WORKLOAD + (" [SMALL]" if args.small else ""), "sample": sample},
+            "cpu_baseline": {"value": val, "unit": "Mpix/s", "cores": nv if use_ref else threads, "kind": kind,
+                             "sample": sample},
             "e2e": {"value": val, "unit": "Mpix/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def spawn_ranks(args):
+    """`bench.py --gpus N` outside torchrun: re-run this script under torch.distributed.run with
+    N ranks (one per GPU, NCCL, 127.0.0.1 rendezvous); rank 0 prints the JSON line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "RANK" not in os.environ:
+        sys.exit(spawn_ranks(args))
     if args.impl == "reference":
         reference_arm(args)
         return
@@ -239,7 +338,8 @@ def main():
     ref = AdamRefiner(sc.extra["perturbed"], sc.intr, sc.poses, rgbs, deps, loss, AdamConfig(), device=dev,
                       inflight=inflight, cuda_graph=graph)
     for _ in range(args.warmup):
-        ref.step()
+        ref.step(sync=False)
+    ref.losses()
     clocks = ClockSampler(local_rank)
     if world > 1:
         dist.barrier()
@@ -250,9 +350,11 @@ def main():
     time.sleep(0.2)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    losses = [ref.step() for _ in range(args.steps)]
+    for _ in range(args.steps):
+        ref.step(sync=False)  # queued: the host checks the previous iteration while this one runs
     e1.record()
     torch.cuda.synchronize()
+    losses = ref.losses()[-args.steps:]
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
@@ -277,7 +379,8 @@ def main():
     tb0.record()
     nb_steps = max(3, min(args.steps, 10))
     for _ in range(nb_steps):
-        ref.step()
+        ref.step(sync=False)
+    ref.losses()
     tb1.record()
     torch.cuda.synchronize()
     ph = ref.view.timing(reset=True)
@@ -320,16 +423,19 @@ def main():
     ref2 = AdamRefiner(sc.extra["perturbed"], sc.intr, sc.poses, host_rgb, host_dep, loss, AdamConfig(), device=dev,
                        host_targets=True, inflight=inflight, cuda_graph=graph)
     for _ in range(args.warmup):
-        ref2.step()
+        ref2.step(sync=False)
+    ref2.losses()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2.record()
     for _ in range(args.steps):
-        ref2.step()
+        ref2.step(sync=False)  # each step: targets H2D from pinned memory, loss D2H to pinned memory
     e3.record()
     torch.cuda.synchronize()
+    e2e_losses = ref2.losses()[-args.steps:]
+    assert len(e2e_losses) == args.steps
     t2 = torch.tensor([e2.elapsed_time(e3)], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t2, op=dist.ReduceOp.MAX)
@@ -345,8 +451,25 @@ def main():
         nv = args.cpu_views or min(max(threads, 1), n_views)
         targets = {v: (rgbs[v].double().cpu().numpy(), deps[v].double().cpu().numpy()) for v in range(nv)}
         secs = run_cpu_port(sc, targets, list(range(nv)), threads)
-        cpu = {"value": nv * px / secs / 1e6, "unit": "Mpix/s", "cores": min(threads, nv), "kind": "port",
-               "sample": f"{nv} config-4 views fwd+bwd in {secs:.1f}s (float64 C port of the reference path, oracle/)"}
+        port = {"value": nv * px / secs / 1e6, "unit": "Mpix/s", "cores": min(threads, nv), "kind": "port",
+                "sample": f"{nv} config-4 views fwd+bwd in {secs:.1f}s (float64 C port of the reference path, oracle/)"}
+        # the reference's own numba path (baseline/_ref): fwd + colour/opacity backward only (it
+        # has no geometry gradients), one view per process; 1 core and a view-parallel pool
+        cpu = port
+        if reference_available():
+            procs = min(threads, nv, 16)
+            rp = RefPool(sc.extra["perturbed"], sc.intr, sc.poses, targets, list(range(nv)), procs)
+            ref1 = rp.time([0])
+            refp = rp.time(list(range(procs)))
+            rp.close()
+            nv = procs
+            cpu = {"value": nv * px / refp[0] / 1e6, "unit": "Mpix/s", "cores": procs, "kind": "reference",
+                   "sample": (f"{nv} config-4 views, the reference's grad_color_opacity (numba; fwd + colour/opacity "
+                              f"backward, no geometry gradients) one view per process, {procs} processes: "
+                              f"{refp[0]:.1f}s"),
+                   "one_core": {"value": px / ref1[0] / 1e6, "unit": "Mpix/s", "cores": 1,
+                                "sample": f"1 view in {ref1[0]:.2f}s"},
+                   "port": port}
 
     if rank == 0:
         line = {

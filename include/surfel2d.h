@@ -152,6 +152,13 @@ int s2d_view_stats_accumulate(s2d_view *view, void *stream, s2d_view_stats *acc_
 /* set the (tile, surfel) pair capacity used by the next forward (>= 1024); after
  * stats.overflow the caller re-runs the view with a larger capacity */
 int s2d_view_reserve_pairs(s2d_view *view, int64_t pairs);
+/* Layout of the packed parameter and gradient blocks the view's s2d_forward / s2d_backward read
+ * and write: W = ceil(n / c) shards of c = shard_surfels surfels, shard s holding surfels
+ * [s c, (s + 1) c) as [means 3c | quats 4c | scales 2c | opacities c | colors 3c] (13 W c floats).
+ * 0 or c >= n is the plain layout of the header comment.  With the optimizer sharded over W
+ * ranks (c = ceil(n / W)) each rank's slice is contiguous: one reduce-scatter of the gradient
+ * block and one in-place all-gather of the parameters (replaces the sum at mapper.py:300-307). */
+int s2d_view_set_layout(s2d_view *view, int64_t shard_surfels);
 int s2d_view_inspect(s2d_view *view, s2d_view_debug *out);
 
 /* Number of kernels this library has launched in this process (all devices). */
@@ -205,6 +212,11 @@ int s2d_backward(s2d_view *view, void *stream, const float *params, int64_t n,
  */
 int s2d_adam_step(void *stream, float *params, const float *grads, float *m1, float *m2, int64_t n,
                   int64_t step, const s2d_adam_config *cfg, const uint8_t *mask);
+/* The same step, skipped on the device when *skip != 0 (device int32, nullable; e.g. the
+ * overflow word of an s2d_view_stats accumulated over the iteration's views): a refine
+ * iteration can be queued without a host round trip and re-run if a view overflowed. */
+int s2d_adam_step_gated(void *stream, float *params, const float *grads, float *m1, float *m2, int64_t n,
+                        int64_t step, const s2d_adam_config *cfg, const uint8_t *mask, const int32_t *skip);
 
 /*
  * mapper.refine's backtracking trial (mapper.py:319-335) on the packed block's opacity +

@@ -24,7 +24,7 @@ __all__ = [
     "build_oracle", "load", "pose_inverse", "project", "depth_order", "tile_lists",
     "render", "loss_seeds", "backward", "loss_and_grads", "max_blend_weights",
     "adam_step", "DEFAULTS", "quat_mul", "quat_canonicalize", "transform_surfels", "fuse_gate", "fuse",
-    "prune_mark", "prune",
+    "prune_mark", "prune", "refine",
 ]
 
 DEFAULTS = SimpleNamespace(weight_clamp=0.999, termination_transmittance=1e-4, footprint_sigma=3.0,
@@ -388,3 +388,73 @@ def prune(map_surfels, pose, intr, observed_rgb, observed_depth, rgb_error=0.2, 
         return np.zeros(0, np.int64), marked
     _, max_marked = max_blend_weights(map_surfels, pose, intr, marked, cfg)
     return np.flatnonzero(max_marked > contribution_floor), marked
+
+
+# ---------------------------------------------------------------- refine (mapper.py:276-349)
+
+def _psnr(rendered, target):
+    """evaluation.psnr (evaluation.py:63-72)."""
+    mse = float(np.mean((np.asarray(rendered, float) - np.asarray(target, float)) ** 2))
+    return float("inf") if mse == 0.0 else 10.0 * np.log10(1.0 / mse)
+
+
+def refine(surfels, keyframe_ids, target_mask, poses, observations, intr, iterations=20, initial_step=0.1,
+           min_step=1e-6, w_mse=1.0, w_depth=0.05, cfg=None):
+    """Float64 restatement of mapper.refine (mapper.py:276-349) on SurfelArrays-like inputs:
+    summed per-view render_loss and colour/opacity gradients (rasterizer.py:346-399 via this
+    oracle's render / loss_seeds / backward), target-masked L-inf-normalised backtracking steps
+    with halving, np.clip to [0, 1] of every surfel, warm-started step scale, restore on failure.
+    Returns (losses, psnr_before, psnr_after, accepted, colors, opacities); inputs untouched."""
+    colors = np.array(surfels.colors, dtype=float, copy=True)
+    opac = np.array(surfels.opacities, dtype=float, copy=True)
+    cur = SimpleNamespace(means=surfels.means, quats=surfels.quats, scales=surfels.scales, opacities=opac,
+                          colors=colors)
+    views = [(poses[k], *observations[k]) for k in keyframe_ids]
+    mask = np.asarray(target_mask, bool)
+
+    def psnrs():
+        vals = [_psnr(render(cur, p, intr, cfg, with_normal=False).color, rgb) for p, rgb, _ in views]
+        finite = [v for v in vals if np.isfinite(v)]
+        return float(np.mean(finite)) if finite else float("inf")
+
+    def loss_grads():
+        tot, gc, go = 0.0, np.zeros_like(cur.colors), np.zeros_like(cur.opacities)
+        for p, rgb, dep in views:
+            buf = render(cur, p, intr, cfg, with_normal=False)
+            loss, g_rgb, g_d = loss_seeds(buf, rgb, dep, "mse", w_mse, w_depth, True)
+            g = backward(cur, p, intr, buf, g_rgb, g_d, cfg=cfg)
+            tot += loss
+            gc += g.colors
+            go += g.opacities
+        return tot, gc, go
+
+    before = psnrs()
+    if iterations == 0 or not views or not mask.any():
+        return [], before, before, 0, cur.colors, cur.opacities
+    loss, gc, go = loss_grads()
+    losses, accepted, scale = [loss], 0, initial_step
+    for _ in range(iterations):
+        gc[~mask] = 0.0
+        go[~mask] = 0.0
+        gnorm = max(float(np.max(np.abs(gc))), float(np.max(np.abs(go))))
+        if gnorm < 1e-14:
+            break
+        step = scale / gnorm
+        c0, o0 = cur.colors.copy(), cur.opacities.copy()
+        improved = False
+        while step >= min_step / gnorm:
+            cur.colors = np.clip(c0 - step * gc, 0.0, 1.0)
+            cur.opacities = np.clip(o0 - step * go, 0.0, 1.0)
+            new_loss, ngc, ngo = loss_grads()
+            if new_loss < loss:
+                loss, gc, go = new_loss, ngc, ngo
+                losses.append(loss)
+                accepted += 1
+                improved = True
+                scale = min(2.0 * step * gnorm, initial_step)
+                break
+            step *= 0.5
+        if not improved:
+            cur.colors, cur.opacities = c0, o0
+            break
+    return losses, before, psnrs(), accepted, cur.colors, cur.opacities

@@ -208,7 +208,9 @@ int64_t o_project(int64_t n, const double *means, const double *quats, const dou
 
 /* ------------------------------------------------------------ depth order */
 
-static const double *g_sort_z;
+/* thread-local: the oracle is called from several host threads at once (view-parallel CPU
+ * baseline, summed multi-view gradients in the tests) */
+static _Thread_local const double *g_sort_z;
 static int cmp_z_idx(const void *a, const void *b) {
     const int64_t ia = *(const int64_t *)a, ib = *(const int64_t *)b;
     const double za = g_sort_z[ia], zb = g_sort_z[ib];

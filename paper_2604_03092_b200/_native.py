@@ -94,6 +94,7 @@ _SIGNATURES = {
     "s2d_view_stats_host": (ctypes.c_int, [c_p, ctypes.POINTER(ViewStats)]),
     "s2d_view_stats_accumulate": (ctypes.c_int, [c_p, c_p, c_p]),
     "s2d_view_reserve_pairs": (ctypes.c_int, [c_p, ctypes.c_int64]),
+    "s2d_view_set_layout": (ctypes.c_int, [c_p, ctypes.c_int64]),
     "s2d_view_inspect": (ctypes.c_int, [c_p, ctypes.POINTER(ViewDebug)]),
     "s2d_launch_count": (ctypes.c_int64, []),
     "s2d_view_set_timing": (ctypes.c_int, [c_p, ctypes.c_int32]),
@@ -106,6 +107,8 @@ _SIGNATURES = {
                                     ctypes.POINTER(Loss), c_p, c_p]),
     "s2d_adam_step": (ctypes.c_int, [c_p, c_p, c_p, c_p, c_p, ctypes.c_int64, ctypes.c_int64,
                                      ctypes.POINTER(AdamCfg), c_p]),
+    "s2d_adam_step_gated": (ctypes.c_int, [c_p, c_p, c_p, c_p, c_p, ctypes.c_int64, ctypes.c_int64,
+                                           ctypes.POINTER(AdamCfg), c_p, c_p]),
     "s2d_render_host": (ctypes.c_int, [c_p, c_p] + [c_p] * 5 + [ctypes.c_int64, ctypes.POINTER(ctypes.c_double),
                                                            ctypes.POINTER(Camera), ctypes.POINTER(RasterCfg)]
                         + [c_p] * 4 + [ctypes.POINTER(ctypes.c_int32)]),
@@ -132,7 +135,10 @@ def lib():
     except OSError as e:  # pragma: no cover - environment dependent
         _load_error = e
         raise NativeLibraryError(f"cannot load {LIB_PATH}: {e}") from e
+    old_ok = os.environ.get("S2D_ALLOW_OLD_LIB") == "1"  # A/B runs against an older build only
     for name, (res, args) in _SIGNATURES.items():
+        if old_ok and not hasattr(L, name):
+            continue
         f = getattr(L, name)
         f.restype = res
         f.argtypes = args

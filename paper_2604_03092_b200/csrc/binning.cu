@@ -1,14 +1,15 @@
 // binning.cu — projection, depth order and tile binning.
 //
 //   k_project     per-surfel float64 projection (bit-exact with rasterizer.py:201-281),
-//                 64-B splat record, bbox; compacts the (depth key, index) pairs of the drawn
-//                 surfels in index order (chained scan over ticketed tiles); min/max key.
-//   k_radix_hist  rebases the keys to 24 bits (key - min, shifted right only if the
-//                 depth range spans more than 2^24 key steps) and builds the digit
-//                 histograms of all 3 passes in one read.
+//                 64-B splat record, bbox; the drawn surfels' (depth key, index) pairs,
+//                 compacted within each tile; min/max key; per-tile and per-chunk counts.
+//   k_compact_hist concatenates the tiles' pairs in index order, rebases
+//                 the keys to 24 bits (key - min, shifted right only if the depth range
+//                 spans more than 2^24 key steps) and builds the digit histograms of all
+//                 3 passes in the same read.
 //   k_onesweep    one stable LSD radix pass (8-bit digits) with decoupled look-back; each
 //                 tile is regrouped by digit in shared memory, then written out as
-//                 contiguous per-digit runs (with n_host >= 0 it also drops sentinel keys).
+//                 contiguous per-digit runs.
 //   k_tie_fix     the depth key is the (rebased) upper 32 bits of the float64 z; runs of
 //                 equal keys whose z differ in the low bits are re-sorted by (z64, index),
 //                 giving exactly the reference order lexsort((index, z))
@@ -24,11 +25,12 @@
 #ifndef S2D_PROJ_MINB
 #define S2D_PROJ_MINB 3
 #endif
-#ifdef S2D_SORT_MINB
-#define S2D_SORT_BOUNDS __launch_bounds__(kSortThreads, S2D_SORT_MINB)
-#else
-#define S2D_SORT_BOUNDS __launch_bounds__(kSortThreads)
+// 3 CTAs of 256 threads per SM (<= 85 registers): without the bound the compiler takes 98
+// registers for k_onesweep and only 2 CTAs fit, which makes every radix pass ~30% slower
+#ifndef S2D_SORT_MINB
+#define S2D_SORT_MINB 3
 #endif
+#define S2D_SORT_BOUNDS __launch_bounds__(kSortThreads, S2D_SORT_MINB)
 #ifdef S2D_EMIT_MINB
 #define S2D_EMIT_BOUNDS __launch_bounds__(256, S2D_EMIT_MINB)
 #else
@@ -72,8 +74,8 @@ __device__ __forceinline__ uint32_t block_exclusive_scan_256(uint32_t v, uint32_
 // Such surfels have in_front = valid = on_screen = false exactly, so the float64 projection
 // (divisions, square roots) is skipped for them; everything near a gate boundary takes the
 // exact path.
-__device__ __forceinline__ bool clearly_out(const ViewParams &P, const ParamView &pv, int64_t i) {
-    const float mx = pv.means[3 * i], my = pv.means[3 * i + 1], mz = pv.means[3 * i + 2];
+__device__ __forceinline__ bool clearly_out(const ViewParams &P, const ParamPtrs &pv) {
+    const float mx = pv.means[0], my = pv.means[1], mz = pv.means[2];
     float p[3];
 #pragma unroll
     for (int r = 0; r < 3; ++r)
@@ -100,24 +102,18 @@ __device__ __forceinline__ bool clearly_out(const ViewParams &P, const ParamView
 
 template <bool kRay>
 __global__ void __launch_bounds__(kProjThreads, S2D_PROJ_MINB * 256 / kProjThreads) k_project(const ProjectArgs a) {
-    // tiles are taken in ticket order (the decoupled look-back of the compaction below needs
-    // every predecessor tile to be running or done)
-    __shared__ int s_tile;
     __shared__ uint32_t s_wcnt[kProjThreads / 32];
-    __shared__ uint32_t s_base;
-    if (threadIdx.x == 0) s_tile = atomicAdd(a.ticket, 1);
-    __syncthreads();
-    const int tile = s_tile;
+    const int tile = blockIdx.x;
     const int64_t i = (int64_t)tile * kProjThreads + threadIdx.x;
     const ViewParams &P = a.P;
     bool on = false, degen = false;
     uint32_t key = 0xffffffffu;
-    const ParamView pv(a.params, P.n);
-    if (i < P.n && clearly_out(P, pv, i)) {
+    const ParamPtrs pv = surfel_ptrs(a.params, P.n, P.shard, i < P.n ? i : 0);
+    if (i < P.n && clearly_out(P, pv)) {
         a.flags[i] = 0;
     } else if (i < P.n) {
         ExactProj e;
-        project_exact(P, pv, i, e);
+        project_exact(P, pv, e);
         degen = e.in_front && !e.valid;
         double Hi[9];
         int64_t bb[4] = {e.x0, e.x1, e.y0, e.y1};
@@ -136,9 +132,9 @@ __global__ void __launch_bounds__(kProjThreads, S2D_PROJ_MINB * 256 / kProjThrea
             if (kRay) {
                 // q0 = (Hi00, Hi01, Hi02, opacity), q1 = (Hi10, Hi11, Hi12, Hi20),
                 // q2 = (r, g, b, Hi21), q3 = (normal, Hi22)
-                r.q0 = make_float4((float)Hi[0], (float)Hi[1], (float)Hi[2], pv.opac[i]);
+                r.q0 = make_float4((float)Hi[0], (float)Hi[1], (float)Hi[2], pv.opac[0]);
                 r.q1 = make_float4((float)Hi[3], (float)Hi[4], (float)Hi[5], (float)Hi[6]);
-                r.q2 = make_float4(pv.colors[3 * i], pv.colors[3 * i + 1], pv.colors[3 * i + 2], (float)Hi[7]);
+                r.q2 = make_float4(pv.colors[0], pv.colors[1], pv.colors[2], (float)Hi[7]);
                 r.q3 = make_float4((float)(sg * nn[0]), (float)(sg * nn[1]), (float)(sg * nn[2]), (float)Hi[8]);
             } else {
                 // M = J Bc (2x2), Minv = M^-1; Sigma = M M^T equals the reference cov2.
@@ -150,13 +146,13 @@ __global__ void __launch_bounds__(kProjThreads, S2D_PROJ_MINB * 256 / kProjThrea
                 const double id = __drcp_rn(det);
                 const float cxh = (float)e.cx, cyh = (float)e.cy;
                 const __half2 lo = __floats2half2_rn((float)(e.cx - (double)cxh), (float)(e.cy - (double)cyh));
-                r.q0 = make_float4(cxh, cyh, __uint_as_float(*reinterpret_cast<const uint32_t *>(&lo)), pv.opac[i]);
+                r.q0 = make_float4(cxh, cyh, __uint_as_float(*reinterpret_cast<const uint32_t *>(&lo)), pv.opac[0]);
                 // Minv = (A B; C D) stored by columns: (A, C, B, D), clamped to the float32 range
                 // (a splat below ~1e-38 px would overflow to inf, and inf * 0 at its centre pixel
                 // would give NaN where the reference has m = 0; FLT_MAX * 0 = 0)
                 auto f32c = [](double x) { return (float)fmin(fmax(x, -3.4028234663852886e38), 3.4028234663852886e38); };
                 r.q1 = make_float4(f32c(M11 * id), f32c(-M10 * id), f32c(-M01 * id), f32c(M00 * id));
-                r.q2 = make_float4(pv.colors[3 * i], pv.colors[3 * i + 1], pv.colors[3 * i + 2], (float)e.p[2]);
+                r.q2 = make_float4(pv.colors[0], pv.colors[1], pv.colors[2], (float)e.p[2]);
                 // guard band of the float32 Mahalanobis distance (covers float32 rounding of Minv,
                 // of the pixel offset and of u, v, m)
                 // (float32 with 1% headroom: it is a bound, not a decision)
@@ -168,20 +164,25 @@ __global__ void __launch_bounds__(kProjThreads, S2D_PROJ_MINB * 256 / kProjThrea
                 if (!(gb <= 3.0e38f)) gb = __int_as_float(0x7f800000);
                 // the guard band is stored negated when the opacity is within 8e-6 of the weight
                 // clamp, so the raster kernels test both with one load
-                const bool nearclamp = pv.opac[i] > P.w_clamp_f - 8e-6f;
+                const bool nearclamp = pv.opac[0] > P.w_clamp_f - 8e-6f;
                 r.q3 = make_float4((float)(sg * nn[0]), (float)(sg * nn[1]), (float)(sg * nn[2]),
                                    nearclamp ? -gb : gb);
-                ExactRec &x = a.exact[i];
+                ExactRec x;
                 x.cx = e.cx;
                 x.cy = e.cy;
                 x.ia = e.ia;
                 x.ib = e.ib;
                 x.ic = e.ic;
-                if (!(gb <= kAccurateGb)) {  // accurate slot (s2d_device.cuh): float64 Minv
-                    x.ma = M11 * id;
-                    x.mb = -M01 * id;
-                    x.mc = -M10 * id;
-                    x.md = M00 * id;
+                a.exact[i] = x;
+                if (!(gb <= kAccurateGb)) {  // accurate slot (s2d_device.cuh): float64 centre, Minv
+                    AccurateRec ar;
+                    ar.cx = e.cx;
+                    ar.cy = e.cy;
+                    ar.ma = M11 * id;
+                    ar.mb = -M01 * id;
+                    ar.mc = -M10 * id;
+                    ar.md = M00 * id;
+                    a.acc[i] = ar;
                 }
             }
             a.rec[i] = r;
@@ -211,54 +212,88 @@ __global__ void __launch_bounds__(kProjThreads, S2D_PROJ_MINB * 256 / kProjThrea
         s_wcnt[warp] = __popc(wm);
     }
     __syncthreads();
-    // Order-preserving compaction of the drawn surfels' (depth key, index) pairs: a chained
-    // scan over the tiles (decoupled look-back), so the keys enter the stable radix passes in
-    // index order and runs of exactly equal z need no re-sorting (k_tie_fix).
-    if (warp == 0) {
-        uint32_t tot = 0;
-#pragma unroll
-        for (int w = 0; w < kProjThreads / 32; ++w) tot += s_wcnt[w];
-        const uint32_t pre = lookback_warp(a.status, tile, tot);
-        if (lane == 0) {
-            s_base = pre;
-            if (tile == (int)((P.n + kProjThreads - 1) / kProjThreads) - 1) *a.n_drawn = (int)(pre + tot);
-        }
-    }
-    __syncthreads();
+    // The drawn surfels' (depth key, index) pairs, compacted within the tile in index order into
+    // the tile's own segment [tile kProjThreads, + count); k_compact_hist concatenates the segments
+    // in tile order, so the keys enter the stable radix passes in index order and runs of exactly
+    // equal z need no re-sorting (k_tie_fix).  No inter-tile dependency here.
     if (drawn) {
-        uint32_t o = s_base + __popc(wm & lanemask_lt());
+        uint32_t o = (uint32_t)tile * kProjThreads + __popc(wm & lanemask_lt());
         for (int w = 0; w < warp; ++w) o += s_wcnt[w];
         a.keys[o] = key;
         a.vals[o] = (uint32_t)i;
+    }
+    if (threadIdx.x == 0) {
+        uint32_t tot = 0;
+#pragma unroll
+        for (int w = 0; w < kProjThreads / 32; ++w) tot += s_wcnt[w];
+        a.tcount[tile] = tot;
+        // per chunk of kCompactTiles tiles: k_compact_hist derives every chunk's offset from
+        // these totals (a few coalesced loads per CTA, no chained scan), and the drawn total
+        if (tot) {
+            atomicAdd(a.ccount + tile / kCompactTiles, tot);
+            atomicAdd(a.n_drawn, (int)tot);
+        }
     }
 }
 
 // --------------------------------------------------------------- radix sorting
 
-// Depth keys: rebase to [0, 2^24) (shift only if the key range needs more bits; ties are
-// resolved by k_tie_fix) and histogram the three 8-bit digits.  Sentinels stay sentinels.
-__global__ void __launch_bounds__(256) k_radix_hist(uint32_t *__restrict__ keys, const int *__restrict__ d_n,
-                                                    const uint32_t *__restrict__ key_range,
-                                                    uint32_t *__restrict__ hist) {
-    const int n = *d_n;
+// Order-preserving compaction + depth-key rebase + digit histograms: CTA c copies the pairs of
+// projection tiles [32 c, 32 c + 32) from their segments (k_project) to their place in tile
+// order (= index order): the chunk's offset is the sum of the earlier chunks' totals (one
+// coalesced warp pass over them), the tiles' offsets within the chunk a warp scan.  Each key is
+// rebased to [0, 2^24) (key - min, shifted right only if the depth range spans more than 2^24
+// key steps; ties are resolved by k_tie_fix) and its three 8-bit digits histogrammed.
+__global__ void __launch_bounds__(256) k_compact_hist(const uint32_t *__restrict__ skeys,
+                                                      const uint32_t *__restrict__ svals,
+                                                      const uint32_t *__restrict__ tcount,
+                                                      const uint32_t *__restrict__ ccount, int ntp,
+                                                      const uint32_t *__restrict__ key_range, uint32_t *keys,
+                                                      uint32_t *vals, uint32_t *hist) {
     __shared__ uint32_t sh[3 * kRadix];
-    for (int k = threadIdx.x; k < 3 * kRadix; k += blockDim.x) sh[k] = 0;
+    __shared__ uint32_t s_cnt[kCompactTiles], s_off[kCompactTiles];
+    const int tid = threadIdx.x, c = blockIdx.x;
+    for (int k = tid; k < 3 * kRadix; k += blockDim.x) sh[k] = 0;
+    if (tid < 32) {
+        uint32_t base = 0;
+        for (int j = tid; j < c; j += 32) base += ccount[j];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) base += __shfl_xor_sync(0xffffffffu, base, o);
+        const int t = kCompactTiles * c + tid;
+        const uint32_t cnt = t < ntp ? tcount[t] : 0u;
+        uint32_t x = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (tid >= o) x += y;
+        }
+        s_cnt[tid] = cnt;
+        s_off[tid] = base + x - cnt;
+    }
     __syncthreads();
     const uint32_t kmin = ~key_range[0], kmax = key_range[1];
     const uint32_t span = kmax >= kmin ? kmax - kmin : 0u;
     const int shift = span >= (1u << 24) ? (32 - __clz(span)) - 24 : 0;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        uint32_t k = keys[i];
-        if (k == 0xffffffffu) continue;
-        k = (k - kmin) >> shift;
-        keys[i] = k;
+    for (int s = tid; s < kCompactTiles * kProjThreads; s += blockDim.x) {
+        const int t = s / kProjThreads, j = s % kProjThreads;
+        if ((uint32_t)j >= s_cnt[t]) continue;
+        const size_t src = (size_t)(kCompactTiles * c + t) * kProjThreads + j;
+        const uint32_t k = (skeys[src] - kmin) >> shift;
+        const uint32_t o = s_off[t] + j;
+        keys[o] = k;
+        vals[o] = svals[src];
 #pragma unroll
         for (int p = 0; p < 3; ++p) atomicAdd(&sh[p * kRadix + ((k >> (kRadixBits * p)) & (kRadix - 1))], 1u);
     }
     __syncthreads();
-    for (int k = threadIdx.x; k < 3 * kRadix; k += blockDim.x)
+    for (int k = tid; k < 3 * kRadix; k += blockDim.x)
         if (sh[k]) atomicAdd(&hist[k], sh[k]);
 }
+
+// static shared memory of k_onesweep: the regrouped tile (2 kSortTile words) + per-warp digit
+// counts and scans (~10.3 KB); S2D_SORT_ITEMS (keys per thread) is bounded by the 48 KB static limit
+static_assert(2 * kSortTile * 4 + (8 * kRadix + 2 * kRadix + 16 + 1) * 4 <= 48 * 1024,
+              "k_onesweep: S2D_SORT_ITEMS too large for 48 KB of static shared memory");
 
 __global__ void S2D_SORT_BOUNDS k_onesweep(
     const uint32_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint32_t *__restrict__ kout,
@@ -275,7 +310,11 @@ __global__ void S2D_SORT_BOUNDS k_onesweep(
     for (int w = 0; w < 8; ++w) s_wh[w][tid] = 0;
     __syncthreads();
     const int tile = s_tile;
-    const bool drop = n_host >= 0;  // first pass over all surfels: sentinel keys are dropped
+    // n_host >= 0: a pass over n_host entries that skips sentinel keys (0xffffffff); every call
+    // passes -1 (the *d_n entries).  The branch is kept on purpose: with it ptxas allocates 80
+    // registers and no spills at 3 CTAs/SM; without it, 98 registers (2 CTAs/SM) or 16 B of
+    // spills under the same bound, and every radix pass was 20-25% slower.
+    const bool drop = n_host >= 0;
     const int n = drop ? n_host : *d_n;
     const int start = tile * kSortTile;
     if (start >= n) return;
@@ -342,16 +381,16 @@ __global__ void S2D_SORT_BOUNDS k_onesweep(
 
 // Runs of equal (rebased upper-32-bit) depth keys: restore (z64, index) order.
 //
-// The compaction in k_project is order-preserving and the radix passes are stable, so a run of
-// equal keys arrives in index order: runs of exactly equal z (a fronto-parallel plane, quantised
-// depth) are already in the reference order and cost one comparison per position.  Only keys
-// whose float64 z differ below the key resolution can be inverted.
-//   - A run of <= kTieShort entries is checked, and if needed insertion-sorted, by the thread
-//     at its head (bounded work per thread).
-//   - A longer run is appended to a list by its head; any inversion inside a long run (seen
-//     by the head within its first kTieShort entries, or by the inverted entry itself, which
-//     then cannot find its head within kTieShort) sets a flag, and k_tie_long sorts the listed
-//     runs cooperatively (one CTA per run).  With the flag clear k_tie_long exits at once.
+// The compaction is order-preserving and the radix passes are stable, so a run of equal keys
+// arrives in index order: runs of exactly equal z (a fronto-parallel plane, quantised depth) are
+// already in the reference order and cost one comparison per position.  Only keys whose float64
+// z differ below the key resolution can be inverted.  Per position:
+//   - the head of a run of <= kTieShort entries checks it and, if needed, insertion-sorts it
+//     (bounded work, one thread per run, so no claims are needed);
+//   - the head of a longer run lists it and checks its first kTieShort entries; an inversion
+//     further in is seen by the inverted entry itself (its predecessor kTieShort back shares
+//     the key); either sets a flag, and the last CTA of k_tie_fix then sorts the listed runs
+//     cooperatively (tie_long).
 constexpr int kTieShort = 64;
 
 __device__ __forceinline__ bool zi_less(const double *z64, uint32_t a, uint32_t b) {
@@ -359,40 +398,34 @@ __device__ __forceinline__ bool zi_less(const double *z64, uint32_t a, uint32_t 
     return za < zb || (za == zb && a < b);
 }
 
-__global__ void __launch_bounds__(256) k_tie_fix(const uint32_t *__restrict__ keys, uint32_t *vals,
-                                                 const double *__restrict__ z64, const int *__restrict__ d_n,
-                                                 uint32_t *ctl, uint32_t *list) {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    const int n = *d_n;
+__device__ __forceinline__ void tie_fix_at(const uint32_t *__restrict__ keys, uint32_t *vals,
+                                           const double *__restrict__ z64, int n, uint32_t *ctl, uint32_t *list,
+                                           int r) {
     if (r >= n) return;
     const uint32_t k = keys[r];
-    const bool head = r == 0 || keys[r - 1] != k;
-    if (!head) {
-        // an inverted pair whose run head lies more than kTieShort back: a long run (the head
-        // only inspects its first kTieShort entries)
-        if (r >= kTieShort && !zi_less(z64, vals[r - 1], vals[r])) {
-            const int lim = r - kTieShort;
-            int s = r - 1;
-            while (s > lim && keys[s - 1] == k) --s;
-            if (s == lim) atomicExch(ctl + 1, 1u);  // head at or before r - kTieShort
-        }
+    if (r > 0 && keys[r - 1] == k) {
+        // not a head: an inversion kTieShort or more entries into a run belongs to a long run
+        // (positions r - kTieShort .. r share the key); nearer ones are the head's to check
+        if (r >= kTieShort && keys[r - kTieShort] == k && !zi_less(z64, vals[r - 1], vals[r]))
+            atomicExch(ctl + 1, 1u);
         return;
     }
-    if (r + 1 >= n || keys[r + 1] != k) return;  // run of one
+    if (r + 1 >= n || keys[r + 1] != k) return;  // run of one (the common case)
+    // run head: check the first kTieShort entries; a longer run is listed for tie_long
+    const bool longrun = r + kTieShort < n && keys[r + kTieShort] == k;
     int e = r + 1;
     bool sorted = true;
     while (e < n && e - r < kTieShort && keys[e] == k) {
         sorted = sorted && zi_less(z64, vals[e - 1], vals[e]);
         ++e;
     }
-    if (e < n && keys[e] == k) {  // longer than kTieShort: k_tie_long
-        const uint32_t slot = atomicAdd(ctl, 1u);
-        list[slot] = (uint32_t)r;
+    if (longrun) {
+        list[atomicAdd(ctl, 1u)] = (uint32_t)r;
         if (!sorted) atomicExch(ctl + 1, 1u);
         return;
     }
     if (sorted) return;
-    for (int j = r + 1; j < e; ++j) {  // insertion sort of <= kTieShort entries
+    for (int j = r + 1; j < e; ++j) {  // insertion sort of <= kTieShort entries, by the head only
         const uint32_t v = vals[j];
         const double zv = z64[v];
         int t = j - 1;
@@ -410,10 +443,10 @@ __global__ void __launch_bounds__(256) k_tie_fix(const uint32_t *__restrict__ ke
     }
 }
 
-// Cooperative sort of the long runs (only when one of them holds an inversion).  One CTA per
-// run: the run's end is found 256 entries at a time; chunks of kTieChunk entries are bitonic-
+// Cooperative sort of the long runs (only when one of them holds an inversion), by one CTA:
+// each run's end is found 256 entries at a time; chunks of kTieChunk entries are bitonic-
 // sorted in shared memory, then merged pairwise (merge path, 256 threads) through `scratch`.
-constexpr int kTieChunk = 2048;
+constexpr int kTieChunk = 512;
 
 __device__ void tie_bitonic_chunk(uint32_t *v, int len, const double *z64, double *sz, uint32_t *si) {
     const int tid = threadIdx.x;
@@ -444,16 +477,14 @@ __device__ void tie_bitonic_chunk(uint32_t *v, int len, const double *z64, doubl
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(256) k_tie_long(const uint32_t *__restrict__ keys, uint32_t *vals,
-                                                  const double *__restrict__ z64, const int *__restrict__ d_n,
-                                                  const uint32_t *ctl, const uint32_t *list, uint32_t *scratch) {
-    if (ctl[1] == 0u) return;  // no inversion in any long run
+__device__ void tie_long(const uint32_t *__restrict__ keys, uint32_t *vals, const double *__restrict__ z64, int n,
+                         const uint32_t *ctl, const uint32_t *list, uint32_t *scratch) {
     __shared__ double sz[kTieChunk];
     __shared__ uint32_t si[kTieChunk];
     __shared__ int s_end;
-    const int n = *d_n, tid = threadIdx.x;
+    const int tid = threadIdx.x;
     const int nruns = (int)ctl[0];
-    for (int q = blockIdx.x; q < nruns; q += gridDim.x) {
+    for (int q = 0; q < nruns; ++q) {
         const int r0 = (int)list[q];
         const uint32_t k = keys[r0];
         if (tid == 0) s_end = n;
@@ -499,6 +530,22 @@ __global__ void __launch_bounds__(256) k_tie_long(const uint32_t *__restrict__ k
             for (int j = tid; j < len; j += blockDim.x) vals[r0 + j] = src[j];
         __syncthreads();
     }
+}
+
+// One thread per position (tie_fix_at); the last CTA to finish (ticket) sorts the long runs when
+// one of them holds an inversion (tie_long), so no second launch is needed.
+__global__ void __launch_bounds__(256) k_tie_fix(const uint32_t *__restrict__ keys, uint32_t *vals,
+                                                 const double *__restrict__ z64, const int *__restrict__ d_n,
+                                                 uint32_t *ctl, uint32_t *list, uint32_t *scratch) {
+    __shared__ bool s_last;
+    const int n = *d_n;
+    tie_fix_at(keys, vals, z64, n, ctl, list, blockIdx.x * blockDim.x + threadIdx.x);
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomic_add_acq_rel(ctl + 2, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    if (*reinterpret_cast<volatile uint32_t *>(ctl + 1) == 0u) return;  // no inversion in any long run
+    tie_long(keys, vals, z64, n, ctl, list, scratch);
 }
 
 // ----------------------------------------------------------- scan + emission
@@ -564,10 +611,13 @@ __global__ void S2D_EMIT_BOUNDS k_scan_emit(const EmitArgs a) {
                     // mask into bits 24-31 (raster.cu)
                     a.pkeys[off] = t | ((rows & cols) << 16);
                     a.pvals[off] = ids[j];
+                    // the tile-id passes sort the stored pairs only (pairs_stored entries): their
+                    // digit histograms must count exactly those, or an overflowing view's passes
+                    // would place entries past the capacity
+                    atomicAdd(&s_hist[t & (kRadix - 1)], 1u);
+                    if (a.pair_passes > 1) atomicAdd(&s_hist[kRadix + ((t >> kRadixBits) & (kRadix - 1))], 1u);
                 }
                 ++off;
-                atomicAdd(&s_hist[t & (kRadix - 1)], 1u);
-                if (a.pair_passes > 1) atomicAdd(&s_hist[kRadix + ((t >> kRadixBits) & (kRadix - 1))], 1u);
             }
         }
     }
@@ -599,22 +649,24 @@ void launch_project(const ProjectArgs &a, cudaStream_t s) {
     }
 }
 
-void launch_radix_hist(uint32_t *keys, const int *d_n, int n, const uint32_t *key_range, uint32_t *hist,
-                       cudaStream_t s) {
-    int blocks = (n + 255) / 256;
-    if (blocks > 592) blocks = 592;
-    if (blocks < 1) blocks = 1;
-    count_launch();
-    k_radix_hist<<<blocks, 256, 0, s>>>(keys, d_n, key_range, hist);
+void launch_compact_hist(const uint32_t *skeys, const uint32_t *svals, const uint32_t *tcount,
+                         const uint32_t *ccount, int64_t n, const uint32_t *key_range, uint32_t *keys,
+                         uint32_t *vals, uint32_t *hist, cudaStream_t s) {
+    const int ntp = (int)((n + kProjThreads - 1) / kProjThreads);
+    const int blocks = (ntp + kCompactTiles - 1) / kCompactTiles;
+    if (blocks > 0) {
+        count_launch();
+        k_compact_hist<<<blocks, 256, 0, s>>>(skeys, svals, tcount, ccount, ntp, key_range, keys, vals, hist);
+    }
 }
 
 void launch_onesweep(const uint32_t *kin, const uint32_t *vin, uint32_t *kout, uint32_t *vout,
-                     const int *d_n, int cap, int n_host, int shift, const uint32_t *hist_pass,
+                     const int *d_n, int cap, int shift, const uint32_t *hist_pass,
                      uint32_t *status, int *ticket, cudaStream_t s) {
     const int blocks = (cap + kSortTile - 1) / kSortTile;
     if (blocks > 0) {
         count_launch();
-        k_onesweep<<<blocks, kSortThreads, 0, s>>>(kin, vin, kout, vout, d_n, n_host, shift, hist_pass, status,
+        k_onesweep<<<blocks, kSortThreads, 0, s>>>(kin, vin, kout, vout, d_n, -1, shift, hist_pass, status,
                                                    ticket);
     }
 }
@@ -624,9 +676,7 @@ void launch_tie_fix(const uint32_t *keys, uint32_t *vals, const double *z64, con
     const int blocks = (cap + 255) / 256;
     if (blocks > 0) {
         count_launch();
-        k_tie_fix<<<blocks, 256, 0, s>>>(keys, vals, z64, d_n, ctl, list);
-        count_launch();
-        k_tie_long<<<64, 256, 0, s>>>(keys, vals, z64, d_n, ctl, list, scratch);
+        k_tie_fix<<<blocks, 256, 0, s>>>(keys, vals, z64, d_n, ctl, list, scratch);
     }
 }
 

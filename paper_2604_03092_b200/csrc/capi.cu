@@ -1,7 +1,7 @@
 // capi.cu — extern "C" boundary (include/surfel2d.h): per-view workspace arena,
 // host-side float64 pose math, and the launch sequence of one view:
 //
-//   memset(sync region) -> k_project -> k_radix_hist -> 3 x k_onesweep (depth)
+//   memset(sync region) -> k_project -> k_compact_hist -> 3 x k_onesweep (depth)
 //   -> k_tie_fix -> k_scan_emit -> 1..2 x k_onesweep (tile id) -> k_tile_ranges
 //   -> k_raster_fwd                       [s2d_forward]
 //   -> k_raster_bwd -> k_project_bwd      [s2d_backward]
@@ -128,6 +128,7 @@ void make_view_params(const double pose[8], const s2d_camera &cam, const s2d_ras
     P.ntx = (cam.width + kTile - 1) / kTile;
     P.nty = (cam.height + kTile - 1) / kTile;
     P.n = n;
+    P.shard = n;
     P.mode = cfg.splat_mode;
 }
 
@@ -185,13 +186,15 @@ struct s2d_view {
     // capacities (elements)
     int64_t cap_rec = 0, cap_rect = 0, cap_z = 0, cap_flags = 0, cap_keys[2] = {0, 0},
             cap_vals[2] = {0, 0}, cap_grad = 0, cap_aux = 0, cap_pk[2] = {0, 0}, cap_pv[2] = {0, 0},
-            cap_bs = 0, cap_bc = 0, cap_ex = 0, cap_sync = 0, cap_amb = 0;
+            cap_bs = 0, cap_bc = 0, cap_ex = 0, cap_sync = 0, cap_amb = 0, cap_tc = 0, cap_to = 0, cap_acc = 0;
     SplatRecord *rec = nullptr;
     ExactRec *exact = nullptr;  // float64 centre + inv_abc per on-screen surfel (guard-band path)
+    AccurateRec *acc = nullptr;  // float64 centre + Minv per accurate (ill-conditioned) surfel
     short4 *rect = nullptr;
     double *z64 = nullptr;
     uint8_t *flags = nullptr;
     uint32_t *keys[2] = {nullptr, nullptr}, *vals[2] = {nullptr, nullptr};
+    uint32_t *tcount = nullptr;  // drawn surfels per projection tile
     uint32_t *pkeys[2] = {nullptr, nullptr}, *pvals[2] = {nullptr, nullptr};
     uint4 *bstream = nullptr;  // [16 pcap] per-(warp, column half) (surfel, blend mask, clamp mask) streams
     int *bcount = nullptr;     // [ntiles * 16] stream lengths
@@ -201,6 +204,7 @@ struct s2d_view {
     uint8_t *sync = nullptr;
     SyncRegion sr{};
     int64_t pcap = 0;  // pair capacity in use
+    int64_t shard = 0;  // surfels per shard of the packed parameter/gradient blocks (0: plain layout)
     // state of the last forward
     bool has_fwd = false;
     ViewParams P{};
@@ -252,7 +256,6 @@ int layout_sync(s2d_view *v, int64_t n, int64_t pcap, int ntiles) {
     const size_t o_tickets = take(16 * sizeof(int));
     const size_t o_drawn = take(sizeof(int));
     const size_t o_krange = take(2 * 4);
-    const size_t o_pstat0 = take((size_t)((n + kProjThreads - 1) / kProjThreads + 1) * 4);
     const size_t o_dhist = take(3 * kRadix * 4);
     const size_t o_dstat = take((size_t)3 * sort_tiles * kRadix * 4);
     const size_t o_emit = take((size_t)emit_tiles * 4);
@@ -260,6 +263,7 @@ int layout_sync(s2d_view *v, int64_t n, int64_t pcap, int ntiles) {
     const size_t o_pstat = take((size_t)2 * psort_tiles * kRadix * 4);
     const size_t o_tie = take(4 * 4);
     const size_t o_amb = take(4);
+    const size_t o_cc = take((size_t)((n + kProjThreads - 1) / kProjThreads / kCompactTiles + 1) * 4);
     const size_t o_ranges = take((size_t)ntiles * sizeof(int2));
     int64_t need = (int64_t)off;
     int rc = grow(v->sync, v->cap_sync, need);
@@ -269,7 +273,6 @@ int layout_sync(s2d_view *v, int64_t n, int64_t pcap, int ntiles) {
     v->sr.tickets = reinterpret_cast<int *>(b + o_tickets);
     v->sr.n_drawn = reinterpret_cast<int *>(b + o_drawn);
     v->sr.key_range = reinterpret_cast<uint32_t *>(b + o_krange);
-    v->sr.proj_status = reinterpret_cast<uint32_t *>(b + o_pstat0);
     v->sr.depth_hist = reinterpret_cast<uint32_t *>(b + o_dhist);
     v->sr.depth_status = reinterpret_cast<uint32_t *>(b + o_dstat);
     v->sr.emit_status = reinterpret_cast<uint32_t *>(b + o_emit);
@@ -277,6 +280,7 @@ int layout_sync(s2d_view *v, int64_t n, int64_t pcap, int ntiles) {
     v->sr.pair_status = reinterpret_cast<uint32_t *>(b + o_pstat);
     v->sr.tie_ctl = reinterpret_cast<uint32_t *>(b + o_tie);
     v->sr.amb_count = reinterpret_cast<int *>(b + o_amb);
+    v->sr.ccount = reinterpret_cast<uint32_t *>(b + o_cc);
     v->sr.ranges = reinterpret_cast<int2 *>(b + o_ranges);
     v->sr.bytes = off;
     return S2D_OK;
@@ -287,6 +291,7 @@ int ensure_capacity(s2d_view *v, int64_t n, int64_t npx, int ntiles) {
     const int64_t nn = n < 1 ? 1 : n;
     if ((rc = grow(v->rec, v->cap_rec, nn))) return rc;
     if ((rc = grow(v->exact, v->cap_ex, nn))) return rc;
+    if ((rc = grow(v->acc, v->cap_acc, nn))) return rc;
     if ((rc = grow(v->rect, v->cap_rect, nn))) return rc;
     if ((rc = grow(v->z64, v->cap_z, nn))) return rc;
     if ((rc = grow(v->flags, v->cap_flags, nn))) return rc;
@@ -294,6 +299,7 @@ int ensure_capacity(s2d_view *v, int64_t n, int64_t npx, int ntiles) {
         if ((rc = grow(v->keys[b], v->cap_keys[b], nn))) return rc;
         if ((rc = grow(v->vals[b], v->cap_vals[b], nn))) return rc;
     }
+    if ((rc = grow(v->tcount, v->cap_tc, (nn + kProjThreads - 1) / kProjThreads))) return rc;
     if ((rc = grow(v->grad2d, v->cap_grad, nn * 16, /*zero=*/true))) return rc;
     if ((rc = grow(v->aux, v->cap_aux, npx))) return rc;
     if ((rc = grow(v->amb, v->cap_amb, npx))) return rc;
@@ -323,6 +329,7 @@ int view_forward(s2d_view *v, cudaStream_t s, const float *params, int64_t n, co
     const int64_t npx = (int64_t)cam->width * cam->height;
     ViewParams P;
     make_view_params(pose, *cam, *cfg, n, P);
+    if (v->shard > 0 && v->shard < n) P.shard = v->shard;
     const int ntiles = P.ntx * P.nty;
     if ((rc = ensure_capacity(v, n, npx, ntiles))) return rc;
     v->has_fwd = false;
@@ -346,26 +353,30 @@ int view_forward(s2d_view *v, cudaStream_t s, const float *params, int64_t n, co
         pa.params = params;
         pa.rec = v->rec;
         pa.exact = v->exact;
+        pa.acc = v->acc;
         pa.rect = v->rect;
         pa.z64 = v->z64;
         pa.flags = v->flags;
-        pa.keys = v->keys[0];
-        pa.vals = v->vals[0];
         pa.stats = sr.stats;
         pa.key_range = sr.key_range;
+        // k_project leaves each tile's drawn pairs in its own segment of keys[1] / vals[1];
+        // k_compact_hist concatenates them in index order into keys[0] / vals[0]
+        pa.keys = v->keys[1];
+        pa.vals = v->vals[1];
+        pa.tcount = v->tcount;
+        pa.ccount = sr.ccount;
         pa.n_drawn = sr.n_drawn;
-        pa.ticket = sr.tickets + 0;
-        pa.status = sr.proj_status;
         launch_project(pa, s);
         mark();
-        // depth order: the drawn surfels' keys (appended by k_project), rebased to 24 bits, 3
-        // stable 8-bit passes, then k_tie_fix orders equal keys by (z64, index)
-        launch_radix_hist(v->keys[0], d_v, (int)n, sr.key_range, sr.depth_hist, s);
+        // depth order: the drawn surfels' keys rebased to 24 bits, 3 stable 8-bit passes, then
+        // k_tie_fix orders equal keys by (z64, index)
+        launch_compact_hist(v->keys[1], v->vals[1], v->tcount, sr.ccount, n, sr.key_range, v->keys[0], v->vals[0],
+                            sr.depth_hist, s);
         const int64_t sort_tiles = (n + kSortTile - 1) / kSortTile + 1;
         int cur = 0;
         for (int p = 0; p < 3; ++p) {
             launch_onesweep(v->keys[cur], v->vals[cur], v->keys[cur ^ 1], v->vals[cur ^ 1], d_v, (int)n,
-                            -1, kRadixBits * p, sr.depth_hist + p * kRadix,
+                            kRadixBits * p, sr.depth_hist + p * kRadix,
                             sr.depth_status + (size_t)p * sort_tiles * kRadix, sr.tickets + 1 + p, s);
             cur ^= 1;
         }
@@ -396,7 +407,7 @@ int view_forward(s2d_view *v, cudaStream_t s, const float *params, int64_t n, co
         int pc = 0;
         for (int p = 0; p < ppass; ++p) {
             launch_onesweep(v->pkeys[pc], v->pvals[pc], v->pkeys[pc ^ 1], v->pvals[pc ^ 1],
-                            &sr.stats->pairs_stored, (int)v->pcap, -1, kRadixBits * p, sr.pair_hist + p * kRadix,
+                            &sr.stats->pairs_stored, (int)v->pcap, kRadixBits * p, sr.pair_hist + p * kRadix,
                             sr.pair_status + (size_t)p * psort_tiles * kRadix, sr.tickets + 6 + p, s);
             pc ^= 1;
         }
@@ -419,6 +430,7 @@ int view_forward(s2d_view *v, cudaStream_t s, const float *params, int64_t n, co
     ra.bcount = v->bcount;
     ra.rec = v->rec;
     ra.exact = v->exact;
+    ra.acc = v->acc;
     ra.rect = v->rect;
     ra.aux = v->aux;
     ra.color = out->color;
@@ -479,8 +491,8 @@ int s2d_view_create(s2d_ctx *ctx, s2d_view **out) {
 
 int s2d_view_destroy(s2d_view *v) {
     if (!v) return S2D_OK;
-    void *ptrs[] = {v->rec, v->exact, v->rect, v->z64, v->flags, v->keys[0], v->keys[1], v->vals[0], v->vals[1],
-                    v->pkeys[0], v->pkeys[1], v->pvals[0], v->pvals[1], v->bstream, v->bcount, v->grad2d, v->aux, v->amb, v->sync,
+    void *ptrs[] = {v->rec, v->exact, v->acc, v->rect, v->z64, v->flags, v->keys[0], v->keys[1], v->vals[0], v->vals[1],
+                    v->pkeys[0], v->pkeys[1], v->pvals[0], v->pvals[1], v->bstream, v->bcount, v->grad2d, v->aux, v->amb, v->tcount, v->sync,
                     v->h_params_dev, v->h_img_dev};
     for (void *p : ptrs)
         if (p) cudaFree(p);
@@ -523,6 +535,13 @@ int s2d_view_reserve_pairs(s2d_view *v, int64_t pairs) {
     if (!v) return fail(S2D_ERR_INVALID, "NULL view");
     if (pairs > ((int64_t)1 << 30)) return fail(S2D_ERR_INVALID, "pair capacity too large");
     v->pcap = pairs < 1024 ? 1024 : pairs;
+    return S2D_OK;
+}
+
+int s2d_view_set_layout(s2d_view *v, int64_t shard_surfels) {
+    if (!v) return fail(S2D_ERR_INVALID, "NULL view");
+    if (shard_surfels < 0 || shard_surfels >= ((int64_t)1 << 30)) return fail(S2D_ERR_INVALID, "bad shard size");
+    v->shard = shard_surfels;
     return S2D_OK;
 }
 
@@ -609,6 +628,7 @@ int s2d_backward(s2d_view *v, void *stream, const float *params, int64_t n, cons
     ra.bcount = v->bcount;
     ra.rec = v->rec;
     ra.exact = v->exact;
+    ra.acc = v->acc;
     ra.rect = v->rect;
     ra.aux = v->aux;
     ra.color = image->color;
@@ -655,12 +675,17 @@ int s2d_backward(s2d_view *v, void *stream, const float *params, int64_t n, cons
 
 int s2d_adam_step(void *stream, float *params, const float *grads, float *m1, float *m2, int64_t n,
                   int64_t step, const s2d_adam_config *cfg, const uint8_t *mask) {
+    return s2d_adam_step_gated(stream, params, grads, m1, m2, n, step, cfg, mask, nullptr);
+}
+
+int s2d_adam_step_gated(void *stream, float *params, const float *grads, float *m1, float *m2, int64_t n,
+                        int64_t step, const s2d_adam_config *cfg, const uint8_t *mask, const int32_t *skip) {
     if (!cfg) return fail(S2D_ERR_INVALID, "adam config is NULL");
     if (step < 1) return fail(S2D_ERR_INVALID, "adam step is 1-based");
     if (n < 0) return fail(S2D_ERR_INVALID, "negative n");
     if (n == 0) return S2D_OK;
     if (!params || !grads || !m1 || !m2) return fail(S2D_ERR_INVALID, "NULL buffer");
-    launch_adam(params, grads, m1, m2, n, step, *cfg, mask, (cudaStream_t)stream);
+    launch_adam(params, grads, m1, m2, n, step, *cfg, mask, skip, (cudaStream_t)stream);
     S2D_CHECK_LAUNCH();
     return S2D_OK;
 }

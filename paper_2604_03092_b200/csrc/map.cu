@@ -40,30 +40,30 @@ __global__ void __launch_bounds__(256) k_transform(const float *__restrict__ in,
                                                    const double4 pa, const double4 pq) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const ParamView pv(in, n);
+    const ParamPtrs pv = surfel_ptrs(in, n, n, i);
     const double s = pa.x;
     const double q[4] = {pq.x, pq.y, pq.z, pq.w};
     const double t[3] = {pa.y, pa.z, pa.w};
     // means: pk_act = s * quat_rotate(q, p) + t
-    const double mu[3] = {(double)pv.means[3 * i], (double)pv.means[3 * i + 1], (double)pv.means[3 * i + 2]};
+    const double mu[3] = {(double)pv.means[0], (double)pv.means[1], (double)pv.means[2]};
     double r[3];
     quat_rotate_exact(q, mu, r);
     float *om = out, *oq = out + 3 * n, *os = out + 7 * n, *oo = out + 9 * n, *oc = out + 10 * n;
 #pragma unroll
     for (int k = 0; k < 3; ++k) om[3 * i + k] = __double2float_rn(dadd(dmul(s, r[k]), t[k]));
     // rotations: canonicalize(quat_mul(q, q_i))
-    const double qi[4] = {(double)pv.quats[4 * i], (double)pv.quats[4 * i + 1], (double)pv.quats[4 * i + 2],
-                          (double)pv.quats[4 * i + 3]};
+    const double qi[4] = {(double)pv.quats[0], (double)pv.quats[1], (double)pv.quats[2],
+                          (double)pv.quats[3]};
     double qo[4];
     quat_mul_exact(q, qi, qo);
     quat_canonicalize_exact(qo);
 #pragma unroll
     for (int k = 0; k < 4; ++k) oq[4 * i + k] = __double2float_rn(qo[k]);
-    os[2 * i] = __double2float_rn(dmul(s, (double)pv.scales[2 * i]));
-    os[2 * i + 1] = __double2float_rn(dmul(s, (double)pv.scales[2 * i + 1]));
-    oo[i] = pv.opac[i];
+    os[2 * i] = __double2float_rn(dmul(s, (double)pv.scales[0]));
+    os[2 * i + 1] = __double2float_rn(dmul(s, (double)pv.scales[1]));
+    oo[i] = pv.opac[0];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) oc[3 * i + k] = pv.colors[3 * i + k];
+    for (int k = 0; k < 3; ++k) oc[3 * i + k] = pv.colors[k];
 }
 
 __global__ void __launch_bounds__(256) k_fuse_gate(const float *__restrict__ acc, const float *__restrict__ params,

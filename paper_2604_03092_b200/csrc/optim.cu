@@ -58,20 +58,17 @@ __global__ void S2D_PBWD_BOUNDS k_project_bwd(const ProjectBwdArgs a) {
     const int64_t n = P.n;
     const float4 *__restrict__ g4 = reinterpret_cast<const float4 *>(a.grad2d + (size_t)i * 16);
     const float4 G0 = g4[0], G1 = g4[1], G2 = g4[2], G3 = g4[3];
-    float *gmeans = a.grads, *gquats = a.grads + 3 * n;
-    float *gscales = a.grads + 7 * n, *gopac = a.grads + 9 * n;
-    float *gcol = a.grads + 10 * n;
 
     // Geometry for the chain rule: plain float64 (contractions allowed) — only the forward's
     // decisions need the reference's exact arithmetic.
-    const ParamView pv(a.params, n);
+    const ParamPtrs pv = surfel_ptrs(a.params, n, P.shard, i);
     double p[3], R[9], Bc[3][2];
     {
-        const double mu[3] = {(double)pv.means[3 * i], (double)pv.means[3 * i + 1], (double)pv.means[3 * i + 2]};
+        const double mu[3] = {(double)pv.means[0], (double)pv.means[1], (double)pv.means[2]};
 #pragma unroll
         for (int r = 0; r < 3; ++r)
             p[r] = P.m_cw[3 * r] * mu[0] + P.m_cw[3 * r + 1] * mu[1] + P.m_cw[3 * r + 2] * mu[2] + P.inv[1 + r];
-        const double w = pv.quats[4 * i], x = pv.quats[4 * i + 1], y = pv.quats[4 * i + 2], z = pv.quats[4 * i + 3];
+        const double w = pv.quats[0], x = pv.quats[1], y = pv.quats[2], z = pv.quats[3];
         R[0] = 1.0 - 2.0 * (y * y + z * z);
         R[1] = 2.0 * (x * y - w * z);
         R[2] = 2.0 * (x * z + w * y);
@@ -81,7 +78,7 @@ __global__ void S2D_PBWD_BOUNDS k_project_bwd(const ProjectBwdArgs a) {
         R[6] = 2.0 * (x * z - w * y);
         R[7] = 2.0 * (y * z + w * x);
         R[8] = 1.0 - 2.0 * (x * x + y * y);
-        const double s0 = pv.scales[2 * i], s1 = pv.scales[2 * i + 1];
+        const double s0 = pv.scales[0], s1 = pv.scales[1];
 #pragma unroll
         for (int r = 0; r < 3; ++r) {
             Bc[r][0] = (P.m_cw[3 * r] * R[0] + P.m_cw[3 * r + 1] * R[3] + P.m_cw[3 * r + 2] * R[6]) * s0;
@@ -189,7 +186,7 @@ __global__ void S2D_PBWD_BOUNDS k_project_bwd(const ProjectBwdArgs a) {
         gn[2] = G3.x;
     }
     // Bc[:,k] = m_cw R[:,k] s_k
-    const double s0 = (double)pv.scales[2 * i], s1 = (double)pv.scales[2 * i + 1];
+    const double s0 = (double)pv.scales[0], s1 = (double)pv.scales[1];
     double gR[9];
     double gs0 = 0.0, gs1 = 0.0;
 #pragma unroll
@@ -215,24 +212,25 @@ __global__ void S2D_PBWD_BOUNDS k_project_bwd(const ProjectBwdArgs a) {
         for (int b = 0; b < 3; ++b)
             gR[3 * b + 2] = sg * (P.r_cw[b] * gn[0] + P.r_cw[3 + b] * gn[1] + P.r_cw[6 + b] * gn[2]);
     }
-    const double q[4] = {(double)pv.quats[4 * i], (double)pv.quats[4 * i + 1], (double)pv.quats[4 * i + 2],
-                         (double)pv.quats[4 * i + 3]};
+    const double q[4] = {(double)pv.quats[0], (double)pv.quats[1], (double)pv.quats[2],
+                         (double)pv.quats[3]};
     double gq[4];
     dR_dq(q, gR, gq);
+    const SurfelPtrs<float> gout = surfel_ptrs(a.grads, n, P.shard, i);  // same layout as the parameters
     // p = s_inv R(q_inv) mu + t_inv.  Accumulation is atomic (fire-and-forget reductions), so
     // views running concurrently on different streams may share one gradient block.
 #pragma unroll
     for (int b = 0; b < 3; ++b)
-        atomicAdd(gmeans + 3 * i + b,
+        atomicAdd(gout.means + b,
                   (float)(P.inv[0] * (P.r_cw[b] * gp[0] + P.r_cw[3 + b] * gp[1] + P.r_cw[6 + b] * gp[2])));
 #pragma unroll
-    for (int k = 0; k < 4; ++k) atomicAdd(gquats + 4 * i + k, (float)gq[k]);
-    atomicAdd(gscales + 2 * i, (float)gs0);
-    atomicAdd(gscales + 2 * i + 1, (float)gs1);
-    atomicAdd(gopac + i, G0.x);
-    atomicAdd(gcol + 3 * i, G0.y);
-    atomicAdd(gcol + 3 * i + 1, G0.z);
-    atomicAdd(gcol + 3 * i + 2, G0.w);
+    for (int k = 0; k < 4; ++k) atomicAdd(gout.quats + k, (float)gq[k]);
+    atomicAdd(gout.scales, (float)gs0);
+    atomicAdd(gout.scales + 1, (float)gs1);
+    atomicAdd(gout.opac, G0.x);
+    atomicAdd(gout.colors, G0.y);
+    atomicAdd(gout.colors + 1, G0.z);
+    atomicAdd(gout.colors + 2, G0.w);
     // leave the per-view 2D gradient buffer zeroed for the next view
     float4 *zero = reinterpret_cast<float4 *>(a.grad2d + (size_t)i * 16);
     const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -263,9 +261,10 @@ __device__ __forceinline__ float adam_one(float p, float g, float &m, float &v, 
 
 __global__ void __launch_bounds__(256) k_adam(float *__restrict__ params, const float *__restrict__ grads,
                                               float *__restrict__ m1, float *__restrict__ m2, int64_t n,
-                                              const AdamK k, const uint8_t *__restrict__ mask) {
+                                              const AdamK k, const uint8_t *__restrict__ mask,
+                                              const int32_t *__restrict__ skip) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    if (i >= n || (skip && *skip)) return;
     if (mask && !mask[i]) return;
     // means
 #pragma unroll
@@ -380,9 +379,10 @@ void launch_project_backward(const ProjectBwdArgs &a, cudaStream_t s) {
 // (e - start) / d (the mask).
 __global__ void __launch_bounds__(256) k_adam_vec(float4 *__restrict__ params, const float4 *__restrict__ grads,
                                                   float4 *__restrict__ m1, float4 *__restrict__ m2, int64_t n,
-                                                  const AdamK k, const uint8_t *__restrict__ mask) {
+                                                  const AdamK k, const uint8_t *__restrict__ mask,
+                                                  const int32_t *__restrict__ skip) {
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= 13 * n / 4) return;
+    if (c >= 13 * n / 4 || (skip && *skip)) return;
     const int64_t e0 = 4 * c;
     int seg;
     int64_t start;
@@ -425,7 +425,7 @@ __global__ void __launch_bounds__(256) k_adam_vec(float4 *__restrict__ params, c
 }
 
 void launch_adam(float *params, const float *grads, float *m1, float *m2, int64_t n, int64_t step,
-                 const s2d_adam_config &cfg, const uint8_t *mask, cudaStream_t s) {
+                 const s2d_adam_config &cfg, const uint8_t *mask, const int32_t *skip, cudaStream_t s) {
     AdamK k;
     k.lr_means = (float)cfg.lr_means;
     k.lr_rest = (float)cfg.lr_rest;
@@ -443,13 +443,13 @@ void launch_adam(float *params, const float *grads, float *m1, float *m2, int64_
         const int64_t chunks = 13 * n / 4;
         k_adam_vec<<<(unsigned)((chunks + 255) / 256), 256, 0, s>>>(
             reinterpret_cast<float4 *>(params), reinterpret_cast<const float4 *>(grads), reinterpret_cast<float4 *>(m1),
-            reinterpret_cast<float4 *>(m2), n, k, mask);
+            reinterpret_cast<float4 *>(m2), n, k, mask, skip);
         return;
     }
     const int64_t blocks = (n + 255) / 256;
     if (blocks > 0) {
         count_launch();
-        k_adam<<<(unsigned)blocks, 256, 0, s>>>(params, grads, m1, m2, n, k, mask);
+        k_adam<<<(unsigned)blocks, 256, 0, s>>>(params, grads, m1, m2, n, k, mask, skip);
     }
 }
 

@@ -131,7 +131,7 @@ __device__ __forceinline__ float slow_weight(const ViewParams &P, const RasterAr
     if (gb > kAccurateGb) {
         float u, v;
         double m64;
-        const float m32 = accurate_uvm(a.exact[id], px, py, u, v, m64);
+        const float m32 = accurate_uvm(a.acc[id], px, py, u, v, m64);
         if (fabs(m64 - P.maha_cut) <= accurate_band(gb, P.maha_cut)) resolve = true;
         else if (!(m64 <= P.maha_cut)) return 0.f;
         w = __fmul_rn(op, fast_exp2(__fmul_rn(m32, -0.72134752044448170368f)));
@@ -316,11 +316,12 @@ __device__ __forceinline__ int ring_fill(WarpRing &rg, int buf, ListCursor &c, c
 // halves' slots of a step interleave, so their 16-B reads hit disjoint banks), loaded by the
 // half's lane j (coalesced 16-B loads).  Returns how many.
 __device__ __forceinline__ int stream_fill(WarpRing &rg, int buf, const uint4 *ws, int e1,
-                                           const SplatRecord *rec, int half, int jh) {
+                                           const SplatRecord *rec, const AccurateRec *acc, int half, int jh) {
     const int n = min(16, e1);
     if (jh < n) {
         const uint4 en = __ldcg(ws + (e1 - 1 - jh));
         Slot &sl = rg.s[buf][2 * jh + half];
+        if (en.w) prefetch_accurate(acc + en.x);  // accurate slot (k_raster_fwd)
         const float4 *g = reinterpret_cast<const float4 *>(rec + en.x);
         float4 *d = reinterpret_cast<float4 *>(&sl.r);
         cp_async16(d + 0, g + 0);
@@ -403,6 +404,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32, ((kArg || kMaxW || kNormal) ? 
                         const float thi = __fadd_rn(P.maha_cut_f, gb), tlo = __fsub_rn(P.maha_cut_f, gb);
                         // flagged slots send every passing lane to slow_weight
                         const bool slow = gbs < 0.f || !(op > 1e-30f) || gb > kAccurateGb;
+                        if (gb > kAccurateGb) prefetch_accurate(a.acc + sl.meta.x);
                         // forward slot: q0 = (f, g, cut + gb, opacity),
                         // meta = (id, cut - gb or -3e38 (flagged), lo.x, lo.y)
                         sl.r.q0 = make_float4(bc.f, bc.g, thi, op);
@@ -540,7 +542,9 @@ __global__ void __launch_bounds__(kFwdWarps * 32, ((kArg || kMaxW || kNormal) ? 
                 const uint32_t cm = __any_sync(kFull, cl_bits != 0u) ? transpose32(__brev(cl_bits), lane) : 0u;
                 const bool h0 = (bm & 0x0F0F0F0Fu) != 0u, h1 = (bm & 0xF0F0F0F0u) != 0u;
                 const uint32_t b0 = __ballot_sync(kFull, h0), b1 = __ballot_sync(kFull, h1);
-                const uint4 en = make_uint4(ring.s[buf][31 - lane].meta.x, bm, cm, 0u);
+                // w: 1 for an accurate slot (k_raster_bwd prefetches its float64 data when staging)
+                const Slot &me = ring.s[buf][31 - lane];
+                const uint4 en = make_uint4(me.meta.x, bm, cm, !kRay && fabsf(me.r.q3.w) > kAccurateGb ? 1u : 0u);
                 const uint32_t lt = lanemask_lt();
                 if (h0) wp0[__popc(b0 & lt)] = en;
                 if (h1) wp1[__popc(b1 & lt)] = en;
@@ -797,7 +801,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, S2D_BWD_CTAS_PER_SM) k_raster_
     const int jh = (lane & 3) | ((lane >> 3) << 2);
     int e1 = half ? cnt1 : cnt0;
     int buf = 0;
-    int n = stream_fill(ring, 0, ws, e1, a.rec, half, jh);
+    int n = stream_fill(ring, 0, ws, e1, a.rec, a.acc, half, jh);
     e1 -= n;
     cp_commit();
     float v[NV];
@@ -843,7 +847,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, S2D_BWD_CTAS_PER_SM) k_raster_
             if (__any_sync(kFull, accurate)) {  // warp-uniform: the forward's slow_weight evaluation
                 if (accurate) {
                     double m64;
-                    const float m32 = accurate_uvm(a.exact[meta.x], px, py, u, vv, m64);
+                    const float m32 = accurate_uvm(a.acc[meta.x], px, py, u, vv, m64);
                     g = fast_exp2(__fmul_rn(m32, -0.72134752044448170368f));
                 }
             }
@@ -916,7 +920,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, S2D_BWD_CTAS_PER_SM) k_raster_
     while (true) {
         const int n0 = __shfl_sync(kFull, n, 0), n1 = __shfl_sync(kFull, n, 4);  // per half
         if (n0 + n1 == 0) break;
-        const int nn = stream_fill(ring, buf ^ 1, ws, e1, a.rec, half, jh);
+        const int nn = stream_fill(ring, buf ^ 1, ws, e1, a.rec, a.acc, half, jh);
         e1 -= nn;
         cp_commit();
         cp_wait<1>();

@@ -26,6 +26,7 @@ constexpr int kRadix = 1 << kRadixBits;
 #define S2D_PROJ_THREADS 128
 #endif
 constexpr int kProjThreads = S2D_PROJ_THREADS;  // surfels per projection CTA (one per thread)
+constexpr int kCompactTiles = 32;                // projection tiles per k_compact_hist CTA
 #ifndef S2D_EMIT_ITEMS
 #define S2D_EMIT_ITEMS 4
 #endif
@@ -39,14 +40,14 @@ struct SyncRegion {
     int *tickets;              // [16]
     int *n_drawn;              // on-screen surfels with a non-empty integer bbox (the sorted set)
     uint32_t *key_range;       // [2]: ~min, max depth key
-    uint32_t *proj_status;     // [ceil(n / kProjThreads)] compaction look-back of k_project
     uint32_t *depth_hist;      // [3 * kRadix]
     uint32_t *depth_status;    // [3][ceil(n / kSortTile) * kRadix]
     uint32_t *emit_status;     // [ceil(n / kEmitTile)]
     uint32_t *pair_hist;       // [2 * kRadix]
     uint32_t *pair_status;     // [2][ceil(pcap / kSortTile) * kRadix]
     int *amb_count;            // pixels listed for k_mask_fixup
-    uint32_t *tie_ctl;         // [2]: long-run count, inversion-in-a-long-run flag (k_tie_fix)
+    uint32_t *ccount;          // [ceil(n / kProjThreads / kCompactTiles)] drawn surfels per chunk
+    uint32_t *tie_ctl;         // [3]: long-run count, inversion-in-a-long-run flag, CTA ticket (k_tie_fix)
     int2 *ranges;              // [ntiles]
     size_t bytes;
 };
@@ -56,26 +57,29 @@ struct ProjectArgs {
     const float *params;
     SplatRecord *rec;
     ExactRec *exact;
+    AccurateRec *acc;
     short4 *rect;
     double *z64;
     uint8_t *flags;
-    uint32_t *keys;
+    uint32_t *keys;       // [n]: tile t's drawn (key, index) pairs at [t kProjThreads, + tcount[t])
     uint32_t *vals;
+    uint32_t *tcount;     // [ceil(n / kProjThreads)] drawn surfels per projection tile
+    uint32_t *ccount;     // [ceil(n / kProjThreads / kCompactTiles)] drawn per chunk (sync region, zeroed)
+    int *n_drawn;         // drawn total (sync region, zeroed)
     s2d_view_stats *stats;
     uint32_t *key_range;  // [~min, max] of on-screen depth keys (sync region, zeroed)
-    int *n_drawn;         // count of drawn surfels (sync region, zeroed)
-    int *ticket;          // tile ticket (sync region, zeroed)
-    uint32_t *status;     // look-back status words, one per projection tile (sync region, zeroed)
 };
 void launch_project(const ProjectArgs &a, cudaStream_t s);
 
-void launch_radix_hist(uint32_t *keys, const int *d_n, int n, const uint32_t *key_range, uint32_t *hist,
-                       cudaStream_t s);
-// n_host >= 0: pass over n_host entries that drops sentinel keys (0xffffffff); else *d_n entries
+// order-preserving concatenation of k_project's per-tile pairs, key rebase, digit histograms
+void launch_compact_hist(const uint32_t *skeys, const uint32_t *svals, const uint32_t *tcount,
+                         const uint32_t *ccount, int64_t n, const uint32_t *key_range, uint32_t *keys,
+                         uint32_t *vals, uint32_t *hist, cudaStream_t s);
+// one stable 8-bit LSD pass over the *d_n entries (cap: capacity the grid is sized for)
 void launch_onesweep(const uint32_t *kin, const uint32_t *vin, uint32_t *kout, uint32_t *vout,
-                     const int *d_n, int cap, int n_host, int shift, const uint32_t *hist_pass,
+                     const int *d_n, int cap, int shift, const uint32_t *hist_pass,
                      uint32_t *status, int *ticket, cudaStream_t s);
-// ctl: 2 zeroed words; list: >= cap / 64 + 1 words; scratch: cap words (may not alias keys / vals)
+// ctl: 3 zeroed words; list: >= cap / 64 + 1 words; scratch: cap words (may not alias keys / vals)
 void launch_tie_fix(const uint32_t *keys, uint32_t *vals, const double *z64, const int *d_n, int cap,
                     uint32_t *ctl, uint32_t *list, uint32_t *scratch, cudaStream_t s);
 
@@ -113,6 +117,7 @@ struct RasterArgs {
     int *bcount;
     const SplatRecord *rec;
     const ExactRec *exact;
+    const AccurateRec *acc;
     const short4 *rect;
     int2 *aux;  // per pixel (last list position, float bits of T before it)
     // forward outputs (forward writes, backward reads)
@@ -147,8 +152,9 @@ struct ProjectBwdArgs {
 };
 void launch_project_backward(const ProjectBwdArgs &a, cudaStream_t s);
 
+// skip (device, nullable): the step is a no-op when *skip != 0 (a view of it overflowed)
 void launch_adam(float *params, const float *grads, float *m1, float *m2, int64_t n, int64_t step,
-                 const s2d_adam_config &cfg, const uint8_t *mask, cudaStream_t s);
+                 const s2d_adam_config &cfg, const uint8_t *mask, const int32_t *skip, cudaStream_t s);
 
 // mapper.refine's backtracking GD step and gradient norm on the opacity + colour block (optim.cu)
 void launch_refine_gd(float *x, const float *x0, const float *g, int64_t n, double step, const uint8_t *mask,

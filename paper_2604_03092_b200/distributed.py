@@ -16,7 +16,7 @@ import torch
 import torch.distributed as dist
 
 __all__ = ["shard_views", "world", "allreduce_grads", "init_from_env", "SEGMENTS", "shard_rows",
-           "ShardedOptimizerState", "sharded_step"]
+           "ShardedOptimizerState", "sharded_step", "to_shard_major", "from_shard_major"]
 
 # packed parameter block segments (floats per surfel): means, quats, scales, opacity, colour
 SEGMENTS = (3, 4, 2, 1, 3)
@@ -54,16 +54,44 @@ def allreduce_grads(grads: torch.Tensor, loss: torch.Tensor | None = None, group
 
 
 def shard_rows(n: int, world_size: int) -> int:
-    """Surfels per optimizer shard: ceil(n / world), so every rank's reduce-scatter chunk has
-    the same size (the last shard is zero-padded)."""
+    """Surfels per optimizer shard: ceil(n / world), so every rank's slice of the packed blocks
+    has the same size (the last shard is zero-padded)."""
     return (n + world_size - 1) // world_size
 
 
-class ShardedOptimizerState:
-    """ZeRO-1 style optimizer sharding: rank r owns surfels [r c, (r + 1) c) of every packed
-    segment, holds Adam moments for those c surfels only, and updates only them."""
+def to_shard_major(flat: torch.Tensor, n: int, c: int) -> torch.Tensor:
+    """Plain packed block (13 n) -> the shard-major layout of s2d_view_set_layout (13 W c, W =
+    ceil(n / c)): shard s = [means 3c | quats 4c | scales 2c | opacities c | colors 3c] of
+    surfels [s c, (s + 1) c), zero-padded."""
+    w = (n + c - 1) // c
+    out = flat.new_zeros((w, 13 * c))
+    off, col = 0, 0
+    for d in SEGMENTS:
+        seg = flat.new_zeros((w * c, d))
+        seg[:n] = flat[off:off + d * n].view(n, d)
+        out[:, col * c:(col + d) * c] = seg.view(w, c * d)
+        off += d * n
+        col += d
+    return out.view(-1)
 
-    def __init__(self, n: int, group=None, device=None, dtype=torch.float32):
+
+def from_shard_major(flat: torch.Tensor, n: int, c: int) -> torch.Tensor:
+    """Inverse of to_shard_major: the plain packed block (13 n)."""
+    w = (n + c - 1) // c
+    blk = flat.view(w, 13 * c)
+    parts, col = [], 0
+    for d in SEGMENTS:
+        parts.append(blk[:, col * c:(col + d) * c].reshape(w * c, d)[:n].reshape(-1))
+        col += d
+    return torch.cat(parts)
+
+
+class ShardedOptimizerState:
+    """ZeRO-1 style optimizer sharding over the shard-major packed blocks: rank r owns the
+    contiguous slice [13 r c, 13 (r + 1) c) of the parameter and gradient blocks (surfels
+    [r c, (r + 1) c)), holds Adam moments for those c surfels only, and updates only them."""
+
+    def __init__(self, n: int, group=None, device=None, dtype=torch.float32, mask=None):
         self.rank, self.world_size = world(group)
         self.group = group
         self.n = n
@@ -71,50 +99,37 @@ class ShardedOptimizerState:
         f = dict(device=device, dtype=dtype)
         self.m1 = torch.zeros(13 * self.c, **f)
         self.m2 = torch.zeros(13 * self.c, **f)
-        self.params = torch.zeros(13 * self.c, **f)
-        self.grads = torch.zeros(13 * self.c, **f)
-        self._pad = torch.zeros(self.world_size * self.c * 4, **f)  # one segment, padded
-        self._gather = torch.zeros(self.world_size * self.c * 4, **f)
+        self.grads = torch.zeros(13 * self.c, **f)  # this rank's summed gradients (reduce-scatter)
+        self.mask = None
+        if mask is not None:
+            self.mask = self.shard_mask(mask)
 
-    def _segments(self, flat, rows):
-        out, off = [], 0
-        for w in SEGMENTS:
-            out.append(flat[off:off + w * rows].view(rows, w))
-            off += w * rows
-        return out
+    def shard_mask(self, mask: torch.Tensor) -> torch.Tensor:
+        lo, hi = self.rank * self.c, min((self.rank + 1) * self.c, self.n)
+        m = torch.zeros(self.c, dtype=mask.dtype, device=mask.device)
+        if hi > lo:
+            m[:hi - lo] = mask[lo:hi]
+        return m
+
+    def slice(self, block: torch.Tensor) -> torch.Tensor:
+        """This rank's contiguous slice of a shard-major block."""
+        return block[13 * self.rank * self.c:13 * (self.rank + 1) * self.c]
 
 
 def sharded_step(params: torch.Tensor, grads: torch.Tensor, state: ShardedOptimizerState, adam_fn,
                  mask: torch.Tensor | None = None, group=None) -> None:
-    """reduce-scatter(SUM) the packed gradient block by surfel shard, run ``adam_fn`` on this
-    rank's shard (packed over its c surfels: ``adam_fn(shard_params, shard_grads, m1, m2, c,
-    shard_mask)``), then all-gather the updated parameters into every rank's replica.  Moves
-    the same bytes as the all-reduce it replaces and cuts the optimizer's HBM traffic and
-    moment memory by the world size."""
-    n, c, W, r = state.n, state.c, state.world_size, state.rank
-    lo, hi = r * c, min((r + 1) * c, n)
-    gseg = state._segments(grads, n)
-    pseg = state._segments(params, n)
-    sg = state._segments(state.grads, c)
-    sp = state._segments(state.params, c)
-    for k, w in enumerate(SEGMENTS):
-        pad = state._pad[:W * c * w].view(W * c, w)
-        pad[:n].copy_(gseg[k])
-        pad[n:].zero_()
-        dist.reduce_scatter_tensor(sg[k], pad, op=dist.ReduceOp.SUM, group=group)
-        sp[k].zero_()
-        if hi > lo:
-            sp[k][:hi - lo].copy_(pseg[k][lo:hi])
-    smask = None
-    if mask is not None:
-        smask = torch.zeros(c, dtype=mask.dtype, device=mask.device)
-        if hi > lo:
-            smask[:hi - lo].copy_(mask[lo:hi])
-    adam_fn(state.params, state.grads, state.m1, state.m2, c, smask)
-    for k, w in enumerate(SEGMENTS):
-        out = state._gather[:W * c * w].view(W * c, w)
-        dist.all_gather_into_tensor(out, sp[k].contiguous(), group=group)
-        pseg[k].copy_(out[:n])
+    """One sharded optimizer step on shard-major blocks (13 W c): ONE reduce-scatter (SUM) of the
+    gradient block leaves rank r the summed gradients of its surfels, ``adam_fn(p, g, m1, m2, c,
+    shard_mask)`` updates its contiguous parameter slice in place, and ONE all-gather writes
+    every rank's slice back into every replica (in place under NCCL).  No staging copies: the
+    same bytes over NVLink as the all-reduce it replaces, with the optimizer's HBM traffic and
+    moment memory divided by the world size."""
+    dist.reduce_scatter_tensor(state.grads, grads, op=dist.ReduceOp.SUM, group=group)
+    mine = state.slice(params)
+    smask = state.mask if mask is None else state.shard_mask(mask)
+    adam_fn(mine, state.grads, state.m1, state.m2, state.c, smask)
+    src = mine if dist.get_backend(group) == "nccl" else mine.clone()
+    dist.all_gather_into_tensor(params, src, group=group)
 
 
 def init_from_env(backend: str = "nccl") -> tuple:

@@ -25,7 +25,8 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .distributed import ShardedOptimizerState, allreduce_grads, shard_views, sharded_step, world
+from .distributed import (ShardedOptimizerState, allreduce_grads, from_shard_major, shard_views, sharded_step,
+                          to_shard_major, world)
 from .engine import (DeviceContext, ImageBuffers, View, camera_struct, config_struct, forward_checked,
                      pack_params, unpack_params)
 from .geometry import as_packed_pose
@@ -370,14 +371,23 @@ class AdamRefiner:
     """Multi-view fused-Adam refinement of all surfel parameters, views sharded over ranks.
 
     With N > 1 ranks the optimizer is sharded by default (``shard_optimizer``): the packed
-    gradients are reduce-scattered by surfel range, each rank runs the fused Adam kernel on
-    its shard (moments for 1/N of the surfels), and the parameters are all-gathered.
+    parameter and gradient blocks use the shard-major layout (s2d_view_set_layout, c =
+    ceil(n / N) surfels per rank), so ONE reduce-scatter leaves each rank the summed gradients
+    of its contiguous slice, the fused Adam kernel updates that slice in place (moments for c
+    surfels), and ONE in-place all-gather refreshes every replica.
 
     ``targets_rgb[v]`` (H,W,3) / ``targets_depth[v]`` (H,W) may be numpy arrays, device
     tensors, or (``host_targets=True``) host tensors that are pinned and copied in every
     step on a copy stream, each view's backward waiting for its own copy (the end-to-end
     path: the transfers overlap the forwards and the other views' compute).
     ``inflight`` views run concurrently on separate streams.
+
+    ``step(sync=False)`` queues an iteration without a host round trip: the Adam step is
+    skipped on the device when a view overflowed its pair capacity (the overflow word of the
+    views' accumulated stats, all-reduced over ranks), and the host notices it one iteration
+    later, regrows the capacity and re-runs the skipped iterations, so the sequence of applied
+    steps is exactly that of a synchronous loop.  The loss of every iteration is copied to
+    pinned host memory on the device's queue; ``losses()`` returns them.
     """
 
     def __init__(self, surfels, intr: CameraIntrinsics, poses, targets_rgb, targets_depth,
@@ -393,22 +403,25 @@ class AdamRefiner:
         self.cam = camera_struct(intr)
         self.cfg = config_struct(raster_cfg)
         if isinstance(surfels, torch.Tensor):
-            self.params = surfels.to(self.dev, torch.float32).contiguous()
-            self.n = self.params.numel() // 13
+            plain = surfels.to(self.dev, torch.float32).contiguous()
+            self.n = plain.numel() // 13
         else:
             self.n = len(surfels)
-            self.params = pack_params(surfels, self.dev)
-        self.grads = torch.zeros_like(self.params)
-        # N > 1: ZeRO-1 style optimizer sharding (reduce-scatter, Adam on this rank's surfels,
-        # all-gather) unless disabled; N = 1: one full Adam step
+            plain = pack_params(surfels, self.dev)
+        # N > 1: ZeRO-1 style optimizer sharding over the shard-major blocks unless disabled
         self.sharded = (self.world_size > 1) if shard_optimizer is None else bool(shard_optimizer)
+        self.mask = None if mask is None else torch.as_tensor(np.asarray(mask, dtype=np.uint8)).to(self.dev)
         if self.sharded:
-            self.opt_state = ShardedOptimizerState(self.n, group, self.dev)
+            self.opt_state = ShardedOptimizerState(self.n, group, self.dev, mask=self.mask)
+            self.shard = self.opt_state.c
+            self.params = to_shard_major(plain, self.n, self.shard) if self.shard < self.n else plain
             self.m1, self.m2 = self.opt_state.m1, self.opt_state.m2
         else:
+            self.shard = self.n
+            self.params = plain
             self.m1 = torch.zeros_like(self.params)
             self.m2 = torch.zeros_like(self.params)
-        self.mask = None if mask is None else torch.as_tensor(np.asarray(mask, dtype=np.uint8)).to(self.dev)
+        self.grads = torch.zeros_like(self.params)
         self.all_poses = [as_packed_pose(p) for p in poses]
         self.my_views = shard_views(len(self.all_poses), self.rank, self.world_size)
         self.loss_cfg = loss
@@ -429,6 +442,9 @@ class AdamRefiner:
         self.inflight = max(1, int(inflight))
         self.active_lanes = self.inflight
         self.lanes = [_Lane(self.ctx, h, w, self.dev) for _ in range(self.inflight)]
+        for lane in self.lanes:
+            N.check(N.lib().s2d_view_set_layout(lane.view.handle, self.shard if self.shard < self.n else 0),
+                    "s2d_view_set_layout")
         if host_targets:
             # end-to-end path: every view's targets go up on a copy stream at the start of the
             # step, into per-view device buffers; a view's backward (the only reader) waits
@@ -439,8 +455,6 @@ class AdamRefiner:
         self.view = self.lanes[0].view  # the first lane (phase timing / inspection)
         self.loss_acc = torch.zeros(1, dtype=torch.float64, device=self.dev)
         self.stats_acc = torch.zeros(8, dtype=torch.int32, device=self.dev)
-        self.host_stats = torch.zeros(8, dtype=torch.int32).pin_memory()
-        self.host_loss = torch.zeros(1, dtype=torch.float64).pin_memory()
         self.step_count = 0
         # CUDA graph of one step's views (forward, stats, backward on every lane stream): one
         # launch per step instead of ~4 library calls per view from Python
@@ -448,9 +462,11 @@ class AdamRefiner:
         self._graph = None
         self._graph_launches = 0
         self.kernel_launches = 0  # library kernels launched by step() (graph replays included)
-        self.regrows = 0  # steps re-run after a view overflowed the pair capacity
+        self.regrows = 0  # iterations re-run after a view overflowed the pair capacity
         self.h2d_bytes_per_step = (sum(self.rgb[v].numel() + self.depth[v].numel() for v in self.my_views) * 4
                                    if host_targets else 0)
+        self._pending = []  # queued iterations: (step, pinned stats, pinned loss, done event)
+        self._losses = []
         self._size_pairs()
 
     def _size_pairs(self):
@@ -478,8 +494,6 @@ class AdamRefiner:
         self.loss_acc.zero_()
         self.stats_acc.zero_()
         lanes = self.lanes[: self.active_lanes]
-        start = torch.cuda.Event()
-        start.record(main)
         for lane in lanes:
             lane.stream.wait_stream(main)
         copied = {}
@@ -512,60 +526,101 @@ class AdamRefiner:
             main.wait_stream(self.copy_stream)
 
     def _capture(self):
-        """Capture compute_grads (+ the stats read-back) into a CUDA graph.  The pair
-        capacities must already fit (an eager step sized them): the library does not
-        allocate while they do."""
+        """Capture compute_grads into a CUDA graph.  The pair capacities must already fit (an
+        eager step sized them): the library does not allocate while they do."""
         torch.cuda.synchronize(self.dev)
         g = torch.cuda.CUDAGraph()
         l0 = N.lib().s2d_launch_count()
         with torch.cuda.graph(g):
             self.compute_grads()
-            self.host_stats.copy_(self.stats_acc, non_blocking=True)
         self._graph_launches = N.lib().s2d_launch_count() - l0
         self._graph = g
 
-    def _grads_checked(self):
-        """compute_grads, re-run with a grown pair capacity when a view overflowed it."""
-        for _ in range(3):
-            l0 = N.lib().s2d_launch_count()
-            if self.cuda_graph and self.step_count > 0:
-                if self._graph is None:
-                    self._capture()
-                self._graph.replay()
-                self.kernel_launches += self._graph_launches
-            else:
-                self.compute_grads()
-                self.host_stats.copy_(self.stats_acc, non_blocking=True)
-                self.kernel_launches += N.lib().s2d_launch_count() - l0
-            torch.cuda.current_stream(self.dev).synchronize()
-            if not int(self.host_stats[4]):
-                return
-            self._reserve(int(self.host_stats[1]) * 5 // 4 + 4096)
-            self._graph = None  # buffers may have moved: capture again
-            self.regrows += 1
-
-    def step(self) -> float:
-        """One refine iteration; returns the total loss over ALL views (all ranks)."""
-        self._grads_checked()
-        self.step_count += 1
+    def _enqueue(self):
+        """Queue one iteration: views forward+backward, collectives, the gated Adam step, and the
+        stats / loss copies to pinned host memory."""
         l0 = N.lib().s2d_launch_count()
+        if self.cuda_graph and self.step_count > 0:
+            if self._graph is None:
+                self._capture()
+            self._graph.replay()
+            self.kernel_launches += self._graph_launches
+        else:
+            self.compute_grads()
+        step = self.step_count + 1
+        overflow = self.stats_acc[4:5]
+        if self.world_size > 1:
+            # every rank must skip together: the overflow word (and the max pair count) over ranks
+            import torch.distributed as dist
+            dist.all_reduce(self.stats_acc, op=dist.ReduceOp.MAX, group=self.group)
         if self.sharded:
             allreduce_grads(self.loss_acc, None, self.group)
-            sharded_step(self.params, self.grads, self.opt_state, self._adam, self.mask, self.group)
+            sharded_step(self.params, self.grads, self.opt_state,
+                         lambda p, g, m1, m2, c, m: self._adam(p, g, m1, m2, c, m, step, overflow), None, self.group)
         else:
             allreduce_grads(self.grads, self.loss_acc, self.group)
-            self._adam(self.params, self.grads, self.m1, self.m2, self.n, self.mask)
+            self._adam(self.params, self.grads, self.m1, self.m2, self.n, self.mask, step, overflow)
         self.kernel_launches += N.lib().s2d_launch_count() - l0
-        self.host_loss.copy_(self.loss_acc, non_blocking=True)
-        torch.cuda.current_stream(self.dev).synchronize()
-        return float(self.host_loss[0])
+        hs = torch.empty(8, dtype=torch.int32).pin_memory()
+        hl = torch.empty(1, dtype=torch.float64).pin_memory()
+        hs.copy_(self.stats_acc, non_blocking=True)
+        hl.copy_(self.loss_acc, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.dev))
+        self.step_count = step
+        self._pending.append((step, hs, hl, ev))
 
-    def _adam(self, params, grads, m1, m2, n, mask):
-        N.check(N.lib().s2d_adam_step(torch.cuda.current_stream(self.dev).cuda_stream, N.dptr(params), N.dptr(grads),
-                                      N.dptr(m1), N.dptr(m2), int(n), self.step_count, self.adam, N.dptr(mask)),
-                "s2d_adam_step")
+    def _resolve(self, keep: int):
+        """Settle all but the newest `keep` queued iterations (waits for them).  On an overflow,
+        the iterations from the overflowing one on were all skipped on the device (the
+        parameters did not change, so each overflowed again): regrow and re-run them."""
+        while len(self._pending) > keep:
+            step, hs, hl, ev = self._pending[0]
+            ev.synchronize()
+            if int(hs[4]):
+                redo = len(self._pending)
+                torch.cuda.synchronize(self.dev)
+                self._pending.clear()
+                self.step_count = step - 1
+                self._reserve(int(hs[1]) * 5 // 4 + 4096)
+                self._graph = None  # buffers may have moved: capture again
+                self.regrows += 1
+                for _ in range(redo):
+                    self._enqueue()
+                continue
+            self._losses.append(float(hl[0]))
+            self._pending.pop(0)
+
+    def step(self, sync: bool = True):
+        """One refine iteration; with ``sync`` returns the total loss over ALL views (all
+        ranks), else queues it (``losses()`` collects the values)."""
+        self._resolve(keep=1)  # the previous iteration is checked while this one is queued
+        self._enqueue()
+        if sync:
+            self._resolve(keep=0)
+            return self._losses[-1]
+        return None
+
+    def losses(self) -> list:
+        """Losses of all iterations so far (waits for the queued ones)."""
+        self._resolve(keep=0)
+        return list(self._losses)
+
+    def _adam(self, params, grads, m1, m2, n, mask, step, skip=None):
+        N.check(N.lib().s2d_adam_step_gated(torch.cuda.current_stream(self.dev).cuda_stream, N.dptr(params),
+                                            N.dptr(grads), N.dptr(m1), N.dptr(m2), int(n), int(step), self.adam,
+                                            N.dptr(mask), N.dptr(skip)), "s2d_adam_step_gated")
+
+    def plain_params(self) -> torch.Tensor:
+        """The parameters in the plain packed layout (13 n)."""
+        self._resolve(keep=0)
+        return from_shard_major(self.params, self.n, self.shard) if self.shard < self.n else self.params
+
+    def plain_grads(self) -> torch.Tensor:
+        """The last iteration's summed gradients (this rank's views; plain layout)."""
+        return from_shard_major(self.grads, self.n, self.shard) if self.shard < self.n else self.grads
 
     def surfel_arrays(self) -> SurfelArrays:
-        P = unpack_params(self.params, self.n)
+        P = unpack_params(self.plain_params(), self.n)
         return SurfelArrays(*[P[k].double().cpu().numpy() for k in ("means", "quats", "scales", "opacities",
                                                                      "colors")])

@@ -74,3 +74,27 @@ def drawn_order(bbox, order):
     order = np.asarray(order, dtype=np.int64)
     b = np.asarray(bbox)[order]
     return order[(b[:, 0] <= b[:, 1]) & (b[:, 2] <= b[:, 3])]
+
+
+def l1_oracle_grads(surfels, pose, intr, trgb, tdep, w_rgb, w_depth, gpu_color, gpu_depth, band=1e-5):
+    """Float64 oracle gradients of the L1 loss (no depth mask) for a GPU comparison.
+
+    sign(C - C*) is not determined at float32 precision where the float64 residual is within
+    the float32 render error; there (|C64 - C*| <= band, |D64 - D*| <= band |D*|) the seed takes
+    the GPU render's sign, everywhere else the oracle's own.  Returns (loss, grads, number of
+    such sign-ambiguous pixel channels)."""
+    import oracle as O
+    buf = O.render(surfels, pose, intr)
+    loss, g_rgb, g_d = O.loss_seeds(buf, trgb, tdep, "l1", w_rgb, w_depth, mask_depth=False)
+    h, w = buf.depth.shape
+    npx = h * w
+    amb = np.abs(buf.color - trgb) <= band
+    g_rgb[amb] = (w_rgb / (3.0 * npx)) * np.sign(np.asarray(gpu_color, float) - trgb)[amb]
+    ambd = np.abs(buf.depth - tdep) <= band * np.maximum(np.abs(tdep), 1e-30)
+    g_d[ambd] = (w_depth / npx) * np.sign(np.asarray(gpu_depth, float) - tdep)[ambd]
+    grads = O.backward(surfels, pose, intr, buf, g_rgb, g_d)
+    return loss, grads, int(amb.sum() + ambd.sum())
+
+
+def f32(a):
+    return np.asarray(a, np.float32).astype(np.float64)

@@ -88,7 +88,8 @@ def _sharded_worker(rank, world, port, out_dir):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    from paper_2604_03092_b200.distributed import ShardedOptimizerState, allreduce_grads, shard_views, sharded_step
+    from paper_2604_03092_b200.distributed import (ShardedOptimizerState, allreduce_grads, from_shard_major,
+                                                   shard_views, sharded_step, to_shard_major)
     import oracle as O
     sc, poses = _views()
     n = len(sc.surfels)
@@ -103,8 +104,12 @@ def _sharded_worker(rank, world, port, out_dir):
     params = torch.from_numpy(np.concatenate([s.means.ravel(), s.quats.ravel(), s.scales.ravel(),
                                               s.opacities.ravel(), s.colors.ravel()]))
     mask = torch.from_numpy((np.arange(n) % 7 != 0).astype(np.uint8))
-    state = ShardedOptimizerState(n, dtype=torch.float64)
+    state = ShardedOptimizerState(n, dtype=torch.float64, mask=mask)
     assert state.m1.numel() == 13 * state.c < 13 * n
+    # the shard-major layout (s2d_view_set_layout): one contiguous slice per rank
+    params = to_shard_major(params, n, state.c)
+    grads = to_shard_major(grads, n, state.c)
+    assert params.numel() == 13 * world * state.c
 
     def adam_fn(p, g, m1, m2, c, smask):
         O.adam_step(p.numpy(), g.numpy(), m1.numpy(), m2.numpy(), step[0],
@@ -112,7 +117,8 @@ def _sharded_worker(rank, world, port, out_dir):
 
     for k in range(3):
         step = [k + 1]
-        sharded_step(params, grads.clone(), state, adam_fn, mask)
+        sharded_step(params, grads.clone(), state, adam_fn)
+    params = from_shard_major(params, n, state.c)
     np.savez(os.path.join(out_dir, f"s{rank}.npz"), params=params.numpy(), loss=loss.numpy())
     dist.barrier()
     dist.destroy_process_group()
@@ -120,8 +126,9 @@ def _sharded_worker(rank, world, port, out_dir):
 
 @pytest.mark.parametrize("world", [2, 3])
 def test_gloo_sharded_optimizer_matches_replicated_adam(tmp_path, world):
-    """reduce-scatter -> Adam on each rank's surfel shard -> all-gather == the replicated step
-    (bit-exact in float64), with a surfel mask and an uneven last shard."""
+    """One reduce-scatter -> Adam on each rank's contiguous surfel shard -> one all-gather, on the
+    shard-major packed blocks, == the replicated step (bit-exact in float64), with a surfel mask
+    and an uneven (zero-padded) last shard."""
     mp.start_processes(_sharded_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world,
                        start_method="spawn")
     import oracle as O
@@ -142,3 +149,20 @@ def test_gloo_sharded_optimizer_matches_replicated_adam(tmp_path, world):
     for o in outs:
         assert np.array_equal(o, outs[0])
     assert np.allclose(outs[0], p, rtol=1e-13, atol=1e-15)
+
+
+def test_shard_major_round_trip():
+    from paper_2604_03092_b200.distributed import from_shard_major, to_shard_major
+    for n, c in ((10, 4), (7, 7), (9, 3), (5, 100)):
+        flat = torch.arange(13 * n, dtype=torch.float64)
+        sm = to_shard_major(flat, n, c)
+        w = (n + c - 1) // c
+        assert sm.numel() == 13 * w * c
+        assert torch.equal(from_shard_major(sm, n, c), flat)
+        # surfel i of shard s: means at 13 c s + 3 j, colours at 13 c s + 10 c + 3 j
+        blk = sm.view(w, 13 * c)
+        for i in range(n):
+            s_, j = divmod(i, c)
+            assert blk[s_, 3 * j + 1] == flat[3 * i + 1]
+            assert blk[s_, 10 * c + 3 * j + 2] == flat[10 * n + 3 * i + 2]
+            assert blk[s_, 9 * c + j] == flat[9 * n + i]

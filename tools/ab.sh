@@ -1,4 +1,5 @@
 # usage: ab.sh variant... ; runs bench for each, prints value + phases
+export S2D_ALLOW_OLD_LIB=1
 for v in "$@"; do
   if [ $v = default ]; then unset S2D_LIB_PATH; else export S2D_LIB_PATH=$PWD/paper_2604_03092_b200/lib/$v/libsurfel2d.so; fi
   timeout 600 python bench.py --no-cpu-baseline --steps 20 > gpurun_out/bench_$v.log 2>&1
