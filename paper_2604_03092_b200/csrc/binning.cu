@@ -228,11 +228,9 @@ __global__ void __launch_bounds__(kProjThreads, S2D_PROJ_MINB * 256 / kProjThrea
         for (int w = 0; w < kProjThreads / 32; ++w) tot += s_wcnt[w];
         a.tcount[tile] = tot;
         // per chunk of kCompactTiles tiles: k_compact_hist derives every chunk's offset from
-        // these totals (a few coalesced loads per CTA, no chained scan), and the drawn total
-        if (tot) {
-            atomicAdd(a.ccount + tile / kCompactTiles, tot);
-            atomicAdd(a.n_drawn, (int)tot);
-        }
+        // these totals (a few coalesced loads per CTA, no chained scan) and the drawn total
+        // (one atomic per tile on a per-chunk word: no single contended counter)
+        if (tot) atomicAdd(a.ccount + tile / kCompactTiles, tot);
     }
 }
 
@@ -249,7 +247,7 @@ __global__ void __launch_bounds__(256) k_compact_hist(const uint32_t *__restrict
                                                       const uint32_t *__restrict__ tcount,
                                                       const uint32_t *__restrict__ ccount, int ntp,
                                                       const uint32_t *__restrict__ key_range, uint32_t *keys,
-                                                      uint32_t *vals, uint32_t *hist) {
+                                                      uint32_t *vals, uint32_t *hist, int *n_drawn) {
     __shared__ uint32_t sh[3 * kRadix];
     __shared__ uint32_t s_cnt[kCompactTiles], s_off[kCompactTiles];
     const int tid = threadIdx.x, c = blockIdx.x;
@@ -269,6 +267,7 @@ __global__ void __launch_bounds__(256) k_compact_hist(const uint32_t *__restrict
         }
         s_cnt[tid] = cnt;
         s_off[tid] = base + x - cnt;
+        if (tid == 31 && c == (int)gridDim.x - 1) *n_drawn = (int)(base + x);  // the drawn total
     }
     __syncthreads();
     const uint32_t kmin = ~key_range[0], kmax = key_range[1];
@@ -651,12 +650,13 @@ void launch_project(const ProjectArgs &a, cudaStream_t s) {
 
 void launch_compact_hist(const uint32_t *skeys, const uint32_t *svals, const uint32_t *tcount,
                          const uint32_t *ccount, int64_t n, const uint32_t *key_range, uint32_t *keys,
-                         uint32_t *vals, uint32_t *hist, cudaStream_t s) {
+                         uint32_t *vals, uint32_t *hist, int *n_drawn, cudaStream_t s) {
     const int ntp = (int)((n + kProjThreads - 1) / kProjThreads);
     const int blocks = (ntp + kCompactTiles - 1) / kCompactTiles;
     if (blocks > 0) {
         count_launch();
-        k_compact_hist<<<blocks, 256, 0, s>>>(skeys, svals, tcount, ccount, ntp, key_range, keys, vals, hist);
+        k_compact_hist<<<blocks, 256, 0, s>>>(skeys, svals, tcount, ccount, ntp, key_range, keys, vals, hist,
+                                               n_drawn);
     }
 }
 

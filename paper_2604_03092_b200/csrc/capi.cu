@@ -365,13 +365,12 @@ int view_forward(s2d_view *v, cudaStream_t s, const float *params, int64_t n, co
         pa.vals = v->vals[1];
         pa.tcount = v->tcount;
         pa.ccount = sr.ccount;
-        pa.n_drawn = sr.n_drawn;
         launch_project(pa, s);
         mark();
         // depth order: the drawn surfels' keys rebased to 24 bits, 3 stable 8-bit passes, then
         // k_tie_fix orders equal keys by (z64, index)
         launch_compact_hist(v->keys[1], v->vals[1], v->tcount, sr.ccount, n, sr.key_range, v->keys[0], v->vals[0],
-                            sr.depth_hist, s);
+                            sr.depth_hist, sr.n_drawn, s);
         const int64_t sort_tiles = (n + kSortTile - 1) / kSortTile + 1;
         int cur = 0;
         for (int p = 0; p < 3; ++p) {

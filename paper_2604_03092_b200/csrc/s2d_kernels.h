@@ -65,7 +65,6 @@ struct ProjectArgs {
     uint32_t *vals;
     uint32_t *tcount;     // [ceil(n / kProjThreads)] drawn surfels per projection tile
     uint32_t *ccount;     // [ceil(n / kProjThreads / kCompactTiles)] drawn per chunk (sync region, zeroed)
-    int *n_drawn;         // drawn total (sync region, zeroed)
     s2d_view_stats *stats;
     uint32_t *key_range;  // [~min, max] of on-screen depth keys (sync region, zeroed)
 };
@@ -74,7 +73,7 @@ void launch_project(const ProjectArgs &a, cudaStream_t s);
 // order-preserving concatenation of k_project's per-tile pairs, key rebase, digit histograms
 void launch_compact_hist(const uint32_t *skeys, const uint32_t *svals, const uint32_t *tcount,
                          const uint32_t *ccount, int64_t n, const uint32_t *key_range, uint32_t *keys,
-                         uint32_t *vals, uint32_t *hist, cudaStream_t s);
+                         uint32_t *vals, uint32_t *hist, int *n_drawn, cudaStream_t s);
 // one stable 8-bit LSD pass over the *d_n entries (cap: capacity the grid is sized for)
 void launch_onesweep(const uint32_t *kin, const uint32_t *vin, uint32_t *kout, uint32_t *vout,
                      const int *d_n, int cap, int shift, const uint32_t *hist_pass,
