@@ -3,20 +3,22 @@
 
 One step = one refine iteration: this rank's share of the 32 views forward+backward
 (projection, depth order, tile binning, compositing, L1 RGB + 0.1 L1 depth seeds,
-reverse-order backward, projection backward), the NCCL all-reduce of the packed
-surfel gradients (N>1), and the fused Adam step.  Views are sharded over ranks
-(strong scaling: 32 views total at every N).
+reverse-order backward, projection backward), the NCCL reduce-scatter / all-gather of the
+shard-major surfel blocks (N>1), and the fused Adam step.  Views are sharded over ranks
+(strong scaling: 32 views total at every N); `--gpus N` outside torchrun starts N ranks.
 
   value  = whole-job Mpix/s = 32 views * 640*480 px / step time (device-resident targets)
   e2e    = the same through the public API with the targets copied in from pinned host
            memory every step and the loss read back (AdamRefiner(host_targets=True))
   refine_iters_per_s = 1 / step time
-  roofline = the dominant kernel's algorithmic bytes / its CUDA-event duration vs measured HBM
-  cpu_baseline = the float64 CPU port (oracle/) on a bounded sample of views, host threads
+  roofline = the dominant kernel's algorithmic bytes / its CUDA-event duration vs measured HBM;
+           roofline_issue = the raster kernels' warp instructions / launch time vs issue peak
+  cpu_baseline = the reference's own numba path (baseline/_ref) on config-4 views, one per
+           process; the float64 C port (oracle/) beside it
 
-``--impl reference`` times the CPU port of the reference path (the reference itself is
-Python+numba and not on the GPU box) on the same config/metric: each step is one
-fwd+bwd view per host thread.
+``--impl reference`` times the reference's own CPU path (surfelslam's numba
+grad_color_opacity from baseline/_ref, one view per process on the host cores; the C port
+when baseline/_ref is absent) on the same config and metric.
 """
 
 from __future__ import annotations
@@ -491,6 +493,10 @@ def main():
                          "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": traffic,
                          "peak_source": peak_src, "algorithmic_bytes_per_launch": pb[dom],
                          "launch_ms": round(per_launch_ms[dom], 4), "sm_issue": issue},
+            # the raster kernels are issue-bound, not HBM-bound: their warp instructions per launch
+            # (ncu, profiles/ncu_traffic.json) over the measured launch time, against the chip's
+            # issue rate (148 SMs x 4 schedulers x the SM clock under load)
+            "roofline_issue": issue_roofline(traffic_src, per_launch_ms, clk),
             "roofline_view": {"bytes": view_bytes, "ms": round(view_ms, 4),
                               "achieved_gbs": round(view_bytes / (view_ms * 1e-3) / 1e9, 1) if view_ms > 0 else None,
                               "frac": round(view_bytes / (view_ms * 1e-3) / 1e9 / hbm, 4) if view_ms > 0 else None},
@@ -506,6 +512,25 @@ def main():
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def issue_roofline(traffic_src, per_launch_ms, clk):
+    """Issue-rate roofline of the raster kernels: warp instructions per launch (the committed
+    ncu capture) / measured launch time vs 148 SMs x 4 issue slots x clock."""
+    if not traffic_src:
+        return None
+    mhz = (clk or {}).get("sm_mhz") or 1965.0
+    peak = 148 * 4 * mhz * 1e6  # warp instructions per second
+    out = {"unit": "warp-instr/s", "peak": peak, "peak_source": f"148 SMs x 4 schedulers x {mhz:.0f} MHz",
+           "source": traffic_src.get("source")}
+    for phase in ("raster_fwd", "raster_bwd"):
+        k = traffic_src.get("per_launch", {}).get(KERNEL_OF_PHASE[phase], {})
+        wi = k.get("warp_instructions")
+        if wi and per_launch_ms.get(phase):
+            ach = wi / (per_launch_ms[phase] * 1e-3)
+            out[phase] = {"warp_instructions": wi, "launch_ms": round(per_launch_ms[phase], 4),
+                          "achieved": ach, "frac": round(ach / peak, 4)}
+    return out
 
 
 def ref_n(sc):

@@ -45,9 +45,6 @@
 #ifndef S2D_FWD_MINB
 #define S2D_FWD_MINB 5
 #endif
-#ifndef S2D_FWD_LANE  // lane-private forward blending (measured: see DESIGN.md)
-#define S2D_FWD_LANE 0
-#endif
 #ifndef S2D_BWD_MINB
 #define S2D_BWD_MINB 4
 #endif
@@ -251,39 +248,6 @@ __device__ __forceinline__ float slot_maha(float2 fg, float2 lo, const float4 &q
     return __fmaf_rn(u, u, __fmul_rn(v, v));
 }
 
-// Conservative lane mask of a forward slot for the lane-private loop: bit l (pixel (l & 7, l >> 3)
-// of the 8x4 block) is set unless the pixel certainly has m > thr.  Per row, m is the quadratic
-// |(A, C) ex + t|^2 in ex = lx - f (t = (B, D) ey + lo, as slot_maha evaluates it), so the
-// pixels with m <= thr are an interval of lx; it is widened by 0.02 px plus a relative term,
-// and thr already exceeds the slot's cut + guard band, so every pixel whose float32 m passes
-// the loop's test is in the mask (a few extra pixels only cost a failed test).
-__device__ __forceinline__ uint32_t slot_lane_mask(const BlockCentre &bc, const float4 &q1, float thr) {
-    const float A = q1.x, C = q1.y, B = q1.z, D = q1.w;
-    const float alpha = fmaf(A, A, C * C);
-    if (!(alpha > 1e-30f && alpha < 1e30f)) return 0xffffffffu;
-    float ia;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ia) : "f"(alpha));
-    uint32_t lm = 0u;
-#pragma unroll
-    for (int ly = 0; ly < 4; ++ly) {
-        const float ey = __fsub_rn((float)ly, bc.g);
-        const float tB = fmaf(B, ey, bc.lo.x), tD = fmaf(D, ey, bc.lo.y);
-        const float beta = fmaf(A, tB, C * tD), gamma = fmaf(tB, tB, tD * tD);
-        const float gt = gamma - thr;
-        const float disc = fmaf(beta, beta, -alpha * gt);
-        const bool row = disc >= -1e-6f * (beta * beta + alpha * fabsf(gt));  // false for NaN
-        float sq;
-        asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sq) : "f"(fmaxf(disc, 0.f)));
-        const float c0 = fmaf(-beta, ia, bc.f), hw = sq * ia;
-        const float d = 0.02f + 1e-5f * fabsf(c0) + 1.01e-3f * hw;
-        const float x0 = fmaxf(c0 - hw - d, -1.f), x1 = fminf(c0 + hw + d, 8.f);
-        const int lo = max(0, __float2int_ru(x0)), hi = min(7, __float2int_rd(x1));
-        const uint32_t bits = lo <= hi ? ((0xFFu >> (7 - hi)) & (0xFFu << lo)) : 0u;
-        lm |= (row ? bits : 0u) << (8 * ly);
-    }
-    return lm;
-}
-
 // Cursor over list positions [lo, hi).  The current 32-wide chunk starts at `cb` (lane l holds
 // position cb + l); `pend` = the chunk's hits not yet handed out, `nxt` = the prefetched next
 // chunk (key, id).
@@ -391,10 +355,6 @@ __global__ void __launch_bounds__(kFwdWarps * 32, ((kArg || kMaxW || kNormal) ? 
     // affine mode: a terminated (or outside) lane carries lxy.x = NaN, so its m is NaN and fails
     // the cut test; no per-candidate `done` test is needed
     float2 lxy = make_float2(inside ? (float)(lane & 7) : kNaN, (float)(lane >> 3));
-    const float2 lxy0 = make_float2((float)(lane & 7), (float)(lane >> 3));
-    // the refine/render variants blend lane-privately; argmax / max-weight / ray keep the
-    // warp-uniform candidate loop (their per-candidate reductions need all lanes together)
-    constexpr bool kLane = S2D_FWD_LANE && !kArg && !kMaxW && !kRay;
     const int2 rg = a.ranges[tile];
 
     float T = 1.0f;
@@ -431,7 +391,6 @@ __global__ void __launch_bounds__(kFwdWarps * 32, ((kArg || kMaxW || kNormal) ? 
             // ellipse cull against the block (ray mode: the bbox bits only) and, for the kept
             // affine slots, the block-origin offset and cut thresholds (slot_prep comment above)
             bool keep = false;
-            uint32_t smask = 0u;  // lane-private loop: the slot's conservative pixel (lane) mask
             if (lane < n) {
                 Slot &sl = ring.s[buf][31 - lane];
                 if (kRay) {
@@ -454,7 +413,6 @@ __global__ void __launch_bounds__(kFwdWarps * 32, ((kArg || kMaxW || kNormal) ? 
                         sl.meta.y = __float_as_uint(slow ? -3.0e38f : tlo);
                         sl.meta.z = __float_as_uint(bc.lo.x);
                         sl.meta.w = __float_as_uint(bc.lo.y);
-                        if (kLane) smask = slow ? kFull : slot_lane_mask(bc, q1, thi + gb + 1e-3f);
                     }
                 }
             }
@@ -465,58 +423,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32, ((kArg || kMaxW || kNormal) ? 
             // per lane, bit 31 - j of bl_bits / cl_bits: this pixel blended list position j / with a
             // clamped weight; transposed into per-slot lane masks once per chunk
             uint32_t bl_bits = 0u, cl_bits = 0u;
-            if (kLane) {
-                // Lane-private blending: each pixel walks only the staged candidates whose
-                // conservative lane mask covers it (bit p = ring index p), in list order.  Every
-                // lane step is a (pixel, candidate) pair that very likely blends, instead of every
-                // lane running every candidate of the block (~22% of them blend at config 4).
-                // (the transpose is a warp collective: every lane runs it, done or not)
-                const uint32_t tm = __brev(transpose32(keep ? smask : 0u, lane)) & rm;
-                uint32_t mine = done ? 0u : tm;
-                // inactive lanes evaluate a staged slot (finite data) with w forced to 0
-                uint32_t kfill;
-                asm("bfind.u32 %0, %1;" : "=r"(kfill) : "r"(rm));
-                while (__any_sync(kFull, mine != 0u)) {
-                    const bool act = mine != 0u;
-                    uint32_t kb, bit;
-                    asm("bfind.u32 %0, %1;" : "=r"(kb) : "r"(mine));
-                    kb = act ? kb : kfill;
-                    bit = act ? (1u << kb) : 0u;
-                    mine ^= bit;
-                    const Slot &sl = ring.s[buf][kb];
-                    const float4 q0 = sl.r.q0, q1 = sl.r.q1;
-                    const uint4 mt = sl.meta;
-                    float u, v;
-                    const float m = slot_maha(make_float2(q0.x, q0.y),
-                                              make_float2(__uint_as_float(mt.z), __uint_as_float(mt.w)), q1, lxy0, u, v);
-                    const bool pass = act && m <= q0.z;
-                    float w = __fmul_rn(q0.w, fast_exp2(__fmul_rn(m, -0.72134752044448170368f)));
-                    w = pass ? w : 0.f;
-                    const bool slow = pass && m >= __uint_as_float(mt.y);
-                    if (__any_sync(kFull, slow)) {  // warp-uniform; lanes that are not slow keep w
-                        bool clamped = false;
-                        w = slow_weight(P, a, mt.x, q0.w, m, w, sl.r.q3.w, slow, px, py, clamped, guard);
-                        if (clamped) cl_bits |= bit;
-                    }
-                    // blend (blend_forward, _raster_kernels.py:47-55), a no-op where w = 0
-                    bl_bits |= w > 0.f ? bit : 0u;
-                    const float contrib = w * T;
-                    const float4 q2 = sl.r.q2;
-                    const float2 cc = make_float2(contrib, contrib);
-                    c01 = __ffma2_rn(cc, make_float2(q2.x, q2.y), c01);
-                    c2d = __ffma2_rn(cc, make_float2(q2.z, q2.w), c2d);
-                    if (kNormal) {
-                        const float4 q3 = sl.r.q3;
-                        n01 = __ffma2_rn(cc, make_float2(q3.x, q3.y), n01);
-                        n2 = fmaf(contrib, q3.z, n2);
-                    }
-                    T = fmaf(-w, T, T);  // T (1 - w), one rounding
-                    const bool term = T < term_t;
-                    done = done || term;
-                    mine = term ? 0u : mine;
-                }
-            }
-            while (!kLane && rm) {
+            while (rm) {
                 uint32_t kb, bit;  // ring index k = highest set bit of rm
                 asm("bfind.u32 %0, %1;" : "=r"(kb) : "r"(rm));
                 asm("shl.b32 %0, 1, %1;" : "=r"(bit) : "r"(kb));
@@ -648,7 +555,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32, ((kArg || kMaxW || kNormal) ? 
                 wc0 += __popc(b0);
                 wc1 += __popc(b1);
             }
-            if (__all_sync(kFull, (kRay || kLane) ? done : lxy.x != lxy.x)) break;
+            if (__all_sync(kFull, kRay ? done : lxy.x != lxy.x)) break;
             __syncwarp();  // slot `buf` is refilled by the next ring_fill
             buf ^= 1;
             n = nn;
