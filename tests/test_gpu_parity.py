@@ -390,3 +390,30 @@ def test_config2_seed_sweep_all_groups(seed):
         for f in ("colors", "opacities", "means", "quats", "scales"):
             ok, mx, l2 = gate(g[f], getattr(og, f))
             assert ok, (seed, kind, f, mx, l2)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2, 3])
+def test_depth_mask_count_matches_float64(seed):
+    """The MSE depth mask `accumulation > 0.5` (rasterizer.py:365-376): after the backward
+    (k_mask_fixup re-decides the pixels within the float32 error band in float64) the mask
+    count equals the float64 oracle's exactly, on scenes with many half-covered pixels
+    (opacities around 0.5)."""
+    sc = scenes.config2(seed)
+    s = sc.surfels
+    rng = np.random.default_rng(40 + seed)
+    op = np.asarray(s.opacities, np.float64)
+    op = np.float32(0.5) + (rng.random(len(op)) < 0.5) * np.float32(rng.normal(0, 0.02, len(op)))
+    s = SurfelArrays(s.means, s.quats, s.scales, np.asarray(op, np.float32).astype(np.float64), s.colors)
+    pose = sc.poses[0]
+    run = Run(s, pose, sc.intr, normal=False, argmax=False)
+    ref = O.render(s, pose, sc.intr)
+    trgb, tdep = far_targets(ref.color, ref.depth, np.random.default_rng(7))
+    g, loss = run.backward("mse", trgb, tdep, 1.0, 0.1, True)
+    st = run.view.stats()
+    near = int((np.abs(ref.accumulation - 0.5) < 1e-4).sum())
+    assert st.n_mask == int((ref.accumulation > 0.5).sum()), (st.n_mask, near)
+    oloss, og, _ = O.loss_and_grads(s, pose, sc.intr, trgb, tdep, "mse", 1.0, 0.1, mask_depth=True)
+    assert abs(loss - oloss) <= 1e-5 * abs(oloss)
+    for f in ("colors", "opacities", "means", "quats", "scales"):
+        ok, mx, l2 = gate(g[f], getattr(og, f))
+        assert ok, (f, mx, l2)
