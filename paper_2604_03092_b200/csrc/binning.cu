@@ -304,17 +304,19 @@ __global__ void S2D_SORT_BOUNDS k_onesweep(
     __shared__ uint32_t s_key[kSortTile], s_val[kSortTile];  // the tile regrouped by digit
     __shared__ int s_tile;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_tile = atomicAdd(ticket, 1);
-#pragma unroll
-    for (int w = 0; w < 8; ++w) s_wh[w][tid] = 0;
-    __syncthreads();
-    const int tile = s_tile;
     // n_host >= 0: a pass over n_host entries that skips sentinel keys (0xffffffff); every call
     // passes -1 (the *d_n entries).  The branch is kept on purpose: with it ptxas allocates 80
     // registers and no spills at 3 CTAs/SM; without it, 98 registers (2 CTAs/SM) or 16 B of
     // spills under the same bound, and every radix pass was 20-25% slower.
     const bool drop = n_host >= 0;
     const int n = drop ? n_host : *d_n;
+    // the grid is sized for the capacity: CTAs past the entries leave before taking a ticket
+    if ((int)blockIdx.x * kSortTile >= n) return;
+    if (tid == 0) s_tile = atomicAdd(ticket, 1);
+#pragma unroll
+    for (int w = 0; w < 8; ++w) s_wh[w][tid] = 0;
+    __syncthreads();
+    const int tile = s_tile;
     const int start = tile * kSortTile;
     if (start >= n) return;
     const int wbase = start + warp * 32 * kSortItems;
@@ -538,9 +540,13 @@ __global__ void __launch_bounds__(256) k_tie_fix(const uint32_t *__restrict__ ke
                                                  uint32_t *ctl, uint32_t *list, uint32_t *scratch) {
     __shared__ bool s_last;
     const int n = *d_n;
+    // the grid is sized for the capacity: CTAs past the drawn count leave at once (they take
+    // no ticket, so the last of the active ones runs tie_long)
+    const int active = (n + (int)blockDim.x - 1) / (int)blockDim.x;
+    if ((int)blockIdx.x >= active) return;
     tie_fix_at(keys, vals, z64, n, ctl, list, blockIdx.x * blockDim.x + threadIdx.x);
     __syncthreads();
-    if (threadIdx.x == 0) s_last = atomic_add_acq_rel(ctl + 2, 1u) == gridDim.x - 1;
+    if (threadIdx.x == 0) s_last = atomic_add_acq_rel(ctl + 2, 1u) == (uint32_t)active - 1;
     __syncthreads();
     if (!s_last) return;
     if (*reinterpret_cast<volatile uint32_t *>(ctl + 1) == 0u) return;  // no inversion in any long run
@@ -555,11 +561,13 @@ __global__ void S2D_EMIT_BOUNDS k_scan_emit(const EmitArgs a) {
     __shared__ uint32_t s_base;
     __shared__ uint32_t s_hist[2 * kRadix];
     const int tid = threadIdx.x;
+    const int nv = *a.d_v;
+    // the grid is sized for the capacity: CTAs past the drawn surfels leave before the ticket
+    if ((int)blockIdx.x * kEmitTile >= nv) return;
     if (tid == 0) s_tile = atomicAdd(a.ticket, 1);
     for (int k = tid; k < 2 * kRadix; k += 256) s_hist[k] = 0;
     __syncthreads();
     const int tile = s_tile;
-    const int nv = *a.d_v;
     const int start = tile * kEmitTile;
     if (start >= nv) return;
     const int r0 = start + tid * kEmitItems;

@@ -95,6 +95,13 @@ __device__ __forceinline__ void red_add_if(float *p, float v, bool c) {
         : "memory");
 }
 
+// bits |= bit where w > 0: one predicated OR (the select + OR the compiler emits otherwise)
+__device__ __forceinline__ void or_if_positive(uint32_t &bits, uint32_t bit, float w) {
+    asm("{\n\t.reg .pred p;\n\tsetp.gt.f32 p, %2, 0f00000000;\n\t@p or.b32 %0, %0, %1;\n\t}"
+        : "+r"(bits)
+        : "r"(bit), "f"(w));
+}
+
 __device__ __forceinline__ float fast_exp2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -486,7 +493,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32, ((kArg || kMaxW || kNormal) ? 
                         if (clamped) cl_bits |= bit;
                     }
                     {  // blend (blend_forward, _raster_kernels.py:47-55), a no-op where w = 0
-                        bl_bits |= w > 0.f ? bit : 0u;
+                        or_if_positive(bl_bits, bit, w);
                         contrib = w * T;
                         const float4 q2 = sl.r.q2;
                         const float2 cc = make_float2(contrib, contrib);
