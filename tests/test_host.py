@@ -120,3 +120,21 @@ def test_scene_generators_seeded_and_float32():
     c3 = scenes.config3(0)
     assert len(c3.surfels) == 512 * 384 and len(c3.poses) == 8
     assert np.all(np.asarray(c3.surfels.scales) > 0)
+
+
+def test_bench_spawns_n_ranks_outside_torchrun(monkeypatch):
+    """`python bench.py --gpus N` outside torchrun re-launches itself under torch.distributed.run
+    with N ranks on one node and a 127.0.0.1 rendezvous (the driver's launch line)."""
+    import subprocess
+    import sys
+    import bench
+    calls = []
+    monkeypatch.setattr(subprocess, "call", lambda cmd: calls.append(cmd) or 0)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "3", "--warmup", "3"])
+    monkeypatch.delenv("RANK", raising=False)
+    args = bench.parse()
+    assert bench.spawn_ranks(args) == 0
+    cmd = calls[0]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"]
+    assert "--nproc-per-node=4" in cmd and "--nnodes=1" in cmd and "--master-addr=127.0.0.1" in cmd
+    assert cmd[-6:] == ["--gpus", "4", "--steps", "3", "--warmup", "3"]
