@@ -140,7 +140,7 @@ def render_targets(sc, device):
 def phase_bytes(n, v, p, x, e):
     return {
         "project": 52 * n + n + 128 * v,           # params in; flags out; drawn keys/vals 8, record 64, exact 40, rect 8, z64 8
-        "depth_sort": 60 * v,                       # hist (rebase in place) + 3 stable passes over the drawn keys/vals, tie fix
+        "depth_sort": 68 * v,                       # compaction + rebase + hist (16), 3 stable passes (48), tie fix (4)
         "tile_bin": 12 * v + 44 * p,                # order+rect in; pairs out; 2 stable passes; tile ranges
         "raster_fwd": 72 * p + 16 * e + 28 * x,     # key+id+record per pair; blend stream out; rgb, depth, acc, aux out
         "raster_bwd": 16 * e + 64 * p + 40 * x + 40 * v,  # stream + records; aux, render, targets; 2D gradients
