@@ -144,6 +144,8 @@ def phase_bytes(n, v, p, x, e):
         "tile_bin": 12 * v + 44 * p,                # order+rect in; pairs out; 2 stable passes; tile ranges
         "raster_fwd": 72 * p + 16 * e + 28 * x,     # key+id+record per pair; blend stream out; rgb, depth, acc, aux out
         "raster_bwd": 16 * e + 64 * p + 40 * x + 40 * v,  # stream + records; aux, render, targets; 2D gradients
+        # forward + backward in one kernel: both minus the image round trip (targets in only)
+        "raster_fused": 136 * p + 32 * e + 16 * x + 40 * v,
         "project_bwd": n + 260 * v,                 # flags; 2D grads in + zeroed; params in; gradients r+w
     }
 
@@ -158,7 +160,7 @@ def load_traffic():
 
 
 KERNEL_OF_PHASE = {"raster_fwd": "k_raster_fwd", "raster_bwd": "k_raster_bwd", "project": "k_project",
-                   "project_bwd": "k_project_bwd"}
+                   "project_bwd": "k_project_bwd", "raster_fused": "k_raster_fused"}
 
 
 def run_cpu_port(sc, targets, views, threads):
@@ -337,8 +339,9 @@ def main():
     # ---- device-resident run (value) ----
     inflight = int(os.environ.get("S2D_INFLIGHT", "16"))
     graph = os.environ.get("S2D_GRAPH", "1") == "1"
+    fused = os.environ.get("S2D_FUSED", "1") == "1"  # one raster kernel per view (s2d_forward_backward)
     ref = AdamRefiner(sc.extra["perturbed"], sc.intr, sc.poses, rgbs, deps, loss, AdamConfig(), device=dev,
-                      inflight=inflight, cuda_graph=graph)
+                      inflight=inflight, cuda_graph=graph, fused=fused)
     for _ in range(args.warmup):
         ref.step(sync=False)
     ref.losses()
@@ -392,6 +395,9 @@ def main():
     st = ref.view.stats()
     nfw = max(ph["n_forward"], 1)
     per_launch_ms = {k: ph[k] / nfw for k in ref.view.PHASES}
+    if ref.fused:  # the fused kernel is timed in the raster_fwd slot
+        per_launch_ms["raster_fused"] = per_launch_ms.pop("raster_fwd")
+        per_launch_ms.pop("raster_bwd")
     nvis, npairs, nblend = st.visible, st.pairs, st.blended
     pb = phase_bytes(ref.n, nvis, npairs, px, nblend)
     peaks = {}
@@ -423,7 +429,7 @@ def main():
     del ref
     torch.cuda.empty_cache()
     ref2 = AdamRefiner(sc.extra["perturbed"], sc.intr, sc.poses, host_rgb, host_dep, loss, AdamConfig(), device=dev,
-                       host_targets=True, inflight=inflight, cuda_graph=graph)
+                       host_targets=True, inflight=inflight, cuda_graph=graph, fused=fused)
     for _ in range(args.warmup):
         ref2.step(sync=False)
     ref2.losses()
@@ -488,6 +494,7 @@ def main():
             "refine_iters_per_s": round(1000.0 / ms_step, 3),
             "fwd_bwd_mpix_per_s_per_view": round(px / (view_ms * 1e-3) / 1e6, 2) if view_ms > 0 else None,
             "views_in_flight": inflight,
+            "raster_path": "fused forward+backward kernel" if fused else "forward and backward kernels",
             "loss_first_last": [losses[0], losses[-1]],
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm,
                          "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": traffic,
@@ -523,7 +530,7 @@ def issue_roofline(traffic_src, per_launch_ms, clk):
     peak = 148 * 4 * mhz * 1e6  # warp instructions per second
     out = {"unit": "warp-instr/s", "peak": peak, "peak_source": f"148 SMs x 4 schedulers x {mhz:.0f} MHz",
            "source": traffic_src.get("source")}
-    for phase in ("raster_fwd", "raster_bwd"):
+    for phase in ("raster_fwd", "raster_bwd", "raster_fused"):
         k = traffic_src.get("per_launch", {}).get(KERNEL_OF_PHASE[phase], {})
         wi = k.get("warp_instructions")
         if wi and per_launch_ms.get(phase):

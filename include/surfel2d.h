@@ -205,6 +205,23 @@ int s2d_backward(s2d_view *view, void *stream, const float *params, int64_t n,
                  const s2d_image *image, const s2d_loss *loss, float *grads, double *loss_accum);
 
 /*
+ * s2d_forward + s2d_backward in one call for the losses that need no whole-image
+ * reduction before their seeds: L1 without the depth mask, and MSE with w_depth = 0
+ * (rasterizer.py:360-380).  The compositing and the reverse traversal run in one kernel, each
+ * warp back-propagating its pixel block right after rendering it (no image round trip).
+ * `out` (nullable) receives color / depth / accumulation where those fields are non-NULL
+ * (normal / max_w / arg_w are not rendered on this path); `wait_event`
+ * (cudaEvent_t, nullable) is waited for before the loss targets are read, e.g. their
+ * upload.  Any other loss falls back to s2d_forward + s2d_backward with `out`, which must
+ * then be complete.  ACCUMULATES into grads like s2d_backward.  The view's forward state is
+ * consumed: run s2d_forward again before an s2d_backward.
+ */
+int s2d_forward_backward(s2d_view *view, void *stream, const float *params, int64_t n,
+                         const double pose_c2w[8], const s2d_camera *cam, const s2d_raster_config *cfg,
+                         const s2d_image *out, const s2d_loss *loss, float *grads, double *loss_accum,
+                         void *wait_event);
+
+/*
  * Fused Adam step + post-step projection on the packed parameter block
  * (replaces the GD update of mapper.py:330-335; D5): m1, m2 are packed 13*n
  * moments.  step is 1-based.  mask (n uint8, nullable) restricts the update

@@ -105,6 +105,9 @@ _SIGNATURES = {
                                    ctypes.POINTER(Image), c_p, c_p, c_p]),
     "s2d_backward": (ctypes.c_int, [c_p, c_p, c_p, ctypes.c_int64, ctypes.POINTER(Image),
                                     ctypes.POINTER(Loss), c_p, c_p]),
+    "s2d_forward_backward": (ctypes.c_int, [c_p, c_p, c_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_double),
+                                            ctypes.POINTER(Camera), ctypes.POINTER(RasterCfg),
+                                            ctypes.POINTER(Image), ctypes.POINTER(Loss), c_p, c_p, c_p]),
     "s2d_adam_step": (ctypes.c_int, [c_p, c_p, c_p, c_p, c_p, ctypes.c_int64, ctypes.c_int64,
                                      ctypes.POINTER(AdamCfg), c_p]),
     "s2d_adam_step_gated": (ctypes.c_int, [c_p, c_p, c_p, c_p, c_p, ctypes.c_int64, ctypes.c_int64,

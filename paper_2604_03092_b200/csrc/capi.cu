@@ -214,9 +214,9 @@ struct s2d_view {
     cudaStream_t last_stream = nullptr;
     // phase timing (events recorded between kernels, resolved in s2d_view_timing)
     struct TimedCall {
-        cudaEvent_t e[5];
+        cudaEvent_t e[6];
         int n;
-        int kind;  // 0 forward, 1 backward
+        int kind;  // 0 forward, 1 backward, 2 fused forward + backward
     };
     bool timing = false;
     std::vector<TimedCall> timed;
@@ -313,9 +313,17 @@ int ensure_capacity(s2d_view *v, int64_t n, int64_t npx, int ntiles) {
     return layout_sync(v, nn, v->pcap, ntiles);
 }
 
+// The loss of a fused forward + backward (s2d_forward_backward)
+struct FusedLoss {
+    const s2d_loss *loss;
+    float *grads;
+    double *loss_accum;
+    cudaEvent_t wait;
+};
+
 int view_forward(s2d_view *v, cudaStream_t s, const float *params, int64_t n, const double pose[8],
                  const s2d_camera *cam, const s2d_raster_config *cfg, const s2d_image *out,
-                 float *max_all, float *max_marked, const uint8_t *mask) {
+                 float *max_all, float *max_marked, const uint8_t *mask, const FusedLoss *fl = nullptr) {
     int rc = validate_camera(cam);
     if (rc) return rc;
     if (!cfg) return fail(S2D_ERR_INVALID, "raster config is NULL");
@@ -335,9 +343,9 @@ int view_forward(s2d_view *v, cudaStream_t s, const float *params, int64_t n, co
     v->has_fwd = false;
     S2D_CUDA(cudaMemsetAsync(v->sync, 0, v->sr.bytes, s));
     s2d_view::TimedCall tc{};
-    tc.kind = 0;
+    tc.kind = fl ? 2 : 0;
     auto mark = [&]() {
-        if (v->timing && tc.n < 5) {
+        if (v->timing && tc.n < 6) {
             tc.e[tc.n] = v->take_event();
             cudaEventRecord(tc.e[tc.n++], s);
         }
@@ -444,13 +452,40 @@ int view_forward(s2d_view *v, cudaStream_t s, const float *params, int64_t n, co
     ra.stats = sr.stats;
     ra.amb_count = sr.amb_count;
     ra.amb_list = v->amb;
-    launch_raster_forward(ra, s);
-    S2D_CHECK_LAUNCH();
-    mark();
+    if (fl) {
+        ra.loss_kind = fl->loss->kind;
+        ra.depth_mask = fl->loss->depth_mask;
+        ra.w_rgb = fl->loss->w_rgb;
+        ra.w_depth = fl->loss->w_depth;
+        ra.target_rgb = fl->loss->target_rgb;
+        ra.target_depth = fl->loss->target_depth;
+        ra.grad2d = v->grad2d;
+        ra.loss_accum = fl->loss_accum;
+        if (fl->wait) S2D_CUDA(cudaStreamWaitEvent(s, fl->wait, 0));
+        launch_raster_fused(ra, s);
+        S2D_CHECK_LAUNCH();
+        mark();
+        if (n > 0) {
+            ProjectBwdArgs pb;
+            pb.P = P;
+            pb.params = params;
+            pb.flags = v->flags;
+            pb.rect = v->rect;
+            pb.grad2d = v->grad2d;
+            pb.grads = fl->grads;
+            launch_project_backward(pb, s);
+            S2D_CHECK_LAUNCH();
+        }
+        mark();
+    } else {
+        launch_raster_forward(ra, s);
+        S2D_CHECK_LAUNCH();
+        mark();
+    }
     if (v->timing) v->timed.push_back(tc);
     v->P = P;
     v->n = n;
-    v->has_fwd = true;
+    v->has_fwd = fl == nullptr;
     v->last_stream = s;
     return S2D_OK;
 }
@@ -560,11 +595,12 @@ int s2d_view_timing(s2d_view *v, double out[8], int32_t reset) {
         for (int k = 0; k + 1 < tc.n; ++k) {
             float ms = 0.f;
             S2D_CUDA(cudaEventElapsedTime(&ms, tc.e[k], tc.e[k + 1]));
-            const int phase = tc.kind == 0 ? k : 4 + k;
+            // fused: project, sort, binning, raster (fused, as phase 3), projection backward
+            const int phase = tc.kind == 0 ? k : tc.kind == 1 ? 4 + k : (k < 4 ? k : 5);
             if (phase < 6) v->phase_ms[phase] += ms;
         }
-        if (tc.kind == 0) v->n_fwd_timed++;
-        else v->n_bwd_timed++;
+        if (tc.kind != 1) v->n_fwd_timed++;
+        if (tc.kind != 0) v->n_bwd_timed++;
         for (int k = 0; k < tc.n; ++k) v->free_events.push_back(tc.e[k]);
     }
     v->timed.clear();
@@ -610,7 +646,7 @@ int s2d_backward(s2d_view *v, void *stream, const float *params, int64_t n, cons
     s2d_view::TimedCall tc{};
     tc.kind = 1;
     auto mark = [&]() {
-        if (v->timing && tc.n < 5) {
+        if (v->timing && tc.n < 6) {
             tc.e[tc.n] = v->take_event();
             cudaEventRecord(tc.e[tc.n++], s);
         }
@@ -670,6 +706,28 @@ int s2d_backward(s2d_view *v, void *stream, const float *params, int64_t n, cons
     if (v->timing) v->timed.push_back(tc);
     v->last_stream = s;
     return S2D_OK;
+}
+
+int s2d_forward_backward(s2d_view *v, void *stream, const float *params, int64_t n, const double pose_c2w[8],
+                         const s2d_camera *cam, const s2d_raster_config *cfg, const s2d_image *out,
+                         const s2d_loss *loss, float *grads, double *loss_accum, void *wait_event) {
+    if (!v || !loss) return fail(S2D_ERR_INVALID, "NULL argument");
+    if (n > 0 && !grads) return fail(S2D_ERR_INVALID, "grads is NULL");
+    const bool fusable = (loss->kind == S2D_LOSS_L1 && !loss->depth_mask) ||
+                         (loss->kind == S2D_LOSS_MSE && loss->w_depth == 0.0);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!fusable) {
+        // the seeds need the whole image's depth-mask count first: two kernels
+        int rc = view_forward(v, s, params, n, pose_c2w, cam, cfg, out, nullptr, nullptr, nullptr);
+        if (rc) return rc;
+        if (wait_event) S2D_CUDA(cudaStreamWaitEvent(s, (cudaEvent_t)wait_event, 0));
+        return s2d_backward(v, stream, params, n, out, loss, grads, loss_accum);
+    }
+    if (!loss->target_rgb || !loss->target_depth) return fail(S2D_ERR_INVALID, "loss targets are NULL");
+    s2d_image none;
+    memset(&none, 0, sizeof(none));
+    const FusedLoss fl{loss, grads, loss_accum, (cudaEvent_t)wait_event};
+    return view_forward(v, s, params, n, pose_c2w, cam, cfg, out ? out : &none, nullptr, nullptr, nullptr, &fl);
 }
 
 int s2d_adam_step(void *stream, float *params, const float *grads, float *m1, float *m2, int64_t n,

@@ -342,11 +342,59 @@ __device__ __forceinline__ int stream_fill(WarpRing &rg, int buf, const uint4 *w
     return n;
 }
 
-// The plain variant (the refine path) fits 48 registers, 5 CTAs/SM: besides its own latency
-// hiding, a smaller footprint lets it share SMs with the other views' kernels in flight.
-template <bool kArg, bool kMaxW, bool kNormal, bool kRay>
-__global__ void __launch_bounds__(kFwdWarps * 32, ((kArg || kMaxW || kNormal) ? 4 : S2D_FWD_MINB) * 8 / kFwdWarps)
-    k_raster_fwd(const RasterArgs a) {
+__device__ __forceinline__ float sgnf(float x) { return x > 0.f ? 1.f : (x < 0.f ? -1.f : 0.f); }
+
+// Per-pixel loss seeds dL/d(rgb, depth) and the pixel's loss term for the MSE
+// (rasterizer.py:375-380) and L1 losses, from the residuals e = rendered - target; `masked` /
+// `nm`: the pixel's depth-mask decision and the image's mask count (unused by the losses
+// without a depth mask), npx = W H.
+__device__ __forceinline__ void loss_seeds(const RasterArgs &a, float e0, float e1, float e2, float ed, bool masked,
+                                           int nm, double npx, float &gc0, float &gc1, float &gc2, float &gd,
+                                           float &lpx) {
+    if (a.loss_kind == S2D_LOSS_MSE) {
+        const float k = (float)(a.w_rgb * (2.0 / (3.0 * npx)));
+        gc0 = k * e0;
+        gc1 = k * e1;
+        gc2 = k * e2;
+        lpx = (float)(a.w_rgb / (3.0 * npx)) * (e0 * e0 + e1 * e1 + e2 * e2);
+        if (a.w_depth != 0.0 && nm > 0 && masked) {
+            gd = (float)(a.w_depth * (2.0 / nm)) * ed;
+            lpx += (float)(a.w_depth / nm) * ed * ed;
+        }
+    } else {  // L1
+        const float k = (float)(a.w_rgb / (3.0 * npx));
+        gc0 = k * sgnf(e0);
+        gc1 = k * sgnf(e1);
+        gc2 = k * sgnf(e2);
+        lpx = k * (fabsf(e0) + fabsf(e1) + fabsf(e2));
+        const bool use = a.depth_mask ? masked : true;
+        const double nd = a.depth_mask ? (double)nm : npx;
+        if (use && nd > 0.0) {
+            const float kd = (float)(a.w_depth / nd);
+            gd = kd * sgnf(ed);
+            lpx += kd * fabsf(ed);
+        }
+    }
+}
+
+// The reverse traversal of one warp block (k_raster_bwd below; also run by the fused
+// forward + backward right after its forward)
+template <bool kExt, bool kRay>
+__device__ __forceinline__ void bwd_traverse(const RasterArgs &a, WarpRing &ring, int tile, int warp, int lane,
+                                             int wx0, int wy0, float gc0, float gc1, float gc2, float gd, float gn0,
+                                             float gn1, float gn2, float ga, float Tn, int cnt0, int cnt1);
+
+#ifndef S2D_BWD_CTAS_PER_SM
+#define S2D_BWD_CTAS_PER_SM (S2D_BWD_MINB * 8 / kBwdWarps)
+#endif
+
+// Forward compositing of one warp block (k_raster_fwd).  kFused (k_raster_fused,
+// s2d_forward_backward, losses without the whole-image depth mask): each warp then seeds the
+// loss from its pixels' final state and runs the backward's reverse traversal over the blend
+// streams it just wrote (bwd_traverse).
+template <bool kArg, bool kMaxW, bool kNormal, bool kRay, bool kFused>
+__device__ __forceinline__ void raster_fwd_body(const RasterArgs &a) {
+    static_assert(!kFused || !(kArg || kMaxW || kNormal), "the fused variant renders colour and depth only");
     __shared__ WarpRing s_ring[kFwdWarps];
     const ViewParams &P = a.P;
     const int tile = blockIdx.x / (8 / kFwdWarps);
@@ -569,6 +617,45 @@ __global__ void __launch_bounds__(kFwdWarps * 32, ((kArg || kMaxW || kNormal) ? 
         }
         cp_wait<0>();
     }
+    if constexpr (kFused) {
+        if (lane == 0 && wc0 + wc1) atomicAdd(&a.stats->blended, wc0 + wc1);
+        float gc0 = 0.f, gc1 = 0.f, gc2 = 0.f, gd = 0.f, lpx = 0.f;
+        if (inside) {
+            const int p = py * P.W + px;
+            if (a.color) {  // the image outputs are optional here
+                a.color[3 * p] = c01.x;
+                a.color[3 * p + 1] = c01.y;
+                a.color[3 * p + 2] = c2d.x;
+            }
+            if (a.depth) a.depth[p] = c2d.y;
+            if (a.accum) a.accum[p] = 1.0f - T;
+            const float e0 = c01.x - a.target_rgb[3 * p];
+            const float e1 = c01.y - a.target_rgb[3 * p + 1];
+            const float e2 = c2d.x - a.target_rgb[3 * p + 2];
+            const float ed = c2d.y - a.target_depth[p];
+            loss_seeds(a, e0, e1, e2, ed, false, 0, (double)P.W * (double)P.H, gc0, gc1, gc2, gd, lpx);
+        }
+        const int nm = __popc(__ballot_sync(kFull, inside && (1.0f - T) > 0.5f));
+        int gsum = guard;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            gsum += __shfl_xor_sync(kFull, gsum, o);
+            lpx += __shfl_xor_sync(kFull, lpx, o);
+        }
+        if (lane == 0) {
+            if (gsum) atomicAdd(&a.stats->guard_hits, gsum);
+            if (nm) atomicAdd(&a.stats->n_mask, nm);
+            if (lpx != 0.f && a.loss_accum) atomicAdd(a.loss_accum, (double)lpx);
+        }
+        if (wc0 + wc1 == 0) return;  // warp-uniform
+        // the blend streams were written by this warp's lanes and are staged (cp.async, L2)
+        // by other lanes of it: release them at GPU scope before the warp barrier
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        __syncwarp();
+        bwd_traverse<false, kRay>(a, ring, tile, warp, lane, wx0, wy0, gc0, gc1, gc2, gd, 0.f, 0.f, 0.f, 0.f, T, wc0,
+                                  wc1);
+        return;
+    }
     if (lane == 0) {
         a.bcount[16 * tile + 2 * warp] = wc0;
         a.bcount[16 * tile + 2 * warp + 1] = wc1;
@@ -606,6 +693,20 @@ __global__ void __launch_bounds__(kFwdWarps * 32, ((kArg || kMaxW || kNormal) ? 
     for (int o = 16; o > 0; o >>= 1) gsum += __shfl_xor_sync(kFull, gsum, o);
     if (lane == 0 && gsum) atomicAdd(&a.stats->guard_hits, gsum);
     if (lane == 0 && nm) atomicAdd(&a.stats->n_mask, nm);
+}
+
+// The plain variant (the refine path) fits 48 registers, 5 CTAs/SM: besides its own latency
+// hiding, a smaller footprint lets it share SMs with the other views' kernels in flight.
+template <bool kArg, bool kMaxW, bool kNormal, bool kRay>
+__global__ void __launch_bounds__(kFwdWarps * 32, ((kArg || kMaxW || kNormal) ? 4 : S2D_FWD_MINB) * 8 / kFwdWarps)
+    k_raster_fwd(const RasterArgs a) {
+    raster_fwd_body<kArg, kMaxW, kNormal, kRay, false>(a);
+}
+
+// The fused variant runs with the backward's register budget (64, 8 CTAs/SM)
+template <bool kRay>
+__global__ void __launch_bounds__(kFwdWarps * 32, S2D_BWD_CTAS_PER_SM) k_raster_fused(const RasterArgs a) {
+    raster_fwd_body<false, false, false, kRay, true>(a);
 }
 
 // Transposed warp reduction of C per-lane values (C <= 32): at each butterfly stage the
@@ -685,12 +786,7 @@ __device__ __forceinline__ void red_map(int lane, int (&vi)[RF], bool (&own)[RF]
     }
 }
 
-__device__ __forceinline__ float sgnf(float x) { return x > 0.f ? 1.f : (x < 0.f ? -1.f : 0.f); }
-
 template <bool kExt, bool kRay>  // kExt: normal / accumulation seeds present (external loss)
-#ifndef S2D_BWD_CTAS_PER_SM
-#define S2D_BWD_CTAS_PER_SM (S2D_BWD_MINB * 8 / kBwdWarps)
-#endif
 __global__ void __launch_bounds__(kBwdWarps * 32, S2D_BWD_CTAS_PER_SM) k_raster_bwd(const RasterArgs a) {
     __shared__ WarpRing s_ring[kBwdWarps];
     __shared__ float s_loss[kBwdWarps];
@@ -702,9 +798,6 @@ __global__ void __launch_bounds__(kBwdWarps * 32, S2D_BWD_CTAS_PER_SM) k_raster_
     const int wx0 = tx * kTile + (warp & 1) * 8, wy0 = ty * kTile + (warp >> 1) * 4;
     const int px = wx0 + (lane & 7), py = wy0 + (lane >> 3);
     const bool inside = px < P.W && py < P.H;
-    const float pxf = (float)px, pyf = (float)py;
-    const float2 lxy = make_float2((float)(lane & 7), (float)(lane >> 3));
-    const int2 rg = a.ranges[tile];
     const int p = py * P.W + px;
 
     // ---- loss seeds (rasterizer.py:375-380 for MSE; L1; external) ----
@@ -736,30 +829,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, S2D_BWD_CTAS_PER_SM) k_raster_
             const int nm = a.stats->n_mask;
             // aux.x bit 30: the mask was re-decided in float64 (k_mask_fixup), value in bit 29
             const bool masked = (ax.x & (1 << 30)) ? ((ax.x >> 29) & 1) != 0 : a.accum[p] > 0.5f;
-            if (a.loss_kind == S2D_LOSS_MSE) {
-                const float k = (float)(a.w_rgb * (2.0 / (3.0 * npx)));
-                gc0 = k * e0;
-                gc1 = k * e1;
-                gc2 = k * e2;
-                lpx = (float)(a.w_rgb / (3.0 * npx)) * (e0 * e0 + e1 * e1 + e2 * e2);
-                if (a.w_depth != 0.0 && nm > 0 && masked) {
-                    gd = (float)(a.w_depth * (2.0 / nm)) * ed;
-                    lpx += (float)(a.w_depth / nm) * ed * ed;
-                }
-            } else {  // L1
-                const float k = (float)(a.w_rgb / (3.0 * npx));
-                gc0 = k * sgnf(e0);
-                gc1 = k * sgnf(e1);
-                gc2 = k * sgnf(e2);
-                lpx = k * (fabsf(e0) + fabsf(e1) + fabsf(e2));
-                const bool use = a.depth_mask ? masked : true;
-                const double nd = a.depth_mask ? (double)nm : npx;
-                if (use && nd > 0.0) {
-                    const float kd = (float)(a.w_depth / nd);
-                    gd = kd * sgnf(ed);
-                    lpx += kd * fabsf(ed);
-                }
-            }
+            loss_seeds(a, e0, e1, e2, ed, masked, nm, npx, gc0, gc1, gc2, gd, lpx);
         }
     }
     // loss: block reduction (the kernel's only barrier)
@@ -775,9 +845,22 @@ __global__ void __launch_bounds__(kBwdWarps * 32, S2D_BWD_CTAS_PER_SM) k_raster_
         for (int w = 0; w < kBwdWarps; ++w) l += s_loss[w];
         if (l != 0.f) atomicAdd(a.loss_accum, (double)l);
     }
-    const int half = (lane >> 2) & 1;  // column half of the block (lane bit 2)
     const int cnt0 = a.bcount[16 * tile + 2 * warp], cnt1 = a.bcount[16 * tile + 2 * warp + 1];
     if (cnt0 + cnt1 == 0) return;  // no pixel of this warp's block blended anything (warp-uniform)
+    bwd_traverse<kExt, kRay>(a, s_ring[tid >> 5], tile, warp, lane, wx0, wy0, gc0, gc1, gc2, gd, gn0, gn1, gn2, ga,
+                             Tn, cnt0, cnt1);
+}
+
+template <bool kExt, bool kRay>
+__device__ __forceinline__ void bwd_traverse(const RasterArgs &a, WarpRing &ring, int tile, int warp, int lane,
+                                             int wx0, int wy0, float gc0, float gc1, float gc2, float gd, float gn0,
+                                             float gn1, float gn2, float ga, float Tn, int cnt0, int cnt1) {
+    const ViewParams &P = a.P;
+    const int px = wx0 + (lane & 7), py = wy0 + (lane >> 3);
+    const float pxf = (float)px, pyf = (float)py;
+    const float2 lxy = make_float2((float)(lane & 7), (float)(lane >> 3));
+    const int2 rg = a.ranges[tile];
+    const int half = (lane >> 2) & 1;  // column half of the block (lane bit 2)
 
     // ---- reverse traversal of the pairs this warp's pixels blended ----
     // Per pair, only the lanes in the forward's lane mask work (no cut / guard-band tests);
@@ -803,7 +886,6 @@ __global__ void __launch_bounds__(kBwdWarps * 32, S2D_BWD_CTAS_PER_SM) k_raster_
     float2 S01 = make_float2(0.f, 0.f), S2d = make_float2(0.f, 0.f);
     float Sn0 = 0.f, Sn1 = 0.f, Sn2 = 0.f;
     const float2 gc01 = make_float2(gc0, gc1), gc2d = make_float2(gc2, gd);
-    WarpRing &ring = s_ring[tid >> 5];
     // this lane's half stream; each half stages up to 16 entries per ring buffer, at ring
     // indices 2 j + half (j-th newest), lane position j in the half = jh
     const uint4 *ws = a.bstream + 16 * (size_t)rg.x + (size_t)(2 * warp + half) * (size_t)(rg.y - rg.x);
@@ -1073,6 +1155,13 @@ void launch_raster_forward(const RasterArgs &a, cudaStream_t s) {
 template <bool kExt, bool kRay>
 static void bwd_launch(const RasterArgs &a, int tiles, cudaStream_t s) {
     k_raster_bwd<kExt, kRay><<<tiles * (8 / kBwdWarps), kBwdWarps * 32, 0, s>>>(a);
+}
+
+void launch_raster_fused(const RasterArgs &a, cudaStream_t s) {
+    const int grid = a.P.ntx * a.P.nty * (8 / kFwdWarps);
+    count_launch();
+    if (a.P.mode == S2D_SPLAT_RAY) k_raster_fused<true><<<grid, kFwdWarps * 32, 0, s>>>(a);
+    else k_raster_fused<false><<<grid, kFwdWarps * 32, 0, s>>>(a);
 }
 
 void launch_raster_backward(const RasterArgs &a, cudaStream_t s) {

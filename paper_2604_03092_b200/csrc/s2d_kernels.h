@@ -138,6 +138,9 @@ struct RasterArgs {
 };
 void launch_raster_forward(const RasterArgs &a, cudaStream_t s);
 void launch_raster_backward(const RasterArgs &a, cudaStream_t s);
+// forward + loss seeds + backward traversal in one kernel (colour/depth losses without the
+// whole-image depth mask); needs a.target_rgb / a.target_depth / a.grad2d
+void launch_raster_fused(const RasterArgs &a, cudaStream_t s);
 // float64 re-decision of the ambiguous depth-mask pixels (before a masked loss's backward)
 void launch_mask_fixup(const RasterArgs &a, cudaStream_t s);
 

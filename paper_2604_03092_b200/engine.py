@@ -181,6 +181,22 @@ class View:
                                      ctypes.byref(img), ctypes.byref(loss), N.dptr(grads),
                                      N.dptr(loss_accum)), "s2d_backward")
 
+    def forward_backward(self, params: torch.Tensor, n: int, pose, cam: N.Camera, cfg: N.RasterCfg,
+                         image: ImageBuffers | None, loss: N.Loss, grads: torch.Tensor,
+                         loss_accum: torch.Tensor | None = None, stream=None, wait_event=None):
+        """s2d_forward_backward: render + loss + backward in one raster kernel for the losses
+        without the whole-image depth mask (else forward then backward).  `image` may be None
+        on the fused path; `wait_event` (torch.cuda.Event) is waited for before the loss
+        targets are read."""
+        pose8 = N.as_doubles(as_packed_pose(pose))
+        img = image.struct() if image is not None else None
+        ev = ctypes.c_void_p(wait_event.cuda_event) if wait_event is not None else None
+        N.check(N.lib().s2d_forward_backward(self.handle, self._stream(stream), N.dptr(params), int(n), pose8,
+                                             ctypes.byref(cam), ctypes.byref(cfg),
+                                             ctypes.byref(img) if img is not None else None, ctypes.byref(loss),
+                                             N.dptr(grads), N.dptr(loss_accum), ev), "s2d_forward_backward")
+        self._last = (int(n), int(cam.height), int(cam.width))
+
     def stats(self) -> N.ViewStats:
         st = N.ViewStats()
         N.check(N.lib().s2d_view_stats_host(self.handle, ctypes.byref(st)), "s2d_view_stats_host")

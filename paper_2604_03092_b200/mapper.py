@@ -357,6 +357,10 @@ class ViewLoss:
     def code(self) -> int:
         return {"l1": N.LOSS_L1, "mse": N.LOSS_MSE}[self.kind]
 
+    def fusable(self) -> bool:
+        """The seeds need no whole-image reduction (s2d_forward_backward's one-kernel path)."""
+        return (self.kind == "l1" and not self.depth_mask) or (self.kind == "mse" and self.w_depth == 0.0)
+
 
 class _Lane:
     """One stream's worth of view state: workspace and render buffers."""
@@ -394,7 +398,7 @@ class AdamRefiner:
                  loss: ViewLoss = ViewLoss(), adam: AdamConfig = AdamConfig(),
                  raster_cfg: RasterConfig = DEFAULT_RASTER_CONFIG, mask=None, group=None, device=None,
                  host_targets: bool = False, inflight: int = 16, shard_optimizer: bool | None = None,
-                 cuda_graph: bool = False):
+                 cuda_graph: bool = False, fused: bool = True):
         self.ctx = DeviceContext.get(device)
         self.dev = self.ctx.device
         self.group = group
@@ -425,6 +429,8 @@ class AdamRefiner:
         self.all_poses = [as_packed_pose(p) for p in poses]
         self.my_views = shard_views(len(self.all_poses), self.rank, self.world_size)
         self.loss_cfg = loss
+        # forward, loss and backward of a view in one raster kernel where the loss allows it
+        self.fused = bool(fused) and loss.fusable()
         self.adam = adam.struct()
         self.host_targets = host_targets
         h, w = intr.height, intr.width
@@ -510,16 +516,23 @@ class AdamRefiner:
         for j, v in enumerate(self.my_views):
             lane = lanes[j % len(lanes)]
             s = lane.stream
+            if self.host_targets:
+                trgb, tdep = self.dev_rgb[v], self.dev_depth[v]
+            else:
+                trgb, tdep = self.rgb[v], self.depth[v]
+            ls = loss_struct(lc.code(), lc.w_rgb, lc.w_depth, lc.depth_mask, trgb, tdep)
+            if self.fused:
+                # the raster kernel waits for this view's target upload, the projection and
+                # sorts before it do not
+                lane.view.forward_backward(self.params, self.n, self.all_poses[v], self.cam, self.cfg, None, ls,
+                                           self.grads, self.loss_acc, stream=s, wait_event=copied.get(v))
+                lane.view.accumulate_stats(self.stats_acc, stream=s)
+                continue
             lane.view.forward(self.params, self.n, self.all_poses[v], self.cam, self.cfg, lane.img, stream=s)
             lane.view.accumulate_stats(self.stats_acc, stream=s)
             if self.host_targets:
                 s.wait_event(copied[v])
-                trgb, tdep = self.dev_rgb[v], self.dev_depth[v]
-            else:
-                trgb, tdep = self.rgb[v], self.depth[v]
-            lane.view.backward(self.params, self.n, lane.img,
-                               loss_struct(lc.code(), lc.w_rgb, lc.w_depth, lc.depth_mask, trgb, tdep),
-                               self.grads, self.loss_acc, stream=s)
+            lane.view.backward(self.params, self.n, lane.img, ls, self.grads, self.loss_acc, stream=s)
         for lane in lanes:
             main.wait_stream(lane.stream)
         if self.host_targets:

@@ -48,6 +48,34 @@ class Run:
         return g, float(loss.item())
 
 
+def fused_grads(surfels, pose, intr, kind, trgb, tdep, w_rgb=1.0, w_depth=0.1, depth_mask=False,
+                cfg=DEFAULT_RASTER_CONFIG, image=False, view=None):
+    """Loss and gradients through s2d_forward_backward (one raster kernel for the losses
+    without the depth mask).  Returns (grads dict, loss, images dict or None, stats)."""
+    ctx = DeviceContext.get()
+    dev = ctx.device
+    view = view or View(ctx)
+    n = len(surfels)
+    params = pack_params(surfels, dev) if n else torch.zeros(13, device=dev)
+    grads = torch.zeros_like(params)
+    loss = torch.zeros(1, dtype=torch.float64, device=dev)
+    t = lambda a: torch.as_tensor(np.asarray(a, dtype=np.float32)).to(dev)  # noqa: E731
+    keep = [t(trgb), t(tdep)]
+    code = {"mse": N.LOSS_MSE, "l1": N.LOSS_L1}[kind]
+    ls = N.Loss(code, int(depth_mask), float(w_rgb), float(w_depth), N.dptr(keep[0]), N.dptr(keep[1]),
+                None, None, None, None)
+    img = ImageBuffers.allocate(intr.height, intr.width, dev, normal=False) if image else None
+    view.reserve_pairs(max(65536, 64 * n))
+    view.forward_backward(params, n, pose, camera_struct(intr), config_struct(cfg), img, ls, grads, loss)
+    torch.cuda.synchronize()
+    st = view.stats()
+    assert st.overflow == 0
+    g = {k: v.double().cpu().numpy() for k, v in unpack_params(grads, n).items()}
+    im = None if img is None else {k: getattr(img, k).double().cpu().numpy()
+                                   for k in ("color", "depth", "accumulation")}
+    return g, float(loss.item()), im, st
+
+
 def far_targets(ref_color, ref_depth, rng, gap=0.05):
     """Targets bounded away from the render (|C - C*| >= gap): L1 seeds have no sign ambiguity."""
     s = rng.choice([-1.0, 1.0], size=ref_color.shape)

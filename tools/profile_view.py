@@ -11,7 +11,8 @@ sc = scenes.config5(0) if os.environ.get("PROFILE_CONFIG", "4") == "5" else scen
 first = int(os.environ.get("PROFILE_FIRST", "12"))
 sc.poses = sc.poses[first:first + nviews]
 rgbs, deps = bench.render_targets(sc, torch.device("cuda", 0))
-ref = AdamRefiner(sc.extra["perturbed"], sc.intr, sc.poses, rgbs, deps, ViewLoss(), AdamConfig())
+ref = AdamRefiner(sc.extra["perturbed"], sc.intr, sc.poses, rgbs, deps, ViewLoss(), AdamConfig(),
+                  fused=os.environ.get("PROFILE_FUSED", "1") == "1")
 for _ in range(2):
     ref.step()
 torch.cuda.synchronize()
