@@ -489,7 +489,8 @@ def main():
                        "surfels": ref_n(sc),
                        "views": n_views, "image": [sc.intr.width, sc.intr.height],
                        "parallelism": f"view-sharded dp{world}",
-                       "l2": "working set per step > L2 (params+grads+moments 208 MB, targets 157 MB)",
+                       "l2": (f"working set per step > L2 (params+grads+moments {4 * 52 * ref_n(sc) / 1e6:.0f} MB, "
+                              f"targets {n_views * px * 16 / 1e6:.0f} MB)"),
                        "visible_last_view": nvis, "pairs_last_view": npairs, "blend_entries_last_view": nblend},
             "refine_iters_per_s": round(1000.0 / ms_step, 3),
             "fwd_bwd_mpix_per_s_per_view": round(px / (view_ms * 1e-3) / 1e6, 2) if view_ms > 0 else None,

@@ -555,11 +555,42 @@ __global__ void __launch_bounds__(256) k_tie_fix(const uint32_t *__restrict__ ke
 
 // ----------------------------------------------------------- scan + emission
 
+// The pairs of surfel j of this thread (bbox rc): calls f(tile key, k) for its k-th pair, k
+// counting from 0, in the reference's order (rows of tiles, then columns).
+template <typename F>
+__device__ __forceinline__ void for_each_pair(const short4 rc, int ntx, F &&f) {
+    if (!(rc.x <= rc.y && rc.z <= rc.w)) return;
+    const int tx0 = rc.x >> 4, tx1 = rc.y >> 4, ty0 = rc.z >> 4, ty1 = rc.w >> 4;
+    int k = 0;
+    for (int ty = ty0; ty <= ty1; ++ty) {
+        // rows of 4-pixel warp blocks the integer bbox overlaps (4 bits -> pairs of mask bits)
+        const int by = ty * kTile;
+        uint32_t rows = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (rc.z <= by + 4 * q + 3 && rc.w >= by + 4 * q) rows |= 3u << (2 * q);
+        for (int tx = tx0; tx <= tx1; ++tx) {
+            const int bx = tx * kTile;
+            const uint32_t cols = (rc.x <= bx + 7 && rc.y >= bx ? 0x55u : 0u) |
+                                  (rc.x <= bx + 15 && rc.y >= bx + 8 ? 0xAAu : 0u);
+            // key: tile | bbox-vs-warp-block mask << 16; the forward ORs the ellipse mask into
+            // bits 24-31 (raster.cu)
+            f((uint32_t)(ty * ntx + tx) | ((rows & cols) << 16), k++);
+        }
+    }
+}
+
+// Per-surfel tile counts scanned in depth order (decoupled look-back across CTAs) and the
+// pairs emitted at the scanned offsets.  While warp 0 looks back, the CTA builds its pairs in
+// shared memory at their CTA-local offsets (and counts the tile-id digit histograms); after the
+// barrier they are written out contiguously from the CTA's base (coalesced).  A CTA whose pairs
+// exceed the staging buffer (huge splats) writes them directly after the look-back.
 __global__ void S2D_EMIT_BOUNDS k_scan_emit(const EmitArgs a) {
     __shared__ int s_tile;
     __shared__ uint32_t s_w[8];
     __shared__ uint32_t s_base;
     __shared__ uint32_t s_hist[2 * kRadix];
+    __shared__ uint2 s_pairs[kEmitStage > 0 ? kEmitStage : 1];
     const int tid = threadIdx.x;
     const int nv = *a.d_v;
     // the grid is sized for the capacity: CTAs past the drawn surfels leave before the ticket
@@ -584,6 +615,8 @@ __global__ void S2D_EMIT_BOUNDS k_scan_emit(const EmitArgs a) {
     }
     uint32_t tot;
     const uint32_t ex = block_exclusive_scan_256(cnt, s_w, &tot);
+    const bool staged = kEmitStage > 0 && tot <= (uint32_t)kEmitStage;  // CTA-uniform
+    const bool two = a.pair_passes > 1;
     if (tid < 32) {
         const uint32_t pre = lookback_warp(a.status, tile, tot);
         const int ntiles = (nv + kEmitTile - 1) / kEmitTile;
@@ -595,37 +628,55 @@ __global__ void S2D_EMIT_BOUNDS k_scan_emit(const EmitArgs a) {
             if (total > a.pcap) a.stats->overflow = 1;
         }
     }
+    if (staged) {
+        uint32_t lo = ex;
+#pragma unroll
+        for (int j = 0; j < kEmitItems; ++j) {
+            const uint32_t id = ids[j];
+            for_each_pair(rc[j], a.ntx, [&](uint32_t key, int k) {
+                s_pairs[lo + k] = make_uint2(key, id);
+                const uint32_t t = key & 0xffffu;
+                atomicAdd(&s_hist[t & (kRadix - 1)], 1u);
+                if (two) atomicAdd(&s_hist[kRadix + ((t >> kRadixBits) & (kRadix - 1))], 1u);
+            });
+            lo += (rc[j].x <= rc[j].y && rc[j].z <= rc[j].w)
+                      ? (uint32_t)(((rc[j].y >> 4) - (rc[j].x >> 4) + 1) * ((rc[j].w >> 4) - (rc[j].z >> 4) + 1))
+                      : 0u;
+        }
+    }
     __syncthreads();
-    uint32_t off = s_base + ex;
+    const uint32_t base = s_base;
+    if (staged) {
+        for (uint32_t k = tid; k < tot; k += 256) {
+            const uint32_t off = base + k;
+            const uint2 pr = s_pairs[k];
+            if (off < a.pcap) {
+                a.pkeys[off] = pr.x;
+                a.pvals[off] = pr.y;
+            } else {
+                // the tile-id passes sort the stored pairs only (pairs_stored entries): their
+                // digit histograms must count exactly those, or an overflowing view's passes
+                // would place entries past the capacity
+                const uint32_t t = pr.x & 0xffffu;
+                atomicSub(&s_hist[t & (kRadix - 1)], 1u);
+                if (two) atomicSub(&s_hist[kRadix + ((t >> kRadixBits) & (kRadix - 1))], 1u);
+            }
+        }
+    } else {
+        uint32_t off = base + ex;
 #pragma unroll
-    for (int j = 0; j < kEmitItems; ++j) {
-        if (!(rc[j].x <= rc[j].y && rc[j].z <= rc[j].w)) continue;
-        const int tx0 = rc[j].x >> 4, tx1 = rc[j].y >> 4, ty0 = rc[j].z >> 4, ty1 = rc[j].w >> 4;
-        for (int ty = ty0; ty <= ty1; ++ty) {
-            // rows of 4-pixel warp blocks the integer bbox overlaps (4 bits -> pairs of mask bits)
-            const int by = ty * kTile;
-            uint32_t rows = 0;
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-                if (rc[j].z <= by + 4 * q + 3 && rc[j].w >= by + 4 * q) rows |= 3u << (2 * q);
-            for (int tx = tx0; tx <= tx1; ++tx) {
-                const int bx = tx * kTile;
-                const uint32_t cols = (rc[j].x <= bx + 7 && rc[j].y >= bx ? 0x55u : 0u) |
-                                      (rc[j].x <= bx + 15 && rc[j].y >= bx + 8 ? 0xAAu : 0u);
-                const uint32_t t = (uint32_t)(ty * a.ntx + tx);
+        for (int j = 0; j < kEmitItems; ++j) {
+            const uint32_t id = ids[j];
+            for_each_pair(rc[j], a.ntx, [&](uint32_t key, int) {
                 if (off < a.pcap) {
-                    // key: tile | bbox-vs-warp-block mask << 16; the forward ORs the ellipse
-                    // mask into bits 24-31 (raster.cu)
-                    a.pkeys[off] = t | ((rows & cols) << 16);
-                    a.pvals[off] = ids[j];
-                    // the tile-id passes sort the stored pairs only (pairs_stored entries): their
-                    // digit histograms must count exactly those, or an overflowing view's passes
-                    // would place entries past the capacity
+                    a.pkeys[off] = key;
+                    a.pvals[off] = id;
+                    const uint32_t t = key & 0xffffu;
                     atomicAdd(&s_hist[t & (kRadix - 1)], 1u);
-                    if (a.pair_passes > 1) atomicAdd(&s_hist[kRadix + ((t >> kRadixBits) & (kRadix - 1))], 1u);
+                    if (two) atomicAdd(&s_hist[kRadix + ((t >> kRadixBits) & (kRadix - 1))], 1u);
                 }
                 ++off;
-            }
+            });
         }
     }
     __syncthreads();

@@ -32,6 +32,10 @@ constexpr int kCompactTiles = 32;                // projection tiles per k_compa
 #endif
 constexpr int kEmitItems = S2D_EMIT_ITEMS;
 constexpr int kEmitTile = 256 * kEmitItems;
+#ifndef S2D_EMIT_STAGE
+#define S2D_EMIT_STAGE 4096
+#endif
+constexpr int kEmitStage = S2D_EMIT_STAGE;  // pairs a scan/emit CTA stages in shared memory (8 B each)
 
 // Zeroed-per-view scratch ("sync region"): look-back status words, tickets,
 // radix histograms, tile ranges, stats.  One memset per view.
