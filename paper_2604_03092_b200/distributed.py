@@ -124,12 +124,25 @@ def sharded_step(params: torch.Tensor, grads: torch.Tensor, state: ShardedOptimi
     every rank's slice back into every replica (in place under NCCL).  No staging copies: the
     same bytes over NVLink as the all-reduce it replaces, with the optimizer's HBM traffic and
     moment memory divided by the world size."""
-    dist.reduce_scatter_tensor(state.grads, grads, op=dist.ReduceOp.SUM, group=group)
+    # gloo has no device reduce-scatter / all-gather: device blocks go through host copies
+    # (the multi-rank tests on one GPU); NCCL moves them in place over NVLink
+    host = dist.get_backend(group) != "nccl" and grads.is_cuda
+    if host:
+        out = torch.empty(state.grads.shape, dtype=state.grads.dtype)
+        dist.reduce_scatter_tensor(out, grads.cpu(), op=dist.ReduceOp.SUM, group=group)
+        state.grads.copy_(out)
+    else:
+        dist.reduce_scatter_tensor(state.grads, grads, op=dist.ReduceOp.SUM, group=group)
     mine = state.slice(params)
     smask = state.mask if mask is None else state.shard_mask(mask)
     adam_fn(mine, state.grads, state.m1, state.m2, state.c, smask)
-    src = mine if dist.get_backend(group) == "nccl" else mine.clone()
-    dist.all_gather_into_tensor(params, src, group=group)
+    if host:
+        full = torch.empty(params.shape, dtype=params.dtype)
+        dist.all_gather_into_tensor(full, mine.cpu(), group=group)
+        params.copy_(full)
+    else:
+        src = mine if dist.get_backend(group) == "nccl" else mine.clone()
+        dist.all_gather_into_tensor(params, src, group=group)
 
 
 def init_from_env(backend: str = "nccl") -> tuple:
