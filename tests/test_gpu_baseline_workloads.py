@@ -15,7 +15,7 @@ import pytest
 import torch
 
 import oracle as O
-from gpu_helpers import Run, f32, gate, l1_oracle_grads
+from gpu_helpers import Run, f32, fused_grads, gate, l1_oracle_grads
 from paper_2604_03092_b200 import scenes
 from paper_2604_03092_b200.engine import unpack_params
 from paper_2604_03092_b200.mapper import AdamConfig, AdamRefiner, ViewLoss
@@ -100,6 +100,12 @@ def test_config5_exposure_gain_gradients():
         assert abs(loss - oloss) <= 1e-5 * abs(oloss)
         _gate_all(g, og, tag=f"view {v}")
         del run
+        torch.cuda.empty_cache()
+        # the one-kernel path the refine step runs (s2d_forward_backward), same oracle
+        gf, lossf, imf, _ = fused_grads(surf, pose, sc.intr, "l1", trgb, tdep, 1.0, 0.1, False, image=True)
+        assert np.array_equal(imf["color"], im["color"]) and np.array_equal(imf["depth"], im["depth"])
+        assert abs(lossf - oloss) <= 1e-5 * abs(oloss)
+        _gate_all(gf, og, tag=f"view {v} fused")
         torch.cuda.empty_cache()
 
 

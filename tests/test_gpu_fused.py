@@ -24,7 +24,13 @@ def _check_vs_oracle(s, pose, intr, kind, trgb, tdep, w_depth=0.1):
     oloss, og, _ = O.loss_and_grads(s, pose, intr, trgb, tdep, kind, 1.0, w_depth, mask_depth=False)
     assert abs(loss - oloss) <= 1e-5 * abs(oloss), (loss, oloss)
     for f in GROUPS:
-        ok, mx, l2 = gate(g[f], getattr(og, f))
+        ref = getattr(og, f)
+        if np.abs(ref).max() < 1e-15:
+            # analytically zero (e.g. the quaternion of an isotropic splat seen head-on, when no
+            # other surfel is on screen): float rounding noise on both sides, compared absolutely
+            assert np.abs(g[f]).max() < 1e-15, (kind, f, np.abs(g[f]).max())
+            continue
+        ok, mx, l2 = gate(g[f], ref)
         assert ok, (kind, f, mx, l2)
     return g, loss, im, st
 
@@ -178,3 +184,26 @@ def test_adam_refiner_fused_matches_two_kernel_trajectory():
     a, b = np.array(out[0]), np.array(out[1])
     assert np.all(np.abs(a - b) <= 1e-5 * np.abs(b)), (a, b)
     assert a[-1] < a[0]
+
+
+@pytest.mark.parametrize("n", [1, 257, 4097])
+def test_ragged_image_and_counts_with_huge_splat_fused(n):
+    """37x23 image (partial tiles at both edges), ragged surfel counts, one splat covering the
+    whole image, identity and rotated poses: the one-kernel path against the oracle."""
+    from paper_2604_03092_b200.geometry import Sim3Transform, UnitQuaternion
+    rng = np.random.default_rng(n)
+    intr = R.CameraIntrinsics(30.0, 30.0, 18.0, 11.0, 37, 23)
+    s = scenes.random_surfels(rng, n)
+    big = SurfelArrays(np.array([[0.0, 0.0, 1.5]]), np.array([[1.0, 0, 0, 0]]), np.array([[2.0, 2.0]]),
+                       np.array([0.3]), np.array([[0.2, 0.4, 0.6]]))
+    s = SurfelArrays.concatenate([s, big])
+    s = SurfelArrays(*[np.asarray(getattr(s, k), np.float32).astype(np.float64)
+                       for k in ("means", "quats", "scales", "opacities", "colors")])
+    for pose in (Sim3Transform.identity(), Sim3Transform(1.0, UnitQuaternion.from_axis_angle([0, 0, 1.0], 0.3),
+                                                         np.zeros(3))):
+        ref = O.render(s, pose, intr)
+        trgb, tdep = far_targets(ref.color, ref.depth, np.random.default_rng(n + 1))
+        _, _, im, _ = _check_vs_oracle(s, pose, intr, "l1", trgb, tdep)
+        for k in ("color", "depth", "accumulation"):
+            ok, mx, l2 = gate(im[k], getattr(ref, k))
+            assert ok, (k, mx, l2)
