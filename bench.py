@@ -134,6 +134,56 @@ def render_targets(sc, device):
     return rgbs, deps
 
 
+def small_config_rates(device, reps=20):
+    """fwd+bwd Mpix/s per view (projection -> sorts -> fused raster -> projection
+    backward, the refine step's per-view work, Adam excluded) for BASELINE configs 1-3, device
+    resident: the median of `reps` CUDA-event timed s2d_forward_backward calls per pose, over the
+    config's poses.  Targets: renders of the config's target map (config 2: its perturbed copy)."""
+    import numpy as np
+    import torch
+    from paper_2604_03092_b200 import _native as N
+    from paper_2604_03092_b200 import scenes
+    from paper_2604_03092_b200.engine import (DeviceContext, ImageBuffers, View, camera_struct, config_struct,
+                                              forward_checked, pack_params)
+    from paper_2604_03092_b200.rasterizer import DEFAULT_RASTER_CONFIG, loss_struct
+    out = {}
+    ctx = DeviceContext.get(device)
+    for name, sc in (("config1", scenes.config1(0)), ("config2", scenes.config2(0)), ("config3", scenes.config3(0))):
+        tgt = sc.extra.get("target_surfels")
+        rgbs, deps = render_targets(scenes.Scene(tgt if tgt is not None else sc.surfels, sc.intr, sc.poses),
+                                    ctx.device)
+        if tgt is None:  # configs 1, 3: the map's own render, recoloured (non-zero residuals)
+            rgbs = [r * 0.8 + 0.1 for r in rgbs]
+            deps = [d * 1.05 for d in deps]
+        view = View(ctx)
+        n = len(sc.surfels)
+        params = pack_params(sc.surfels, ctx.device)
+        grads = torch.zeros_like(params)
+        loss = torch.zeros(1, dtype=torch.float64, device=ctx.device)
+        cam, cfg = camera_struct(sc.intr), config_struct(DEFAULT_RASTER_CONFIG)
+        mx = 0
+        for pose in sc.poses:  # pair capacity for the largest view
+            img = ImageBuffers.allocate(sc.intr.height, sc.intr.width, ctx.device, normal=False)
+            mx = max(mx, forward_checked(view, params, n, pose, cam, cfg, img).pairs)
+        view.reserve_pairs(int(mx * 1.3) + 4096)
+        times = []
+        for v, pose in enumerate(sc.poses):
+            ls = loss_struct(N.LOSS_L1, 1.0, 0.1, False, rgbs[v], deps[v])
+            for r in range(reps + 3):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                view.forward_backward(params, n, pose, cam, cfg, None, ls, grads, loss)
+                e1.record()
+                torch.cuda.synchronize()
+                if r >= 3:
+                    times.append(e0.elapsed_time(e1))
+        ms = float(np.median(times))
+        px = sc.intr.width * sc.intr.height
+        out[name] = {"surfels": n, "image": [sc.intr.width, sc.intr.height], "poses": len(sc.poses),
+                     "ms_per_view": round(ms, 4), "mpix_per_s": round(px / (ms * 1e-3) / 1e6, 1)}
+    return out
+
+
 # algorithmic bytes per launch of each phase (DESIGN.md "Kernels, their bound and algorithmic
 # bytes"): every logical tensor access counted once.  n surfels, v visible, p (tile, surfel)
 # pairs, e blend-stream entries ((pair, 8x4 block) with >= 1 blended pixel), x pixels.
@@ -452,6 +502,11 @@ def main():
     h2d = ref2.h2d_bytes_per_step
     del ref2
 
+    # ---- configs 1-3 per-view fwd+bwd rates, rank 0 at N=1 ----
+    small = None
+    if rank == 0 and world == 1 and args.config == 4 and not args.small:
+        small = small_config_rates(dev)
+
     # ---- CPU baseline (rank 0, N=1 only) ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -509,6 +564,7 @@ def main():
                               "achieved_gbs": round(view_bytes / (view_ms * 1e-3) / 1e9, 1) if view_ms > 0 else None,
                               "frac": round(view_bytes / (view_ms * 1e-3) / 1e9 / hbm, 4) if view_ms > 0 else None},
             "phases_per_view": phases,
+            "other_configs_per_view": small,
             "e2e": {"value": round(e2e_value, 3), "unit": "Mpix/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": 8 + 32, "ms_per_step": round(e2e_ms_step, 4)},
             "gpu_launches": int(launches),
