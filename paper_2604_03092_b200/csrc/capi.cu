@@ -5,6 +5,7 @@
 //   -> k_tie_fix -> k_scan_emit -> 1..2 x k_onesweep (tile id) -> k_tile_ranges
 //   -> k_raster_fwd                       [s2d_forward]
 //   -> k_raster_bwd -> k_project_bwd      [s2d_backward]
+//   or, after the tile ranges, k_raster_fused -> k_project_bwd   [s2d_forward_backward]
 //
 // Every count (visible surfels V, pairs P) stays on the device; kernels read it
 // there, so a view is a fixed launch sequence with no host round trip (CUDA-graph

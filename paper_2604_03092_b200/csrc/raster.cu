@@ -17,12 +17,17 @@
 // every slot its pixels blended the warp appends (surfel, lane mask of the pixels that blended
 // it, lane mask of those whose weight clamped) to its blend stream.
 //
-// Backward (k_raster_bwd): each warp walks its blend stream newest first and runs the
-// reverse recurrence (transmittance recovered by division, normalised suffix
-// S <- w c + (1 - w) S) on exactly the forward's blended set.  Every lane runs every entry
-// (branch-free: lanes outside the entry's mask take w = 0, which leaves their state unchanged
-// and zeroes their values); the per-entry 2D gradients of two entries are reduced over the
-// warp together (transposed butterfly) and added with one atomic per value.
+// Backward (k_raster_bwd): each warp walks its blend streams newest first — one per column
+// half of its block, the halves in step, one entry each per step — and runs the reverse
+// recurrence (transmittance recovered by division, normalised suffix S <- w c + (1 - w) S) on
+// exactly the forward's blended set.  Every lane of a half runs the half's entry (branch-free:
+// lanes outside the entry's mask take w = 0, which leaves their state unchanged and zeroes
+// their values); each half reduces its entry's 2D gradients over its 16 lanes (transposed
+// butterfly) and adds them with one atomic per value.
+//
+// Fused (k_raster_fused, the refine step's losses without the depth mask): both, per warp
+// block — the forward, the loss seeds from the lanes' registers, then the backward traversal
+// of the streams just written (still in L2), in one kernel.
 //
 // Semantics follow blend_forward (_raster_kernels.py:22-55) exactly: the termination test
 // precedes blending, pixel (row y, col x) samples (x, y), the Mahalanobis cut is
