@@ -107,6 +107,8 @@ typedef struct s2d_view_debug {
     int64_t pair_capacity;
     int32_t drawn; /* length of `order` (copied to the host by s2d_view_inspect; synchronous) */
     int32_t reserved;
+    const int32_t *stream_lengths; /* (ntiles, 8, 2) blend-stream entries per (tile, 8x4 warp block,
+                                      column half): the backward's work list lengths */
 } s2d_view_debug;
 
 /* Loss definition for the backward pass (seeds fused into the backward kernel) */

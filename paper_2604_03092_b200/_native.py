@@ -64,7 +64,8 @@ class ViewDebug(ctypes.Structure):
     _fields_ = [("order", c_p), ("pair_tiles", c_p), ("pair_ids", c_p), ("ranges", c_p),
                 ("bbox", c_p), ("z", c_p), ("flags", c_p), ("records", c_p),
                 ("pixel_state", c_p), ("ntiles", ctypes.c_int32), ("tiles_x", ctypes.c_int32),
-                ("pair_capacity", ctypes.c_int64), ("drawn", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("pair_capacity", ctypes.c_int64), ("drawn", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("stream_lengths", c_p)]
 
 
 class Loss(ctypes.Structure):

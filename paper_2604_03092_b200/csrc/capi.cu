@@ -786,6 +786,7 @@ int s2d_view_inspect(s2d_view *v, s2d_view_debug *out) {
     out->ntiles = v->P.ntx * v->P.nty;
     out->tiles_x = v->P.ntx;
     out->pair_capacity = v->pcap;
+    out->stream_lengths = v->bcount;
     return S2D_OK;
 }
 

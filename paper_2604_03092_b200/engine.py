@@ -241,6 +241,7 @@ class View:
             "flags": _wrap(d.flags, (n,), "|u1", dev).clone() if n else torch.zeros(0, dtype=torch.uint8),
             "records": _wrap(d.records, (n, 16), "<f4", dev).clone() if n else torch.zeros((0, 16)),
             "pixel_state": _wrap(d.pixel_state, (h * w, 2), "<i4", dev).clone(),
+            "stream_lengths": _wrap(d.stream_lengths, (d.ntiles, 8, 2), "<i4", dev).clone(),
             "tiles_x": d.tiles_x,
             "stats": st,
         }
