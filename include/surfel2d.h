@@ -216,7 +216,9 @@ int s2d_backward(s2d_view *view, void *stream, const float *params, int64_t n,
  * (cudaEvent_t, nullable) is waited for before the loss targets are read, e.g. their
  * upload.  Any other loss falls back to s2d_forward + s2d_backward with `out`, which must
  * then be complete.  ACCUMULATES into grads like s2d_backward.  The view's forward state is
- * consumed: run s2d_forward again before an s2d_backward.
+ * consumed: run s2d_forward again before an s2d_backward.  On the one-kernel path the view's
+ * stats.n_mask is the float32 count of accumulation > 0.5 (no loss on that path reads it; the
+ * depth-mask losses re-decide it in float64, as s2d_backward does).
  */
 int s2d_forward_backward(s2d_view *view, void *stream, const float *params, int64_t n,
                          const double pose_c2w[8], const s2d_camera *cam, const s2d_raster_config *cfg,

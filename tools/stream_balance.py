@@ -23,5 +23,7 @@ for v in (0, 12, 31):
     n0, n1 = sl[..., 0], sl[..., 1]
     e = int((n0 + n1).sum()); steps = int(torch.maximum(n0, n1).sum())
     both = int(((n0 > 0) & (n1 > 0)).sum()); blocks = int(((n0 + n1) > 0).sum())
+    nb = int((d["pixel_state"][:, 0] & ((1 << 29) - 1)).long().sum())
+    print(f"view {v}: blended (pixel, surfel) pairs {nb}, lanes used per half-entry {nb / e:.2f} of 16")
     print(f"view {v}: entries {e}, warp steps {steps}, slot use {e / (2 * steps):.3f}, "
           f"blocks with work {blocks}, both halves {both}, mean |n0-n1| {float((n0 - n1).abs().float().mean()):.1f}")
