@@ -69,6 +69,12 @@ def test_c_abi_rejects_bad_arguments_without_gpu():
     assert b"NULL" in L.s2d_last_error()
     cfgA = N.AdamCfg(1e-3, 5e-3, 0.9, 0.999, 1e-8, 1e-7)
     assert L.s2d_adam_step(None, None, None, None, None, 10, 0, ctypes.byref(cfgA), None) == N.S2D_ERR_INVALID
+    # s2d_forward_backward: no view / no loss / no gradient block
+    loss = N.Loss(N.LOSS_L1, 0, 1.0, 0.1, None, None, None, None, None, None)
+    pose = N.as_doubles([1, 0, 0, 0, 1, 0, 0, 0])
+    assert L.s2d_forward_backward(None, None, None, 0, pose, ctypes.byref(cam), ctypes.byref(cfg), None,
+                                  ctypes.byref(loss), None, None, None) == N.S2D_ERR_INVALID
+    assert b"NULL" in L.s2d_last_error()
 
 
 def test_intrinsics_and_surfel_validation():
