@@ -109,6 +109,9 @@ typedef struct s2d_view_debug {
     int32_t reserved;
     const int32_t *stream_lengths; /* (ntiles, 8, 2) blend-stream entries per (tile, 8x4 warp block,
                                       column half): the backward's work list lengths */
+    const uint32_t *streams;       /* blend streams, 4 words per entry (surfel, blend lane mask, clamp
+                                      lane mask, flags); half h of block w of tile t starts at entry
+                                      16 ranges[t].start + (2 w + h) (ranges[t].end - ranges[t].start) */
 } s2d_view_debug;
 
 /* Loss definition for the backward pass (seeds fused into the backward kernel) */

@@ -65,7 +65,7 @@ class ViewDebug(ctypes.Structure):
                 ("bbox", c_p), ("z", c_p), ("flags", c_p), ("records", c_p),
                 ("pixel_state", c_p), ("ntiles", ctypes.c_int32), ("tiles_x", ctypes.c_int32),
                 ("pair_capacity", ctypes.c_int64), ("drawn", ctypes.c_int32), ("reserved", ctypes.c_int32),
-                ("stream_lengths", c_p)]
+                ("stream_lengths", c_p), ("streams", c_p)]
 
 
 class Loss(ctypes.Structure):

@@ -787,6 +787,7 @@ int s2d_view_inspect(s2d_view *v, s2d_view_debug *out) {
     out->tiles_x = v->P.ntx;
     out->pair_capacity = v->pcap;
     out->stream_lengths = v->bcount;
+    out->streams = reinterpret_cast<const uint32_t *>(v->bstream);
     return S2D_OK;
 }
 

@@ -242,6 +242,7 @@ class View:
             "records": _wrap(d.records, (n, 16), "<f4", dev).clone() if n else torch.zeros((0, 16)),
             "pixel_state": _wrap(d.pixel_state, (h * w, 2), "<i4", dev).clone(),
             "stream_lengths": _wrap(d.stream_lengths, (d.ntiles, 8, 2), "<i4", dev).clone(),
+            "streams": _wrap(d.streams, (16 * p, 4), "<i4", dev).clone() if p else None,
             "tiles_x": d.tiles_x,
             "stats": st,
         }
