@@ -196,7 +196,7 @@ def phase_bytes(n, v, p, x, e):
         "raster_bwd": 16 * e + 64 * p + 40 * x + 40 * v,  # stream + records; aux, render, targets; 2D gradients
         # forward + backward in one kernel: both minus the image round trip (targets in only)
         "raster_fused": 136 * p + 32 * e + 16 * x + 40 * v,
-        "project_bwd": n + 260 * v,                 # flags; 2D grads in + zeroed; params in; gradients r+w
+        "project_bwd": n + 228 * v,                 # flags; 2D grad rows (48 B) in + zeroed; params in; gradients r+w
     }
 
 

@@ -473,6 +473,7 @@ int view_forward(s2d_view *v, cudaStream_t s, const float *params, int64_t n, co
             pb.flags = v->flags;
             pb.rect = v->rect;
             pb.grad2d = v->grad2d;
+            pb.g2_stride = g2_stride(P.mode == S2D_SPLAT_RAY, false);  // k_raster_fused: no external seeds
             pb.grads = fl->grads;
             launch_project_backward(pb, s);
             S2D_CHECK_LAUNCH();
@@ -699,6 +700,9 @@ int s2d_backward(s2d_view *v, void *stream, const float *params, int64_t n, cons
         pb.flags = v->flags;
         pb.rect = v->rect;
         pb.grad2d = v->grad2d;
+        // the row width launch_raster_backward's kernel wrote (k_raster_bwd<kExt, kRay>)
+        const bool ext = loss->kind == S2D_LOSS_EXTERNAL && (loss->d_normal != nullptr || loss->d_accumulation != nullptr);
+        pb.g2_stride = g2_stride(v->P.mode == S2D_SPLAT_RAY, ext);
         pb.grads = grads;
         launch_project_backward(pb, s);
     }

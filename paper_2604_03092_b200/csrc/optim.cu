@@ -56,8 +56,11 @@ __global__ void S2D_PBWD_BOUNDS k_project_bwd(const ProjectBwdArgs a) {
     if (!(fl & 8)) return;  // not drawn: no pixel, no 2D gradient
     // all independent loads are issued up front (one exposed memory latency); stores at the end
     const int64_t n = P.n;
-    const float4 *__restrict__ g4 = reinterpret_cast<const float4 *>(a.grad2d + (size_t)i * 16);
-    const float4 G0 = g4[0], G1 = g4[1], G2 = g4[2], G3 = g4[3];
+    // the raster backward's row of this surfel: 12 floats (affine, no normal seeds) or 16
+    const bool wide = a.g2_stride == 16;
+    const float4 *__restrict__ g4 = reinterpret_cast<const float4 *>(a.grad2d + (size_t)i * a.g2_stride);
+    const float4 G0 = g4[0], G1 = g4[1], G2 = g4[2];
+    const float4 G3 = wide ? g4[3] : make_float4(0.f, 0.f, 0.f, 0.f);
 
     // Geometry for the chain rule: plain float64 (contractions allowed) — only the forward's
     // decisions need the reference's exact arithmetic.
@@ -232,12 +235,12 @@ __global__ void S2D_PBWD_BOUNDS k_project_bwd(const ProjectBwdArgs a) {
     atomicAdd(gout.colors + 1, G0.z);
     atomicAdd(gout.colors + 2, G0.w);
     // leave the per-view 2D gradient buffer zeroed for the next view
-    float4 *zero = reinterpret_cast<float4 *>(a.grad2d + (size_t)i * 16);
+    float4 *zero = reinterpret_cast<float4 *>(a.grad2d + (size_t)i * a.g2_stride);
     const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
     zero[0] = z4;
     zero[1] = z4;
     zero[2] = z4;
-    zero[3] = z4;
+    if (wide) zero[3] = z4;
 }
 
 struct AdamK {

@@ -886,6 +886,7 @@ __device__ __forceinline__ void bwd_traverse(const RasterArgs &a, WarpRing &ring
     float *gcol[RF];  // this lane's gradient columns (where it owns a sum)
 #pragma unroll
     for (int t = 0; t < RF; ++t) gcol[t] = a.grad2d + vi[t];
+    constexpr int kG2 = g2_stride(kRay, kExt);  // floats per surfel row of grad2d
     float R = 1.f;     // prod_{j later} (1 - w_j)
     // suffixes (S_r, S_g), (S_b, S_depth) as register pairs for the packed FFMA2
     float2 S01 = make_float2(0.f, 0.f), S2d = make_float2(0.f, 0.f);
@@ -1050,7 +1051,7 @@ __device__ __forceinline__ void bwd_traverse(const RasterArgs &a, WarpRing &ring
                 const uint32_t id = entry(act ? 2 * st + half : kidle, act, 0, acc_t);
                 red_stage<NV, red_first(kMode), kMode>(v, lane);
 #pragma unroll
-                for (int t = 0; t < RF; ++t) red_add_if(gcol[t] + (size_t)id * 16, v[t], own[t] && act);
+                for (int t = 0; t < RF; ++t) red_add_if(gcol[t] + (size_t)id * kG2, v[t], own[t] && act);
             }
         };
         if (!kRay && chunk_acc) run_steps(std::integral_constant<bool, !kRay>{});

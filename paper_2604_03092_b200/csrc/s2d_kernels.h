@@ -134,7 +134,7 @@ struct RasterArgs {
     double w_rgb, w_depth;
     const float *target_rgb, *target_depth;
     const float *d_color, *d_depth, *d_normal, *d_accum;
-    float *grad2d;  // [n][16] per-view 2D gradients (layout in raster.cu, k_raster_bwd)
+    float *grad2d;  // [n][16] per-view 2D gradients, rows of g2_stride(ray, ext) floats (raster.cu)
     double *loss_accum;
     // pixels whose float32 depth-mask decision is within the error band (k_mask_fixup)
     int *amb_count;  // sync region (zeroed per view)
@@ -155,7 +155,11 @@ struct ProjectBwdArgs {
     const short4 *rect;  // per-surfel bbox (ray mode: reference corner of the 2D gradients)
     float *grad2d;
     float *grads;
+    int g2_stride;  // floats per surfel in grad2d, as the raster backward wrote them (g2_stride())
 };
+// Floats per surfel of the 2D-gradient rows: the affine mode's 10 values (+ 3 normal values
+// with external normal / accumulation seeds, 13 in ray mode, 16 with both) in rows of 12 or 16.
+constexpr int g2_stride(bool ray, bool ext) { return (ray || ext) ? 16 : 12; }
 void launch_project_backward(const ProjectBwdArgs &a, cudaStream_t s);
 
 // skip (device, nullable): the step is a no-op when *skip != 0 (a view of it overflowed)
