@@ -77,3 +77,58 @@ def test_random_scene_parity(seed):
     oloss, og, _ = O.loss_and_grads(s, pose, intr, trgb, tdep, "mse", 1.0, 0.1, mask_depth=True, cfg=cfg)
     assert abs(loss - oloss) <= 1e-5 * abs(oloss), (seed, loss, oloss)
     _gate_groups(g, og, (seed, "mse"))
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_random_scene_ray_mode(seed):
+    """Ray-splat mode (no reference counterpart): random scenes at footprint_sigma = 6 (the cut
+    at a weight of ~1e-8, so float32 cut decisions are invisible at the gate) against the
+    float64 PyTorch oracle, images and L1 gradients by autograd through the one-kernel path."""
+    import torch
+    import oracle.raysplat as RS
+    s, pose, intr, _ = _case(seed)
+    n = len(s)
+    keep = np.arange(min(n, 250))
+    s = s.select(keep)
+    cfg = RasterConfig(splat_mode="ray", footprint_sigma=6.0)
+    pr = RS.params_from_arrays(s)
+    ref = RS.render_ray(pr, pose, intr, cfg)
+    buf = R.render(s, pose, intr, cfg)
+    for k in ("color", "depth", "accumulation"):
+        ok, mx, l2 = gate(getattr(buf, k), ref[k].detach().numpy())
+        assert ok, (seed, k, mx, l2)
+    trgb, tdep = far_targets(ref["color"].detach().numpy(), ref["depth"].detach().numpy(),
+                             np.random.default_rng(seed))
+    g, loss, _, _ = fused_grads(s, pose, intr, "l1", trgb, tdep, 1.0, 0.1, False, cfg=cfg)
+    npx = intr.width * intr.height
+    L = ((ref["color"] - torch.as_tensor(trgb)).abs().sum() / (3 * npx)
+         + 0.1 * (ref["depth"] - torch.as_tensor(tdep)).abs().sum() / npx)
+    L.backward()
+    assert abs(loss - L.item()) <= 1e-5 * abs(L.item()), (seed, loss, L.item())
+    for f in GROUPS:
+        gr = pr[f].grad.numpy()
+        if np.abs(gr).max() < 1e-15:
+            assert np.abs(g[f]).max() < 1e-12, (seed, f)
+            continue
+        ok, mx, l2 = gate(g[f], gr)
+        assert ok, (seed, f, mx, l2)
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_random_scene_exact_depth_ties(seed):
+    """Depths quantised to a few levels (camera z equal across many surfels: identity pose or a
+    roll about the optical axis): the (z, index) order and tile lists stay bit-exact."""
+    from test_gpu_parity import check_binning
+    s, _, intr, cfg = _case(seed)
+    rng = np.random.default_rng(seed)
+    m = np.asarray(s.means, np.float64).copy()
+    m[:, 2] = np.round(m[:, 2] / 0.25) * 0.25
+    s = SurfelArrays(scenes.f32(m), s.quats, s.scales, s.opacities, s.colors)
+    pose = Sim3Transform(1.0, UnitQuaternion.from_axis_angle([0.0, 0.0, 1.0], float(rng.uniform(-0.5, 0.5))),
+                         np.zeros(3))
+    run = Run(s, pose, intr, cfg=cfg, normal=False, argmax=False)
+    proj = O.project(s, pose, intr, cfg)
+    check_binning(run, proj, O.depth_order(proj), intr)
+    ref = O.render(s, pose, intr, cfg)
+    ok, mx, l2 = gate(run.images()["color"], ref.color)
+    assert ok, (seed, mx, l2)
