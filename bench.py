@@ -166,7 +166,8 @@ def small_config_rates(device, reps=20):
             img = ImageBuffers.allocate(sc.intr.height, sc.intr.width, ctx.device, normal=False)
             mx = max(mx, forward_checked(view, params, n, pose, cam, cfg, img).pairs)
         view.reserve_pairs(int(mx * 1.3) + 4096)
-        times = []
+        times, gtimes = [], []
+        side = torch.cuda.Stream(ctx.device)
         for v, pose in enumerate(sc.poses):
             ls = loss_struct(N.LOSS_L1, 1.0, 0.1, False, rgbs[v], deps[v])
             for r in range(reps + 3):
@@ -177,10 +178,26 @@ def small_config_rates(device, reps=20):
                 torch.cuda.synchronize()
                 if r >= 3:
                     times.append(e0.elapsed_time(e1))
-        ms = float(np.median(times))
+            # the same view as one CUDA-graph launch (how a training loop issues it)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(side):
+                with torch.cuda.graph(g, stream=side):
+                    view.forward_backward(params, n, pose, cam, cfg, None, ls, grads, loss, stream=side)
+            torch.cuda.synchronize()
+            for r in range(reps + 3):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                g.replay()
+                e1.record()
+                torch.cuda.synchronize()
+                if r >= 3:
+                    gtimes.append(e0.elapsed_time(e1))
+            del g
+        ms, gms = float(np.median(times)), float(np.median(gtimes))
         px = sc.intr.width * sc.intr.height
         out[name] = {"surfels": n, "image": [sc.intr.width, sc.intr.height], "poses": len(sc.poses),
-                     "ms_per_view": round(ms, 4), "mpix_per_s": round(px / (ms * 1e-3) / 1e6, 1)}
+                     "ms_per_view": round(ms, 4), "mpix_per_s": round(px / (ms * 1e-3) / 1e6, 1),
+                     "graph_ms_per_view": round(gms, 4), "graph_mpix_per_s": round(px / (gms * 1e-3) / 1e6, 1)}
     return out
 
 
