@@ -382,8 +382,9 @@ class AdamRefiner:
 
     ``targets_rgb[v]`` (H,W,3) / ``targets_depth[v]`` (H,W) may be numpy arrays, device
     tensors, or (``host_targets=True``) host tensors that are pinned and copied in every
-    step on a copy stream, each view's backward waiting for its own copy (the end-to-end
-    path: the transfers overlap the forwards and the other views' compute).
+    step on a copy stream, each view's first reader of them (the fused raster kernel, or the
+    backward) waiting for its own copy (the end-to-end path: the transfers overlap the
+    projections, sorts and the other views' compute).
     ``inflight`` views run concurrently on separate streams.
 
     ``step(sync=False)`` queues an iteration without a host round trip: the Adam step is
@@ -453,8 +454,9 @@ class AdamRefiner:
                     "s2d_view_set_layout")
         if host_targets:
             # end-to-end path: every view's targets go up on a copy stream at the start of the
-            # step, into per-view device buffers; a view's backward (the only reader) waits
-            # for its own copy, so the transfers overlap the forwards and the other views
+            # step, into per-view device buffers; a view's raster kernel (the fused path) or
+            # backward, the only reader, waits for its own copy, so the transfers overlap the
+            # projections, sorts and the other views
             self.copy_stream = torch.cuda.Stream(self.dev)
             self.dev_rgb = {v: torch.empty((h, w, 3), device=self.dev) for v in self.my_views}
             self.dev_depth = {v: torch.empty((h, w), device=self.dev) for v in self.my_views}
