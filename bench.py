@@ -538,7 +538,8 @@ def main():
         except Exception as e:  # pragma: no cover - the oracle library missing on the box
             secs = float("nan")
             print(f"cpu port failed: {type(e).__name__}: {e}", file=sys.stderr)
-        port = {"value": nv * px / secs / 1e6, "unit": "Mpix/s", "cores": min(threads, nv), "kind": "port",
+        port = {"value": nv * px / secs / 1e6 if secs == secs else None, "unit": "Mpix/s",
+                "cores": min(threads, nv), "kind": "port",
                 "sample": f"{nv} config-4 views fwd+bwd in {secs:.1f}s (float64 C port of the reference path, oracle/)"}
         # the reference's own numba path (baseline/_ref): fwd + colour/opacity backward only (it
         # has no geometry gradients), one view per process; 1 core and a view-parallel pool
