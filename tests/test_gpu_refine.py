@@ -140,6 +140,22 @@ def test_host_target_path_matches_device_path():
     assert float(d.max()) <= 3 * 2 * 5e-3
 
 
+def test_host_target_path_with_cuda_graph():
+    """The bench's end-to-end configuration: host targets uploaded on the copy stream inside a
+    captured step, each view's fused raster kernel waiting on its own upload event, queued
+    steps; the losses follow the device-target run."""
+    sc, rgbs, deps = _c4_small(2, 4)
+    a = AdamRefiner(sc.extra["perturbed"], sc.intr, sc.poses, rgbs, deps, inflight=2)
+    b = AdamRefiner(sc.extra["perturbed"], sc.intr, sc.poses, [r.cpu() for r in rgbs], [d.cpu() for d in deps],
+                    host_targets=True, inflight=2, cuda_graph=True)
+    assert b.fused
+    la = [a.step() for _ in range(4)]
+    for _ in range(4):
+        b.step(sync=False)
+    lb = b.losses()
+    assert np.allclose(la, lb, rtol=1e-5), (la, lb)
+
+
 def test_sharded_optimizer_path_on_nccl_world_of_one():
     """The N > 1 optimizer path (reduce-scatter -> fused Adam on the shard -> all-gather) run
     through NCCL on a one-rank group equals the replicated path (up to the order of the
